@@ -1,0 +1,196 @@
+/*
+ * nndtw.h -- C ABI of libnndtw.so: exact 1-NN search under windowed DTW pruned by the
+ * LB_Kim -> LB_Enhanced^V cascade of arxiv 1808.09617, as hand-written CUDA for sm_100a (B200).
+ *
+ * Citations: "P:<line>" = PAPER.md line (section / equation / algorithm given alongside),
+ * "Cn" = reading n of DESIGN.md ("Readings of the paper").
+ *
+ * Conventions (all entry points):
+ *  - Every float/int array argument is a DEVICE pointer unless marked "host".  Arrays are
+ *    caller-owned, row-major and contiguous; series are float32 [n][L].  The library never
+ *    allocates device memory, never frees or retains a caller pointer past the call; scratch
+ *    comes from the caller's `ws` (size from the matching *_workspace_bytes function).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Calls are
+ *    asynchronous on `stream` unless stated; a call that fills a host-side nndtw_stats
+ *    synchronises `stream` before returning.
+ *  - Distances are SQUARED (the accumulated cost D(L,L) of Eq. 1); DTW itself is
+ *    its square root (Eq. 2).  delta(a,b) = (a-b)^2 (reading C1).
+ *  - The window w is absolute (reading C4 resolves fractions); w >= L-1 is clamped to L-1,
+ *    which is unconstrained DTW (reading C3).  w = 0 is the squared Euclidean distance.
+ *  - Return value: NNDTW_OK or an NNDTW_E_* code; nndtw_last_error() gives a thread-local
+ *    message.  No C++ exception crosses the ABI.  Inputs must be finite (the Python layer
+ *    checks; NaN would silently be dropped by fminf).
+ */
+#ifndef NNDTW_H
+#define NNDTW_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define NNDTW_API __attribute__((visibility("default")))
+#else
+#define NNDTW_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NNDTW_OK 0
+#define NNDTW_E_ARG 1        /* null pointer, negative count, misaligned pointer */
+#define NNDTW_E_LENGTH 2     /* L < 2 (Algorithm 1 is not admissible at L = 1, reading C11) */
+#define NNDTW_E_WINDOW 3     /* w < 0 */
+#define NNDTW_E_V 4          /* V < 1 */
+#define NNDTW_E_WORKSPACE 5  /* ws too small */
+#define NNDTW_E_CUDA 6       /* a CUDA runtime error (message has the name) */
+#define NNDTW_E_ARCH 7       /* the current device is not sm_100 */
+#define NNDTW_E_INDEX 8      /* a global train index does not fit in 32 bits */
+
+/* Per-series LB_Kim features (sum variant P:619-621, reading C7):
+ * min / max value and their lowest indices (ties -> lowest index).  First and last values are
+ * read from the series itself.  16 bytes, naturally aligned. */
+typedef struct {
+    float vmin, vmax;
+    int32_t imin, imax;
+} nndtw_kim;
+
+/* Host-side counters, filled (after a stream synchronisation) when a non-NULL pointer is
+ * passed.  All counts are exact integers. */
+typedef struct {
+    int64_t lb_pairs;       /* (query, train) pairs whose cascade bound was computed */
+    int64_t survivors;      /* pairs with LB <= bsf*(1+eps_p) after the seed round */
+    int64_t dtw_calls;      /* DTW work items started (seeds + survivors) */
+    int64_t dtw_abandoned;  /* items stopped by early abandoning */
+    int64_t cells;          /* in-band DP cells on the diagonals actually processed */
+    int64_t near_tie_pairs; /* pairs re-ranked in fp64 (reading C16) */
+    int32_t rounds;         /* DTW rounds run (seed round included) */
+    int32_t launches;       /* kernel launches issued by the call */
+    float ms_envelopes, ms_lb, ms_dtw, ms_other; /* CUDA-event stage times (stats != NULL) */
+} nndtw_stats;
+
+/* Library identity and introspection. */
+NNDTW_API const char *nndtw_last_error(void);
+NNDTW_API int nndtw_version(void);
+/* Number of kernels this library has launched in the process so far (bench bookkeeping). */
+NNDTW_API int64_t nndtw_launch_count(void);
+/* NNDTW_OK if the current device is sm_100 (B200); NNDTW_E_ARCH otherwise. */
+NNDTW_API int nndtw_check_device(void);
+/* *bad (device int32, caller-zeroed) is set to 1 if x [n] holds a NaN or infinity. */
+NNDTW_API int nndtw_check_finite(const float *x, int64_t n, int32_t *bad, void *stream);
+
+/*
+ * S1 -- envelopes, Eq. 3-4:
+ *   upper[i][k] = max_{max(0,k-w) <= j <= min(L-1,k+w)} x[i][j],  lower = min over the same.
+ * x: [n][L]; upper, lower: [n][L] outputs (bit-exact: min/max of floats are exact).
+ * kim: [n] output, nullable: the LB_Kim features of each series (nndtw_kim).
+ * Precomputed "at training time".  Errors: E_ARG, E_LENGTH (L < 1), E_WINDOW.
+ */
+NNDTW_API int nndtw_envelopes(const float *x, int64_t n, int32_t L, int32_t w, float *upper,
+                    float *lower, nndtw_kim *kim, void *stream);
+
+/* LB_Kim features only (query side): kim[i] for x [n][L]. */
+NNDTW_API int nndtw_series_stats(const float *x, int64_t n, int32_t L, nndtw_kim *kim, void *stream);
+
+/*
+ * S2 -- batched cascade bound over all (query, train) pairs:
+ *   lb[i*ldlb + j] = LB_Enhanced^V_W(q_i, t_j)                   (flags & 1 == 0)
+ *                  = max(LB_Kim_sum(q_i,t_j), LB_Enhanced^V_W)     (flags & NNDTW_LB_WITH_KIM)
+ * LB_Enhanced is Eq. 7 computed as Algorithm 1 without the line-12
+ * abort (the bound is wanted for every pair): boundary terms, n_bands = min(floor(L/2), V)
+ * left/right bands (readings C8-C10) and the LB_Keogh bridge over
+ * columns n_bands+1 .. L-n_bands against t_j's envelopes.
+ * q: [nq][L]; t, upper, lower: [nt][L]; qkim: [nq], tkim: [nt] (both required with WITH_KIM,
+ * else nullable); lb: [nq][ldlb], ldlb >= nt.  fp32 arithmetic.
+ */
+#define NNDTW_LB_WITH_KIM 1u
+NNDTW_API int nndtw_lb_enhanced(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
+                      const float *upper, const float *lower, const nndtw_kim *tkim,
+                      int64_t nt, int32_t L, int32_t w, int32_t v, uint32_t flags, float *lb,
+                      int64_t ldlb, void *stream);
+
+/*
+ * S4 -- batched windowed DTW, Eq. 1 inside |i-j| <= w, with early
+ * abandoning.  Pair p compares a[ia[p]] with b[ib[p]] (ia/ib nullable = p).
+ * cutoff: [npairs] squared cutoffs, nullable (= +inf).  out[p] = squared DTW in fp32, or +inf
+ * when abandoned; abandoning happens only when the minimum over a cut of the DP (two
+ * consecutive anti-diagonals, reading C14) exceeds cutoff*(1+(4L+8)*2^-24), which guarantees
+ * the exact value exceeds cutoff.  a: [*][L], b: [*][L].
+ */
+NNDTW_API int nndtw_dtw_batch(const float *a, const float *b, const int32_t *ia, const int32_t *ib,
+                    int64_t npairs, int32_t L, int32_t w, const float *cutoff, float *out,
+                    void *stream);
+
+/*
+ * S2-S7 -- 1-NN search of every query against one train shard.
+ * Key format: key[i] = (float bits of the squared distance << 32) | global train index;
+ * global index = index_base + local index (< 2^32).  Non-negative floats order like their
+ * bits, so an unsigned (or signed int64: bit 63 is 0) MIN over keys gives the smallest
+ * distance with ties to the lowest index (reading C13) -- the shard combine of S6.
+ * Stages: LB cascade for all pairs (S2); seed = DTW to the argmin-LB candidate (S3); prune
+ * pairs with LB > bsf*(1+eps_p), eps_p = (3L+8)*2^-24 (reading C16); DTW with early abandon
+ * against the live per-query best on the survivors, atomicMin on the key (S4/S5).
+ * flags & NNDTW_CLASSIFY_EXACT: also run the fp64 near-tie re-rank locally (S7; only valid
+ * for a single shard) so that key is final: the candidate chosen is the one the fp64 oracle
+ * chooses, its fp32 distance in the high half.
+ * Without EXACT the caller combines shards with MIN over keys, then calls
+ * nndtw_classify_refine and nndtw_classify_resolve with the same ws (see dist.py).
+ * q: [nq][L]; t, upper, lower: [nt][L]; tkim: [nt] (from nndtw_envelopes); key: [nq] out.
+ * self_offset >= 0 excludes train index (local) i + self_offset for query i (leave-one-out);
+ * pass -1 otherwise.  stats: host, nullable (non-NULL synchronises).
+ */
+#define NNDTW_CLASSIFY_EXACT 1u
+NNDTW_API size_t nndtw_classify_workspace_bytes(int64_t nq, int64_t nt, int32_t L, int32_t w);
+NNDTW_API int nndtw_classify(const float *q, int64_t nq, const float *t, const float *upper,
+                   const float *lower, const nndtw_kim *tkim, int64_t nt, int64_t index_base,
+                   int64_t self_offset, int32_t L, int32_t w, int32_t v, uint32_t flags,
+                   void *ws, size_t ws_bytes, uint64_t *key, nndtw_stats *stats, void *stream);
+
+/*
+ * S7 (sharded) -- near-tie re-rank, step 1.  gkey: [nq] the MIN of all shards' keys.  For
+ * every locally completed candidate whose fp32 distance is within gkey*(1+eps_t) of the global
+ * best, recompute DTW in fp64 with the oracle's per-cell operation sequence (DESIGN.md
+ * "fp64 re-rank"); f64key[i] = bits of the smallest such fp64 value (UINT64_MAX if none).
+ * Requires the ws of the preceding nndtw_classify call (same q, t).
+ */
+NNDTW_API int nndtw_classify_refine(void *ws, size_t ws_bytes, const float *q, int64_t nq,
+                          const float *t, int64_t nt, int32_t L, int32_t w,
+                          const uint64_t *gkey, uint64_t *f64key, void *stream);
+/* S7 step 2.  gf64: [nq] MIN over shards of f64key; gkey as for refine.  out[i] = (global
+ * index << 32) | fp32 bits of the local candidate with fp64 value == gf64[i] and the lowest
+ * index (UINT64_MAX if none); a MIN over shards gives the final answer (key_format 1).
+ * Same ws and arguments as the preceding refine call. */
+NNDTW_API int nndtw_classify_resolve(void *ws, size_t ws_bytes, const float *q, int64_t nq,
+                           const float *t, int64_t nt, int32_t L, int32_t w,
+                           int64_t index_base, const uint64_t *gkey, const uint64_t *gf64,
+                           uint64_t *out, void *stream);
+
+/*
+ * Decode keys: key_format 0 = (f32 bits << 32) | idx (nndtw_classify), 1 = (idx << 32) | f32
+ * bits (nndtw_classify_resolve).  idx_out [nq] int64, label_out [nq] int32 (labels[idx]),
+ * dist_out [nq] float (squared distance); each nullable.  labels: [nlabels] (global ids).
+ */
+NNDTW_API int nndtw_finalize(const uint64_t *key, int64_t nq, int32_t key_format, const int32_t *labels,
+                   int64_t nlabels, int64_t *idx_out, int32_t *label_out, float *dist_out,
+                   void *stream);
+
+/*
+ * S8 -- leave-one-out warping-window search (reading C17).  For every window
+ * windows[p] (host array, absolute w, any order) and every held-out series i in
+ * [q_begin, q_end): the exact 1-NN of x[i] among x[j], j != i, under DTW_{w_p}
+ * (ties -> lowest j, fp64-exact via the local re-rank).  errors[p] += #{i: labels[nn] !=
+ * labels[i]} (device int64 [nw], accumulated -- zero it first); nn_out: [nw][q_end-q_begin]
+ * int32, nullable.  The train set is all n series (replicated); shard the held-out range
+ * across ranks and SUM errors.  Windows are processed in the given order and each window is
+ * seeded with the previous window's neighbour (DTW is monotone in w).
+ */
+NNDTW_API size_t nndtw_loocv_workspace_bytes(int64_t n, int32_t L, int64_t q_begin, int64_t q_end);
+NNDTW_API int nndtw_loocv_window(const float *x, const int32_t *labels, int64_t n, int32_t L,
+                       const int32_t *windows, int32_t nw, int32_t v, int64_t q_begin,
+                       int64_t q_end, void *ws, size_t ws_bytes, int64_t *errors,
+                       int32_t *nn_out, nndtw_stats *stats, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NNDTW_H */

@@ -1,0 +1,507 @@
+// abi.cu -- host orchestration behind the C ABI of include/nndtw.h.
+//
+// No host synchronisation on the search path: every stage reads its work counts from device
+// memory (persistent DTW grids), so nndtw_classify is a fixed sequence of kernel launches on
+// the caller's stream (CUDA-graph capturable when stats == NULL).
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "launchers.cuh"
+
+namespace nndtw {
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int64_t launches_total() { return g_launches.load(std::memory_order_relaxed); }
+
+// ---- finite check (input validation for the Python layer) -----------------------------------
+__global__ void k_check_finite(const float *x, int64_t n, int32_t *bad) {
+    int found = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(x[i])) found = 1;
+    if (__any_sync(0xffffffffu, found) && (threadIdx.x & 31) == 0) *bad = 1;
+}
+
+int launch_check_finite(const float *x, int64_t n, int32_t *bad, cudaStream_t st) {
+    if (n <= 0) return 0;
+    int64_t grid = (n + 255) / 256;
+    if (grid > 2048) grid = 2048;
+    k_check_finite<<<(unsigned)grid, 256, 0, st>>>(x, n, bad);
+    count_launch();
+    return 0;
+}
+
+}  // namespace nndtw
+
+using namespace nndtw;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+static int cuda_fail(const char *where) {
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) return NNDTW_OK;
+    return fail(NNDTW_E_CUDA, std::string(where) + ": " + cudaGetErrorName(e) + " (" +
+                                  cudaGetErrorString(e) + ")");
+}
+
+static int device_sms(int *sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cuda_fail("cudaGetDevice");
+    static std::mutex mu;
+    static int cache_dev = -1, cache_sms = 0, cache_ok = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache_dev != dev) {
+        int major = 0, minor = 0, n = 0;
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cache_dev = dev;
+        cache_sms = n;
+        cache_ok = (major == 10 && minor == 0);
+    }
+    *sms = cache_sms;
+    if (!cache_ok) return fail(NNDTW_E_ARCH, "libnndtw is built for sm_100a (B200) only");
+    return NNDTW_OK;
+}
+
+static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// ---- classify workspace layout -----------------------------------------------------------
+struct ClassifyWs {
+    unsigned long long *counters;  // CNT_N + 3 (seed count, item count, log count)
+    unsigned long long *seed_count, *main_count, *log_count;
+    nndtw_kim *qkim;
+    unsigned long long *minkey, *f64key, *resolve_out;
+    unsigned *overflow;
+    float *lb;
+    int64_t ldlb;
+    Item *seed_items;
+    Item *items;
+    unsigned long long item_cap;
+    TieEntry *log;
+    unsigned long long log_cap;
+    long long *cells_prefix;
+    size_t bytes;
+};
+
+static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
+    ClassifyWs W;
+    size_t off = 0;
+    char *b = (char *)base;
+    auto take = [&](size_t bytes) -> char * {
+        char *p = b ? b + off : nullptr;
+        off = align256(off + bytes);
+        return p;
+    };
+    const size_t q1 = (size_t)(nq > 0 ? nq : 1);
+    W.counters = (unsigned long long *)take(sizeof(unsigned long long) * (CNT_N + 3));
+    W.seed_count = W.counters ? W.counters + CNT_N : nullptr;
+    W.main_count = W.counters ? W.counters + CNT_N + 1 : nullptr;
+    W.log_count = W.counters ? W.counters + CNT_N + 2 : nullptr;
+    W.qkim = (nndtw_kim *)take(sizeof(nndtw_kim) * q1);
+    W.minkey = (unsigned long long *)take(8 * q1);
+    W.f64key = (unsigned long long *)take(8 * q1);
+    W.resolve_out = (unsigned long long *)take(8 * q1);
+    W.overflow = (unsigned *)take(4 * q1);
+    W.ldlb = (nt + 3) / 4 * 4;
+    W.lb = (float *)take(sizeof(float) * (size_t)nq * (size_t)W.ldlb);
+    W.seed_items = (Item *)take(sizeof(Item) * (2 * q1 + 1));
+    W.item_cap = (unsigned long long)nq * (unsigned long long)nt + 1;
+    W.items = (Item *)take(sizeof(Item) * (size_t)W.item_cap);
+    W.log_cap = (unsigned long long)(64 * nq > 65536 ? 64 * nq : 65536);
+    W.log = (TieEntry *)take(sizeof(TieEntry) * (size_t)W.log_cap);
+    W.cells_prefix = (long long *)take(sizeof(long long) * (size_t)(2 * L));
+    W.bytes = off;
+    return W;
+}
+
+static int check_common(int64_t n, int L, int w) {
+    if (n < 0) return fail(NNDTW_E_ARG, "negative count");
+    if (L < 2) return fail(NNDTW_E_LENGTH, "L must be >= 2 (Algorithm 1 needs L >= 2)");
+    if (L > 8192) return fail(NNDTW_E_LENGTH, "L > 8192 is not supported");
+    if (w < 0) return fail(NNDTW_E_WINDOW, "w must be >= 0");
+    return NNDTW_OK;
+}
+
+static int dtw_fail(int rc, int L, int w) {
+    if (rc == 0) return NNDTW_OK;
+    return fail(NNDTW_E_WINDOW, "no DTW kernel for L=" + std::to_string(L) +
+                                    " w=" + std::to_string(w));
+}
+
+struct StageTimer {
+    bool on;
+    cudaStream_t st;
+    cudaEvent_t ev[8];
+    int n = 0;
+    StageTimer(bool on_, cudaStream_t s) : on(on_), st(s) {
+        if (on)
+            for (auto &e : ev) cudaEventCreate(&e);
+    }
+    void mark() {
+        if (on && n < 8) cudaEventRecord(ev[n++], st);
+    }
+    float ms(int a, int b) {
+        float m = 0;
+        if (on && b < n) cudaEventElapsedTime(&m, ev[a], ev[b]);
+        return m;
+    }
+    ~StageTimer() {
+        if (on)
+            for (auto &e : ev) cudaEventDestroy(e);
+    }
+};
+
+// S7 for one shard whose local best is the global best (single GPU, LOOCV).
+static void exact_local(ClassifyWs &W, const float *q, int64_t nq, const float *t, int64_t nt,
+                        int L, int w, int64_t index_base, unsigned long long *key,
+                        unsigned long long *cnt, int sms, cudaStream_t st) {
+    const float eps_p = eps_prune(L), eps_t = eps_tie(L);
+    launch_refine(W.log, W.log_count, W.log_cap, q, t, L, w, key, eps_t, W.f64key, cnt, sms, st);
+    launch_refine_overflow(W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w, key, eps_p, 0,
+                           W.f64key, nullptr, index_base, nullptr, sms, st);
+    launch_resolve(W.log, W.log_count, W.log_cap, W.f64key, index_base, W.resolve_out, sms, st);
+    launch_refine_overflow(W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w, key, eps_p, 1,
+                           W.f64key, W.f64key, index_base, W.resolve_out, sms, st);
+    launch_swap_key(W.resolve_out, nq, key, st);
+}
+
+// Core of nndtw_classify (also used per window by nndtw_loocv_window).
+static int classify_impl(const float *q, int64_t nq, const float *t, const float *U,
+                         const float *Lo, const nndtw_kim *tkim, int64_t nt, int64_t index_base,
+                         int64_t self_offset, int L, int w, int v, uint32_t flags,
+                         const int32_t *seed2, void *ws, size_t ws_bytes,
+                         unsigned long long *key, nndtw_stats *stats, cudaStream_t st,
+                         StageTimer *outer_tm = nullptr) {
+    int sms = 0;
+    int rc = device_sms(&sms);
+    if (rc) return rc;
+    if ((rc = check_common(nq, L, w))) return rc;
+    if (nt < 0) return fail(NNDTW_E_ARG, "negative nt");
+    if (v < 1) return fail(NNDTW_E_V, "V must be >= 1");
+    if (w > L - 1) w = L - 1;
+    if (nq > 0 && (!q || !key || !ws)) return fail(NNDTW_E_ARG, "null pointer argument");
+    if (nt > 0 && (!t || !U || !Lo || !tkim)) return fail(NNDTW_E_ARG, "null pointer argument");
+    if (index_base < 0 || index_base + nt > 0xffffffffll)
+        return fail(NNDTW_E_INDEX, "global train indices must fit in 32 bits");
+    ClassifyWs W = classify_layout(ws, nq, nt, L);
+    if (ws_bytes < W.bytes) return fail(NNDTW_E_WORKSPACE, "workspace too small");
+    if (nq == 0) return NNDTW_OK;
+    const int64_t launches0 = launches_total();
+    StageTimer tm(stats != nullptr && outer_tm == nullptr, st);
+    const float eps_p = eps_prune(L), eps_t = eps_tie(L);
+
+    tm.mark();  // 0
+    cudaMemsetAsync(W.counters, 0, sizeof(unsigned long long) * (CNT_N + 3), st);
+    launch_fill_u64(key, nq, kKeyInit, st);
+    cudaMemsetAsync(W.minkey, 0xff, 8 * (size_t)nq, st);
+    cudaMemsetAsync(W.f64key, 0xff, 8 * (size_t)nq, st);
+    cudaMemsetAsync(W.resolve_out, 0xff, 8 * (size_t)nq, st);
+    cudaMemsetAsync(W.overflow, 0, 4 * (size_t)nq, st);
+    if (stats) launch_cells_prefix(L, w, W.cells_prefix, st);
+    // S2: cascade bound for all pairs + per-query argmin-LB candidate
+    launch_series_stats(q, nq, L, W.qkim, st);
+    tm.mark();  // 1
+    if (nt > 0 && launch_lb(q, nq, W.qkim, t, U, Lo, tkim, nt, L, w, v, 1, self_offset, W.lb,
+                            W.ldlb, W.minkey, st))
+        return fail(NNDTW_E_ARG, "too many train series for one launch");
+    tm.mark();  // 2
+    if ((rc = cuda_fail("lb"))) return rc;
+    TieLog log{W.log, W.log_count, W.log_cap, W.overflow};
+    unsigned long long *cnt = stats ? W.counters : nullptr;
+    if (nt > 0) {
+        // S3: seed round (argmin-LB candidate, plus seed2 if given)
+        launch_seed_items(W.minkey, seed2, nq, nt, W.seed_items, W.seed_count, st);
+        rc = dispatch_dtw(q, t, W.seed_items, W.seed_count, 2 * (unsigned long long)nq + 1,
+                          nullptr, nullptr, 0, L, w, 0, key, index_base, eps_t, log, cnt,
+                          W.cells_prefix, nullptr, nullptr, st, sms);
+        if ((rc = dtw_fail(rc, L, w))) return rc;
+        // S3: prune + compact the survivors against the seeded best-so-far
+        launch_compact(W.lb, W.ldlb, nq, nt, key, W.minkey, seed2, eps_p, W.items,
+                       W.main_count, W.item_cap, sms, st);
+        // S4/S5: DTW with early abandoning on the survivors
+        rc = dispatch_dtw(q, t, W.items, W.main_count, W.item_cap, nullptr, nullptr, 0, L, w, 0,
+                          key, index_base, eps_t, log, cnt, W.cells_prefix, nullptr, nullptr,
+                          st, sms);
+        if ((rc = dtw_fail(rc, L, w))) return rc;
+    }
+    tm.mark();  // 3
+    if ((rc = cuda_fail("dtw"))) return rc;
+    if ((flags & NNDTW_CLASSIFY_EXACT) && nt > 0)
+        exact_local(W, q, nq, t, nt, L, w, index_base, key, cnt, sms, st);
+    tm.mark();  // 4
+    if ((rc = cuda_fail("classify"))) return rc;
+    if (stats) {
+        unsigned long long h[CNT_N + 3];
+        cudaMemcpyAsync(h, W.counters, sizeof h, cudaMemcpyDeviceToHost, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_fail("classify sync");
+        stats->lb_pairs += nq * nt;
+        stats->survivors += (int64_t)h[CNT_N + 1];
+        stats->dtw_calls += (int64_t)h[CNT_ITEMS];
+        stats->dtw_abandoned += (int64_t)h[CNT_ABANDONED];
+        stats->cells += (int64_t)h[CNT_CELLS];
+        stats->near_tie_pairs += (int64_t)h[CNT_TIES];
+        stats->rounds += 2;
+        stats->launches += (int32_t)(launches_total() - launches0);
+        if (outer_tm == nullptr) {
+            stats->ms_lb += tm.ms(1, 2);
+            stats->ms_dtw += tm.ms(2, 3);
+            stats->ms_other += tm.ms(0, 1) + tm.ms(3, 4);
+        }
+    }
+    return NNDTW_OK;
+}
+
+// ---- LOOCV workspace ---------------------------------------------------------------------
+struct LoocvWs {
+    float *U, *Lo;
+    nndtw_kim *kim;
+    int32_t *prev_nn;
+    unsigned long long *key;
+    void *cws;
+    size_t cws_bytes;
+    size_t bytes;
+};
+
+static LoocvWs loocv_layout(void *base, int64_t n, int L, int64_t nq) {
+    LoocvWs W;
+    size_t off = 0;
+    char *b = (char *)base;
+    auto take = [&](size_t bytes) -> char * {
+        char *p = b ? b + off : nullptr;
+        off = align256(off + bytes);
+        return p;
+    };
+    const size_t q1 = (size_t)(nq > 0 ? nq : 1);
+    W.U = (float *)take(sizeof(float) * (size_t)n * L);
+    W.Lo = (float *)take(sizeof(float) * (size_t)n * L);
+    W.kim = (nndtw_kim *)take(sizeof(nndtw_kim) * (size_t)(n > 0 ? n : 1));
+    W.prev_nn = (int32_t *)take(4 * q1);
+    W.key = (unsigned long long *)take(8 * q1);
+    W.cws_bytes = classify_layout(nullptr, nq, n, L).bytes;
+    W.cws = take(W.cws_bytes);
+    W.bytes = off;
+    return W;
+}
+
+extern "C" {
+
+const char *nndtw_last_error(void) { return g_err.c_str(); }
+int nndtw_version(void) { return 1; }
+int64_t nndtw_launch_count(void) { return launches_total(); }
+
+int nndtw_check_device(void) {
+    int sms;
+    return device_sms(&sms);
+}
+
+int nndtw_check_finite(const float *x, int64_t n, int32_t *bad, void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if (n < 0 || (n > 0 && (!x || !bad))) return fail(NNDTW_E_ARG, "bad arguments");
+    launch_check_finite(x, n, bad, (cudaStream_t)stream);
+    return cuda_fail("nndtw_check_finite");
+}
+
+int nndtw_envelopes(const float *x, int64_t n, int32_t L, int32_t w, float *upper,
+                    float *lower, nndtw_kim *kim, void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if (n < 0) return fail(NNDTW_E_ARG, "negative count");
+    if (L < 1 || L > 8192) return fail(NNDTW_E_LENGTH, "L must be in [1, 8192]");
+    if (w < 0) return fail(NNDTW_E_WINDOW, "w must be >= 0");
+    if (n > 0 && (!x || !upper || !lower)) return fail(NNDTW_E_ARG, "null pointer argument");
+    if (launch_envelopes(x, n, L, w, upper, lower, kim, (cudaStream_t)stream))
+        return fail(NNDTW_E_LENGTH, "unsupported envelope shape");
+    return cuda_fail("nndtw_envelopes");
+}
+
+int nndtw_series_stats(const float *x, int64_t n, int32_t L, nndtw_kim *kim, void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if (n < 0 || (n > 0 && (!x || !kim))) return fail(NNDTW_E_ARG, "bad arguments");
+    if (L < 1) return fail(NNDTW_E_LENGTH, "L must be >= 1");
+    launch_series_stats(x, n, L, kim, (cudaStream_t)stream);
+    return cuda_fail("nndtw_series_stats");
+}
+
+int nndtw_lb_enhanced(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
+                      const float *upper, const float *lower, const nndtw_kim *tkim,
+                      int64_t nt, int32_t L, int32_t w, int32_t v, uint32_t flags, float *lb,
+                      int64_t ldlb, void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if ((rc = check_common(nq, L, w))) return rc;
+    if (nt < 0) return fail(NNDTW_E_ARG, "negative nt");
+    if (v < 1) return fail(NNDTW_E_V, "V must be >= 1");
+    if (ldlb < nt) return fail(NNDTW_E_ARG, "ldlb < nt");
+    bool kim = (flags & NNDTW_LB_WITH_KIM) != 0;
+    if (nq > 0 && nt > 0 && (!q || !t || !upper || !lower || !lb || (kim && (!qkim || !tkim))))
+        return fail(NNDTW_E_ARG, "null pointer argument");
+    if (launch_lb(q, nq, qkim, t, upper, lower, tkim, nt, L, w, v, kim ? 1 : 0, -1, lb, ldlb,
+                  nullptr, (cudaStream_t)stream))
+        return fail(NNDTW_E_ARG, "too many train series for one launch");
+    return cuda_fail("nndtw_lb_enhanced");
+}
+
+int nndtw_dtw_batch(const float *a, const float *b, const int32_t *ia, const int32_t *ib,
+                    int64_t npairs, int32_t L, int32_t w, const float *cutoff, float *out,
+                    void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if ((rc = check_common(npairs, L, w))) return rc;
+    if (npairs == 0) return NNDTW_OK;
+    if (!a || !b || !out) return fail(NNDTW_E_ARG, "null pointer argument");
+    if (w > L - 1) w = L - 1;
+    TieLog log{nullptr, nullptr, 0, nullptr};
+    rc = dispatch_dtw(a, b, nullptr, nullptr, 0, ia, ib, npairs, L, w, 1, nullptr, 0,
+                      eps_tie(L), log, nullptr, nullptr, cutoff, out, (cudaStream_t)stream, sms);
+    if ((rc = dtw_fail(rc, L, w))) return rc;
+    return cuda_fail("nndtw_dtw_batch");
+}
+
+size_t nndtw_classify_workspace_bytes(int64_t nq, int64_t nt, int32_t L, int32_t w) {
+    (void)w;
+    return classify_layout(nullptr, nq, nt, L).bytes;
+}
+
+int nndtw_classify(const float *q, int64_t nq, const float *t, const float *upper,
+                   const float *lower, const nndtw_kim *tkim, int64_t nt, int64_t index_base,
+                   int64_t self_offset, int32_t L, int32_t w, int32_t v, uint32_t flags,
+                   void *ws, size_t ws_bytes, uint64_t *key, nndtw_stats *stats, void *stream) {
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    return classify_impl(q, nq, t, upper, lower, tkim, nt, index_base, self_offset, L, w, v,
+                         flags, nullptr, ws, ws_bytes, (unsigned long long *)key, stats,
+                         (cudaStream_t)stream);
+}
+
+int nndtw_classify_refine(void *ws, size_t ws_bytes, const float *q, int64_t nq,
+                          const float *t, int64_t nt, int32_t L, int32_t w,
+                          const uint64_t *gkey, uint64_t *f64key, void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if ((rc = check_common(nq, L, w))) return rc;
+    if (w > L - 1) w = L - 1;
+    ClassifyWs W = classify_layout(ws, nq, nt, L);
+    if (!ws || ws_bytes < W.bytes) return fail(NNDTW_E_WORKSPACE, "workspace too small");
+    if (nq == 0) return NNDTW_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(f64key, 0xff, 8 * (size_t)nq, st);
+    if (nt > 0) {
+        launch_refine(W.log, W.log_count, W.log_cap, q, t, L, w,
+                      (const unsigned long long *)gkey, eps_tie(L),
+                      (unsigned long long *)f64key, nullptr, sms, st);
+        launch_refine_overflow(W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w,
+                               (const unsigned long long *)gkey, eps_prune(L), 0,
+                               (unsigned long long *)f64key, nullptr, 0, nullptr, sms, st);
+    }
+    return cuda_fail("nndtw_classify_refine");
+}
+
+int nndtw_classify_resolve(void *ws, size_t ws_bytes, const float *q, int64_t nq,
+                           const float *t, int64_t nt, int32_t L, int32_t w,
+                           int64_t index_base, const uint64_t *gkey, const uint64_t *gf64,
+                           uint64_t *out, void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if ((rc = check_common(nq, L, w))) return rc;
+    if (w > L - 1) w = L - 1;
+    ClassifyWs W = classify_layout(ws, nq, nt, L);
+    if (!ws || ws_bytes < W.bytes) return fail(NNDTW_E_WORKSPACE, "workspace too small");
+    if (nq == 0) return NNDTW_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(out, 0xff, 8 * (size_t)nq, st);
+    if (nt > 0) {
+        launch_resolve(W.log, W.log_count, W.log_cap, (const unsigned long long *)gf64,
+                       index_base, (unsigned long long *)out, sms, st);
+        launch_refine_overflow(W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w,
+                               (const unsigned long long *)gkey, eps_prune(L), 1, nullptr,
+                               (const unsigned long long *)gf64, index_base,
+                               (unsigned long long *)out, sms, st);
+    }
+    return cuda_fail("nndtw_classify_resolve");
+}
+
+int nndtw_finalize(const uint64_t *key, int64_t nq, int32_t key_format, const int32_t *labels,
+                   int64_t nlabels, int64_t *idx_out, int32_t *label_out, float *dist_out,
+                   void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if (nq < 0 || (nq > 0 && !key) || (key_format != 0 && key_format != 1))
+        return fail(NNDTW_E_ARG, "bad arguments");
+    launch_finalize((const unsigned long long *)key, nq, key_format, labels, nlabels, idx_out,
+                    label_out, dist_out, (cudaStream_t)stream);
+    return cuda_fail("nndtw_finalize");
+}
+
+size_t nndtw_loocv_workspace_bytes(int64_t n, int32_t L, int64_t q_begin, int64_t q_end) {
+    return loocv_layout(nullptr, n, L, q_end - q_begin).bytes;
+}
+
+int nndtw_loocv_window(const float *x, const int32_t *labels, int64_t n, int32_t L,
+                       const int32_t *windows, int32_t nw, int32_t v, int64_t q_begin,
+                       int64_t q_end, void *ws, size_t ws_bytes, int64_t *errors,
+                       int32_t *nn_out, nndtw_stats *stats, void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if ((rc = check_common(n, L, 0))) return rc;
+    if (v < 1) return fail(NNDTW_E_V, "V must be >= 1");
+    if (nw < 0 || (nw > 0 && !windows)) return fail(NNDTW_E_ARG, "bad window list");
+    if (q_begin < 0 || q_end < q_begin || q_end > n)
+        return fail(NNDTW_E_ARG, "query range outside [0, n]");
+    if (n > 0 && (!x || !labels || !errors || !ws)) return fail(NNDTW_E_ARG, "null pointer");
+    for (int p = 0; p < nw; ++p)
+        if (windows[p] < 0) return fail(NNDTW_E_WINDOW, "w must be >= 0");
+    const int64_t nq = q_end - q_begin;
+    LoocvWs W = loocv_layout(ws, n, L, nq);
+    if (ws_bytes < W.bytes) return fail(NNDTW_E_WORKSPACE, "workspace too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    if (nq == 0 || nw == 0) return NNDTW_OK;
+    const float *qx = x + q_begin * (int64_t)L;
+    cudaEvent_t e0, e1, e2;
+    if (stats) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventCreate(&e2);
+    }
+    float ms_env = 0, ms_rest = 0;
+    for (int p = 0; p < nw; ++p) {
+        int w = windows[p] > L - 1 ? L - 1 : windows[p];
+        if (stats) cudaEventRecord(e0, st);
+        launch_envelopes(x, n, L, w, W.U, W.Lo, p == 0 ? W.kim : nullptr, st);
+        if (stats) cudaEventRecord(e1, st);
+        rc = classify_impl(qx, nq, x, W.U, W.Lo, W.kim, n, 0, q_begin, L, w, v,
+                           NNDTW_CLASSIFY_EXACT, p == 0 ? nullptr : W.prev_nn, W.cws,
+                           W.cws_bytes, W.key, stats, st, nullptr);
+        if (rc) return rc;
+        launch_count_errors(W.key, nq, labels, q_begin, errors + p,
+                            nn_out ? nn_out + (int64_t)p * nq : nullptr, W.prev_nn, st);
+        if (stats) {
+            cudaEventRecord(e2, st);
+            cudaEventSynchronize(e2);
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, e0, e1);
+            cudaEventElapsedTime(&b, e1, e2);
+            ms_env += a;
+            ms_rest += b;
+        }
+    }
+    if (stats) {
+        stats->ms_envelopes = ms_env;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaEventDestroy(e2);
+    }
+    return cuda_fail("nndtw_loocv_window");
+}
+
+}  // extern "C"

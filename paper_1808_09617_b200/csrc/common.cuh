@@ -1,0 +1,75 @@
+// common.cuh -- internal helpers shared by the libnndtw.so translation units (not part of
+// the ABI).  Nothing here is shared with oracle/ (DESIGN.md "Oracle independence").
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdio>
+
+#include "../../include/nndtw.h"
+
+namespace nndtw {
+
+constexpr float kInf = __builtin_huge_valf();
+constexpr unsigned long long kKeyInit = 0x7F800000FFFFFFFFull;  // (+inf bits << 32) | ~0
+constexpr unsigned long long kNone = ~0ull;
+
+// Rounding-error margins of reading C16 (u = 2^-24, fp32 storage and accumulation):
+//  prune a pair only if LB > bsf*(1+eps_p), eps_p = (3L+8)u;
+//  abandon / near-tie band at bsf*(1+eps_t), eps_t = (4L+8)u.
+inline float eps_prune(int L) { return (3.0f * (float)L + 8.0f) * 0x1p-24f; }
+inline float eps_tie(int L) { return (4.0f * (float)L + 8.0f) * 0x1p-24f; }
+
+// process-wide launch counter (bench bookkeeping; incremented by every launcher)
+void count_launch(int n = 1);
+int64_t launches_total();
+
+struct CudaCheck {
+    static int last(const char *where);
+};
+
+// ---- small device helpers ----------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ float key_dist(unsigned long long k) {
+    return __uint_as_float((unsigned)(k >> 32));
+}
+
+__device__ __forceinline__ unsigned long long make_key(float d, unsigned idx) {
+    return ((unsigned long long)__float_as_uint(d) << 32) | (unsigned long long)idx;
+}
+
+__device__ __forceinline__ float sq(float x) { return x * x; }
+
+// ---- work items ---------------------------------------------------------------------------
+// A DTW work item: query (row of A) and train (row of B), local indices.
+struct Item {
+    unsigned q, n;
+};
+
+// near-tie log entry (S7): completed candidate within the band of the live best at the time
+struct TieEntry {
+    unsigned q, n;
+    float d32;
+    float pad;
+    double d64;
+};
+
+struct TieLog {
+    TieEntry *e;
+    unsigned long long *count;   // appended entries (may exceed capacity: overflow)
+    unsigned long long capacity;
+    unsigned *overflow;          // [nq] 1 if an entry of query q was dropped
+};
+
+// Per-call device counters (stats); index meaning below.
+enum { CNT_ITEMS = 0, CNT_ABANDONED = 1, CNT_CELLS = 2, CNT_SURVIVORS = 3, CNT_TIES = 4,
+       CNT_N = 8 };
+
+}  // namespace nndtw

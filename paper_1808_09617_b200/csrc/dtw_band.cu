@@ -1,0 +1,358 @@
+// dtw_band.cu -- S4: windowed DTW (Eq. 1; Sakoe-Chiba band P:164-171) on a list of
+// (query, train) work items, with early abandoning against a per-query best-so-far.
+//
+// B200 design.  A group of G lanes owns one DP matrix; lane g
+// holds R (even) consecutive band offsets d = j - i, slots s = g*R + r <-> d = s - w, in
+// registers D[r].  The matrix is swept by anti-diagonals k = i + j: cell (k, d) depends on
+// (k-2, d) [diagonal move], (k-1, d-1) [left] and (k-1, d+1) [up], so one register per offset
+// suffices -- on diagonal k only offsets with d = k (mod 2) exist and they read neighbours of
+// the other parity, last written on diagonal k-1:
+//     D[r] <- (A_i*sc_r - B_j)^2 + min(D[r], D[r-1], D[r+1])    (FFMA, FMNMX3, FFMA)
+// Neighbours across lanes: one warp shuffle per diagonal (shfl_up of D[R-1] on even-phase
+// diagonals, shfl_down of D[0] on odd ones).  A and B sit in shared memory with index-dependent
+// pads (+-2^64*k, distinct per index) so that cells outside the matrix get +inf (their squared
+// difference overflows) while the cells (x, x) outside it get 0 -- this makes D(-1,-1) = 0 the
+// start condition and carries D(L-1,L-1) unchanged to the end of the last unrolled period, so
+// the R-diagonal period is fully unrolled with no boundary tests.  The band edge d = w+1 is a
+// "kill" slot whose A value is scaled by +inf (NaN/inf results, ignored by fminf); slots
+// beyond it stay +inf.  Early abandoning (reading C14): after every period the registers hold
+// two consecutive anti-diagonals, a cut of every warping path; the group abandons when every
+// lane's minimum exceeds bsf*(1+eps_t) (one warp ballot).
+#include "launchers.cuh"
+
+namespace nndtw {
+
+struct BandParams {
+    const float *A, *B;
+    const Item *items;                    // search mode: (q, n)
+    const unsigned long long *nitems_dev; // search mode: device count
+    unsigned long long item_cap;          // search mode: capacity of items
+    const int32_t *ia, *ib;               // batch mode (nullable = identity)
+    int64_t nitems_host;                  // batch mode count
+    int L, w, G, gpw, nper, k0, padl, seglen;
+    int mode;                             // 0 search, 1 batch
+    unsigned long long *key;
+    int64_t index_base;
+    float eps_t;
+    TieLog log;
+    unsigned long long *counters;         // nullable
+    const long long *cells_prefix;        // [2L-1], nullable iff counters null
+    const float *cutoff;                  // batch, nullable
+    float *out;                           // batch
+};
+
+template <int R, bool ALIGNED>
+__global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
+    extern __shared__ __align__(16) float smem_f[];
+    constexpr int H = R / 2;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int G = p.G, gpw = p.gpw, L = p.L, w = p.w;
+    const int gw = lane / G;
+    const int g = lane - gw * G;
+    const bool valid_lane = gw < gpw;
+    const int warps_per_block = blockDim.x >> 5;
+    const int64_t gid = ((int64_t)blockIdx.x * warps_per_block + warp) * gpw + gw;
+    const int64_t ngroups = (int64_t)gridDim.x * warps_per_block * gpw;
+    const unsigned gbits = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
+
+    float *sA = smem_f + (size_t)(warp * gpw + (valid_lane ? gw : 0)) * 2 * p.seglen;
+    float *sB = sA + p.seglen;
+
+    // index-dependent pads, written once (they never change)
+    if (valid_lane) {
+        for (int x = g; x < p.seglen; x += G) {
+            int idx = x - p.padl;
+            if (idx < 0 || idx >= L) {
+                float v = idx < 0 ? 0x1p64f * (float)idx : 0x1p64f * (float)(idx - L + 1);
+                sA[x] = v;
+                sB[x] = v;
+            }
+        }
+    }
+
+    // slot bookkeeping
+    const int g0 = w / R, r0 = w - (w / R) * R;     // slot of d = 0 (result)
+    const int skill = 2 * w + 1;                     // kill slot d = w+1
+    float sc[ALIGNED ? 1 : R];
+    if (ALIGNED) {
+        sc[0] = (g * R + R - 1 == skill) ? kInf : 1.0f;
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) sc[r] = (g * R + r == skill) ? kInf : 1.0f;
+    }
+    const float nbmask_lo = (g == 0) ? kInf : 0.0f;        // selects +inf at group edges
+    const float nbmask_hi = (g == G - 1) ? kInf : 0.0f;
+
+    int64_t nitems = p.nitems_host;
+    if (p.mode == 0) {
+        unsigned long long c = *p.nitems_dev;
+        nitems = (int64_t)(c < p.item_cap ? c : p.item_cap);
+    }
+    int64_t it = gid;
+    bool active = valid_lane && it < nitems;
+
+    float D[R];
+    int per = 0;
+    unsigned qcur = 0, ncur = 0;
+    float thr_batch = kInf;
+    long long my_items = 0, my_aband = 0, my_cells = 0;
+
+    auto setup = [&]() {
+        unsigned a_idx, b_idx;
+        if (p.mode == 0) {
+            Item itm = p.items[it];
+            a_idx = itm.q;
+            b_idx = itm.n;
+        } else {
+            a_idx = p.ia ? (unsigned)p.ia[it] : (unsigned)it;
+            b_idx = p.ib ? (unsigned)p.ib[it] : (unsigned)it;
+            thr_batch = p.cutoff ? p.cutoff[it] * (1.0f + p.eps_t) : kInf;
+        }
+        qcur = a_idx;
+        ncur = b_idx;
+        const float *ga = p.A + (int64_t)a_idx * L;
+        const float *gb = p.B + (int64_t)b_idx * L;
+        for (int x = g; x < L; x += G) {
+            sA[p.padl + x] = __ldg(ga + x);
+            sB[p.padl + x] = __ldg(gb + x);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) D[r] = (g == g0 && r == r0) ? 0.0f : kInf;
+        per = 0;
+    };
+
+    if (active) setup();
+    __syncwarp();
+
+    while (__any_sync(0xffffffffu, active)) {
+        unsigned long long kraw = 0;
+        if (p.mode == 0 && active) kraw = ld_volatile_u64(p.key + qcur);
+
+        // ---- one period: R anti-diagonals, fully unrolled ----------------------------
+        const int kp = p.k0 + per * R;
+        const int I0 = (kp + w - g * R) >> 1;   // kp + w is even by construction
+        const int J0 = (kp - w + g * R) >> 1;
+        const float *pa = sA + p.padl + I0 - (H - 1);
+        const float *pb = sB + p.padl + J0;
+        float aw[R - 1], bw[R];
+#pragma unroll
+        for (int x = 0; x < R - 1; ++x) aw[x] = pa[x];
+#pragma unroll
+        for (int y = 0; y < R; ++y) bw[y] = pb[y];
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            const int phi = t & 1;
+            float nlo = 0.0f, nhi = 0.0f;
+            if (phi == 0) nlo = __shfl_up_sync(0xffffffffu, D[R - 1], 1) + nbmask_lo;
+            else nhi = __shfl_down_sync(0xffffffffu, D[0], 1) + nbmask_hi;
+#pragma unroll
+            for (int m = 0; m < H; ++m) {
+                const int r = phi + 2 * m;
+                const float a = aw[(t >> 1) - m + H - 1];
+                const float b = bw[((t + 1) >> 1) + m];
+                float s;
+                if (ALIGNED) s = (r == R - 1) ? sc[0] : 1.0f;
+                else s = sc[r];
+                const float tt = (ALIGNED && r != R - 1) ? (a - b) : fmaf(a, s, -b);
+                const float lo = (r == 0) ? nlo : D[r - 1];
+                const float hi = (r == R - 1) ? nhi : D[r + 1];
+                D[r] = fmaf(tt, tt, fminf(fminf(D[r], lo), hi));
+            }
+        }
+        ++per;
+
+        // ---- events: completion / early abandon --------------------------------------
+        float lmin = D[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r) lmin = fminf(lmin, D[r]);
+        float thr = p.mode == 0 ? key_dist(kraw) * (1.0f + p.eps_t) : thr_batch;
+        bool vote = !(lmin <= thr);
+        unsigned ballot = __ballot_sync(0xffffffffu, vote);
+        bool done = active && per == p.nper;
+        bool abandon = active && !done && ((ballot & gbits) == gbits);
+        float res = D[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r)
+            if (r == r0) res = D[r];
+        if (done && g == g0) {
+            if (p.mode == 0) {
+                unsigned gidx = (unsigned)(p.index_base + ncur);
+                unsigned long long old = atomicMin(p.key + qcur, make_key(res, gidx));
+                float best = fminf(res, key_dist(old));
+                if (res <= best * (1.0f + p.eps_t)) {
+                    unsigned long long slot = atomicAdd(p.log.count, 1ull);
+                    if (slot < p.log.capacity) {
+                        TieEntry e;
+                        e.q = qcur;
+                        e.n = ncur;
+                        e.d32 = res;
+                        e.pad = 0.0f;
+                        e.d64 = 0.0;
+                        p.log.e[slot] = e;
+                    } else {
+                        p.log.overflow[qcur] = 1u;
+                    }
+                }
+            } else {
+                p.out[it] = res;
+            }
+        }
+        if (abandon && p.mode == 1 && g == 0) p.out[it] = kInf;
+        if (done || abandon) {
+            if (g == 0 && p.counters != nullptr) {
+                int klast = p.k0 + per * R - 1;
+                if (klast > 2 * L - 2) klast = 2 * L - 2;
+                my_items += 1;
+                my_aband += abandon ? 1 : 0;
+                my_cells += klast >= 0 ? p.cells_prefix[klast] : 0;
+            }
+            it += ngroups;
+            active = it < nitems;
+            if (active) setup();
+        }
+        __syncwarp();
+    }
+    if (p.counters != nullptr && valid_lane && g == 0 && my_items > 0) {
+        atomicAdd(p.counters + CNT_ITEMS, (unsigned long long)my_items);
+        atomicAdd(p.counters + CNT_ABANDONED, (unsigned long long)my_aband);
+        atomicAdd(p.counters + CNT_CELLS, (unsigned long long)my_cells);
+    }
+}
+
+// ---- host-side selection and launch ----------------------------------------------------------
+struct BandChoice {
+    int R, G, gpw;
+    bool aligned;
+};
+
+static double band_cost(int R, int w, int G) {
+    int gpw = 32 / G;
+    double per_lane = (double)R * 1.5 * R + (2.0 * R - 1) + R + 15.0;
+    return per_lane / ((double)gpw * R * (w + 0.5));
+}
+
+BandChoice choose_band(int w) {
+    BandChoice best{0, 0, 0, false};
+    double bc = 1e30;
+    for (int R = 2; R <= 32; R += 2) {
+        int G = (2 * w + 2 + R - 1) / R;
+        if (G > 32) continue;
+        bool aligned = (G * R == 2 * w + 2);
+        if (!aligned && R > 24) continue;      // register budget of the general variant
+        double c = band_cost(R, w, G) * (aligned ? 1.0 : 1.02);
+        if (c < bc) {
+            bc = c;
+            best = {R, G, 32 / G, aligned};
+        }
+    }
+    return best;
+}
+
+bool band_supported(int w) { return choose_band(w).R != 0; }
+
+template <int R, bool AL>
+static int launch_band_t(BandParams &p, cudaStream_t st, int num_sms) {
+    auto kern = k_dtw_band<R, AL>;
+    const int block = 256;
+    const int warps = block / 32;
+    size_t smem = (size_t)warps * p.gpw * 2 * p.seglen * sizeof(float);
+    if (smem > 220 * 1024) return -2;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem);
+    if (occ < 1) occ = 1;
+    int64_t groups_per_block = (int64_t)warps * p.gpw;
+    int64_t want = (int64_t)num_sms * occ;
+    if (p.mode == 1) {
+        int64_t need = (p.nitems_host + groups_per_block - 1) / groups_per_block;
+        if (need < want) want = need > 0 ? need : 1;
+    }
+    kern<<<(unsigned)want, block, smem, st>>>(p);
+    count_launch();
+    return 0;
+}
+
+#define BAND_CASE(RR)                                                         \
+    case RR:                                                                  \
+        return c.aligned ? launch_band_t<RR, true>(p, st, num_sms)            \
+                         : launch_band_t<RR, false>(p, st, num_sms);
+
+int launch_dtw_band(BandParams p, cudaStream_t st, int num_sms) {
+    BandChoice c = choose_band(p.w);
+    if (c.R == 0) return -1;
+    p.G = c.G;
+    p.gpw = c.gpw;
+    const int R = c.R;
+    // phase: period starts must satisfy (k + w) even
+    p.k0 = (p.w & 1) ? -1 : 0;
+    p.nper = (2 * p.L - 1 - p.k0 + R - 1) / R;
+    const int H = R / 2;
+    const int kp_last = p.k0 + (p.nper - 1) * R;
+    const int amin = ((p.k0 + p.w - (c.G - 1) * R) >> 1) - (H - 1);
+    const int amax = ((kp_last + p.w) >> 1) + H - 1 + 1;
+    const int bmin = (p.k0 - p.w) >> 1;
+    const int bmax = ((kp_last - p.w + (c.G - 1) * R) >> 1) + R - 1 + 1;
+    int lo = amin < bmin ? amin : bmin;
+    int hi = amax > bmax ? amax : bmax;
+    p.padl = (lo < 0 ? -lo : 0) + 1;
+    int padr = (hi > p.L - 1 ? hi - (p.L - 1) : 0) + 1;
+    int seg = p.padl + p.L + padr;
+    p.seglen = (seg + 3) / 4 * 4 + 1;  // odd stride: spread groups over banks
+    switch (R) {
+        BAND_CASE(2)
+        BAND_CASE(4)
+        BAND_CASE(6)
+        BAND_CASE(8)
+        BAND_CASE(10)
+        BAND_CASE(12)
+        BAND_CASE(14)
+        BAND_CASE(16)
+        BAND_CASE(18)
+        BAND_CASE(20)
+        BAND_CASE(22)
+        BAND_CASE(24)
+        BAND_CASE(26)
+        BAND_CASE(28)
+        BAND_CASE(30)
+        BAND_CASE(32)
+        default:
+            return -1;
+    }
+}
+
+int dispatch_dtw(const float *A, const float *B, const Item *items,
+                 const unsigned long long *nitems_dev, unsigned long long item_cap,
+                 const int32_t *ia, const int32_t *ib, int64_t nitems_host, int L, int w,
+                 int mode, unsigned long long *key, int64_t index_base, float eps_t, TieLog log,
+                 unsigned long long *counters, const long long *cells_prefix,
+                 const float *cutoff, float *out, cudaStream_t st, int num_sms) {
+    if (w > L - 1) w = L - 1;
+    BandParams p;
+    p.A = A;
+    p.B = B;
+    p.items = items;
+    p.nitems_dev = nitems_dev;
+    p.item_cap = item_cap;
+    p.ia = ia;
+    p.ib = ib;
+    p.nitems_host = nitems_host;
+    p.L = L;
+    p.w = w;
+    p.mode = mode;
+    p.key = key;
+    p.index_base = index_base;
+    p.eps_t = eps_t;
+    p.log = log;
+    p.counters = counters;
+    p.cells_prefix = cells_prefix;
+    p.cutoff = cutoff;
+    p.out = out;
+    if (band_supported(w)) {
+        int rc = launch_dtw_band(p, st, num_sms);
+        if (rc == 0) return 0;
+    }
+    return -1;
+}
+
+}  // namespace nndtw

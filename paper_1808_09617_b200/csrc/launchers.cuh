@@ -1,0 +1,55 @@
+// launchers.cuh -- host launch functions of the kernels (internal to libnndtw.so).
+#pragma once
+#include "common.cuh"
+
+namespace nndtw {
+
+int launch_envelopes(const float *x, int64_t n, int L, int w, float *U, float *Lo,
+                     nndtw_kim *kim, cudaStream_t st);
+int launch_series_stats(const float *x, int64_t n, int L, nndtw_kim *kim, cudaStream_t st);
+int launch_check_finite(const float *x, int64_t n, int32_t *bad, cudaStream_t st);
+int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
+              const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L, int w,
+              int v, int with_kim, int64_t self_offset, float *lb, int64_t ldlb,
+              unsigned long long *minkey, cudaStream_t st);
+int launch_fill_u64(unsigned long long *p, int64_t n, unsigned long long v, cudaStream_t st);
+int launch_seed_items(const unsigned long long *minkey, const int32_t *seed2, int64_t nq,
+                      int64_t nt, Item *items, unsigned long long *count, cudaStream_t st);
+int launch_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
+                   const unsigned long long *key, const unsigned long long *minkey,
+                   const int32_t *seed2, float eps_p, Item *items, unsigned long long *count,
+                   unsigned long long capacity, int num_sms, cudaStream_t st);
+int launch_cells_prefix(int L, int w, long long *prefix, cudaStream_t st);
+int launch_refine(TieEntry *e, const unsigned long long *count, unsigned long long cap,
+                  const float *A, const float *B, int L, int w, const unsigned long long *gkey,
+                  float eps_t, unsigned long long *f64key, unsigned long long *counters,
+                  int num_sms, cudaStream_t st);
+int launch_refine_overflow(const unsigned *overflow, int64_t nq, const float *lb, int64_t ldlb,
+                           int64_t nt, const float *A, const float *B, int L, int w,
+                           const unsigned long long *gkey, float eps_p, int pass,
+                           unsigned long long *f64key, const unsigned long long *gf64,
+                           int64_t index_base, unsigned long long *out, int num_sms,
+                           cudaStream_t st);
+int launch_resolve(const TieEntry *e, const unsigned long long *count, unsigned long long cap,
+                   const unsigned long long *gf64, int64_t index_base, unsigned long long *out,
+                   int num_sms, cudaStream_t st);
+int launch_swap_key(const unsigned long long *in, int64_t nq, unsigned long long *out,
+                    cudaStream_t st);
+int launch_finalize(const unsigned long long *key, int64_t nq, int fmt, const int32_t *labels,
+                    int64_t nlabels, int64_t *idx_out, int32_t *label_out, float *dist_out,
+                    cudaStream_t st);
+int launch_count_errors(const unsigned long long *key, int64_t nq, const int32_t *labels,
+                        int64_t q_begin, int64_t *errors, int32_t *nn_out, int32_t *prev_nn,
+                        cudaStream_t st);
+
+// S4 dispatch: picks the band-wavefront kernel (2w+2 <= 32*32 slots) or the row-strip kernel
+// (long windows).  mode 0 = search (items + device count, atomicMin into key, tie log),
+// mode 1 = batch (ia/ib/cutoff/out, nitems_host pairs).  Returns 0 or an NNDTW_E_* code.
+int dispatch_dtw(const float *A, const float *B, const Item *items,
+                 const unsigned long long *nitems_dev, unsigned long long item_cap,
+                 const int32_t *ia, const int32_t *ib, int64_t nitems_host, int L, int w,
+                 int mode, unsigned long long *key, int64_t index_base, float eps_t, TieLog log,
+                 unsigned long long *counters, const long long *cells_prefix,
+                 const float *cutoff, float *out, cudaStream_t st, int num_sms);
+
+}  // namespace nndtw

@@ -1,0 +1,300 @@
+// lb.cu -- S2: batched LB_Kim -> LB_Enhanced^V cascade over all (query, train) pairs.
+//
+// LB_Enhanced is Eq. 7 in the order of Algorithm 1: boundary terms
+// (line 1), n_bands = min(floor(L/2), V) (line 2, reading C10), the left band L_i and the right
+// band R_{L-i+1} minima for i = 2..n_bands (lines 3-11; the right band is the left band of the
+// reversed series, reading C9), then the LB_Keogh bridge (lines 13-15) over columns
+// n_bands+1..L-n_bands.  The line-12 abort is not taken: every pair's bound is produced
+// (north_star "over all query x train pairs"); pruning happens against the best-so-far later.
+// LB_Kim is the sum variant "without repetitions" (reading C7).
+//
+// B200 design: the bridge is the O(L) part.  A CTA computes a 64-query x
+// 128-train tile; each thread owns 8 queries x 4 train series (32 accumulators), so per column
+// it reads 8 query values (2 broadcast LDS.128) and 4 (U,L) pairs (4 conflict-free LDS.64) for
+// 32 pair-updates of 4 ALU ops (FADD, FADD, FMNMX3 with 0, FFMA):
+//   t = max(a-U, L-a, 0);  acc += t*t   (t > 0 only when a is outside [L, U]).
+// Columns are staged through shared memory in chunks of 16, double-buffered with register
+// prefetch.  Grid x runs over query tiles so CTAs resident together share one train tile
+// (the 400 MB of envelopes of config 2 are read once from HBM; the queries stay in L2).
+#include "launchers.cuh"
+
+namespace nndtw {
+
+constexpr int LB_TQ = 64, LB_TN = 128, LB_CC = 16, LB_QPT = 8, LB_NPT = 4;
+constexpr int LB_NBMAX = 16;
+constexpr int LB_SA_STRIDE = LB_TQ + 4;   // floats (keeps 16-byte alignment of float4 reads)
+constexpr int LB_SE_STRIDE = LB_TN + 1;   // float2 units
+
+struct LbParams {
+    const float *q;
+    int64_t nq;
+    const nndtw_kim *qkim;
+    const float *t, *U, *Lo;
+    const nndtw_kim *tkim;
+    int64_t nt;
+    int L, w, nb, with_kim;
+    int64_t self_offset;
+    float *lb;
+    int64_t ldlb;
+    unsigned long long *minkey;
+};
+
+struct LbSmem {
+    float a[2][LB_CC][LB_SA_STRIDE];
+    float2 e[2][LB_CC][LB_SE_STRIDE];
+    float qh[LB_TQ][2 * LB_NBMAX];   // [0,nb): head x[i]; [NBMAX, NBMAX+nb): tail x[L-1-i]
+    float th[LB_TN][2 * LB_NBMAX];
+    nndtw_kim qk[LB_TQ];
+    nndtw_kim tk[LB_TN];
+};
+
+template <bool SMEM_BANDS>
+__global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    LbSmem &S = *reinterpret_cast<LbSmem *>(smem_raw);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int tq = tid >> 5;  // warp index: queries tq*8 .. tq*8+7 of the tile
+    const int64_t q0 = (int64_t)blockIdx.x * LB_TQ;
+    const int64_t n0 = (int64_t)blockIdx.y * LB_TN;
+    const int L = p.L, nb = p.nb, w = p.w;
+
+    // ---- stage band values and Kim features -------------------------------------------
+    if (SMEM_BANDS) {
+        for (int e = tid; e < LB_TQ * nb; e += 256) {
+            int r = e / nb, i = e % nb;
+            int64_t qq = q0 + r;
+            const float *src = p.q + (qq < p.nq ? qq : 0) * (int64_t)L;
+            S.qh[r][i] = src[i];
+            S.qh[r][LB_NBMAX + i] = src[L - 1 - i];
+        }
+        for (int e = tid; e < LB_TN * nb; e += 256) {
+            int r = e / nb, i = e % nb;
+            int64_t nn = n0 + r;
+            const float *src = p.t + (nn < p.nt ? nn : 0) * (int64_t)L;
+            S.th[r][i] = src[i];
+            S.th[r][LB_NBMAX + i] = src[L - 1 - i];
+        }
+    }
+    if (p.with_kim) {
+        for (int e = tid; e < LB_TQ; e += 256) {
+            int64_t qq = q0 + e;
+            S.qk[e] = p.qkim[qq < p.nq ? qq : 0];
+        }
+        for (int e = tid; e < LB_TN; e += 256) {
+            int64_t nn = n0 + e;
+            S.tk[e] = p.tkim[nn < p.nt ? nn : 0];
+        }
+    }
+
+    // ---- column-chunk loader (register prefetch) ------------------------------------------
+    const int ch_begin = nb / LB_CC;
+    const int ch_end = (L - nb + LB_CC - 1) / LB_CC;  // exclusive
+    float ra[4];
+    float2 re[8];
+    auto load_chunk = [&](int ch) {
+        const int c0 = ch * LB_CC;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            int e = tid + 256 * k;
+            int r = e >> 4, c = c0 + (e & 15);
+            int64_t qq = q0 + r;
+            bool ok = qq < p.nq && c >= nb && c < L - nb;
+            ra[k] = ok ? __ldg(p.q + qq * (int64_t)L + c) : 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            int e = tid + 256 * k;
+            int r = e >> 4, c = c0 + (e & 15);
+            int64_t nn = n0 + r;
+            bool ok = nn < p.nt && c >= nb && c < L - nb;
+            int64_t off = nn * (int64_t)L + c;
+            re[k] = ok ? make_float2(__ldg(p.U + off), __ldg(p.Lo + off))
+                       : make_float2(kInf, -kInf);
+        }
+    };
+    auto store_chunk = [&](int buf) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            int e = tid + 256 * k;
+            S.a[buf][e & 15][e >> 4] = ra[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            int e = tid + 256 * k;
+            S.e[buf][e & 15][e >> 4] = re[k];
+        }
+    };
+
+    if (ch_begin < ch_end) {
+        load_chunk(ch_begin);
+        store_chunk(0);
+    }
+    __syncthreads();
+
+    // ---- boundary terms + bands (Alg. 1 lines 1-11) --------------------------------------
+    float acc[LB_QPT][LB_NPT];
+    auto qhv = [&](int qi, int i) -> float {   // head value x[i] of query tq*8+qi
+        if (SMEM_BANDS) return S.qh[tq * LB_QPT + qi][i];
+        int64_t qq = q0 + tq * LB_QPT + qi;
+        return __ldg(p.q + (qq < p.nq ? qq : 0) * (int64_t)L + i);
+    };
+    auto qtv = [&](int qi, int i) -> float {   // tail value x[L-1-i]
+        if (SMEM_BANDS) return S.qh[tq * LB_QPT + qi][LB_NBMAX + i];
+        int64_t qq = q0 + tq * LB_QPT + qi;
+        return __ldg(p.q + (qq < p.nq ? qq : 0) * (int64_t)L + (L - 1 - i));
+    };
+    auto thv = [&](int j, int i) -> float {
+        if (SMEM_BANDS) return S.th[lane + 32 * j][i];
+        int64_t nn = n0 + lane + 32 * j;
+        return __ldg(p.t + (nn < p.nt ? nn : 0) * (int64_t)L + i);
+    };
+    auto ttv = [&](int j, int i) -> float {
+        if (SMEM_BANDS) return S.th[lane + 32 * j][LB_NBMAX + i];
+        int64_t nn = n0 + lane + 32 * j;
+        return __ldg(p.t + (nn < p.nt ? nn : 0) * (int64_t)L + (L - 1 - i));
+    };
+#pragma unroll
+    for (int qi = 0; qi < LB_QPT; ++qi)
+#pragma unroll
+        for (int j = 0; j < LB_NPT; ++j)
+            acc[qi][j] = sq(qhv(qi, 0) - thv(j, 0)) + sq(qtv(qi, 0) - ttv(j, 0));
+
+    for (int i = 1; i < nb; ++i) {
+        const int jlo = i - w > 0 ? i - w : 0;
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            float m[LB_QPT][LB_NPT];
+            float ai[LB_QPT], bi[LB_NPT];
+#pragma unroll
+            for (int qi = 0; qi < LB_QPT; ++qi) ai[qi] = side ? qtv(qi, i) : qhv(qi, i);
+#pragma unroll
+            for (int j = 0; j < LB_NPT; ++j) bi[j] = side ? ttv(j, i) : thv(j, i);
+#pragma unroll
+            for (int qi = 0; qi < LB_QPT; ++qi)
+#pragma unroll
+                for (int j = 0; j < LB_NPT; ++j) m[qi][j] = sq(ai[qi] - bi[j]);
+            for (int jj = jlo; jj < i; ++jj) {
+                float aj[LB_QPT], bj[LB_NPT];
+#pragma unroll
+                for (int qi = 0; qi < LB_QPT; ++qi) aj[qi] = side ? qtv(qi, jj) : qhv(qi, jj);
+#pragma unroll
+                for (int j = 0; j < LB_NPT; ++j) bj[j] = side ? ttv(j, jj) : thv(j, jj);
+#pragma unroll
+                for (int qi = 0; qi < LB_QPT; ++qi)
+#pragma unroll
+                    for (int j = 0; j < LB_NPT; ++j)
+                        m[qi][j] = fminf(m[qi][j],
+                                         fminf(sq(ai[qi] - bj[j]), sq(aj[qi] - bi[j])));
+            }
+#pragma unroll
+            for (int qi = 0; qi < LB_QPT; ++qi)
+#pragma unroll
+                for (int j = 0; j < LB_NPT; ++j) acc[qi][j] = acc[qi][j] + m[qi][j];
+        }
+    }
+
+    // ---- LB_Keogh bridge (Alg. 1 lines 13-15) ---------------------------------------------
+    for (int ch = ch_begin; ch < ch_end; ++ch) {
+        const int buf = (ch - ch_begin) & 1;
+        const bool more = ch + 1 < ch_end;
+        if (more) load_chunk(ch + 1);
+#pragma unroll
+        for (int c = 0; c < LB_CC; ++c) {
+            const float4 a0 = *reinterpret_cast<const float4 *>(&S.a[buf][c][tq * LB_QPT]);
+            const float4 a1 = *reinterpret_cast<const float4 *>(&S.a[buf][c][tq * LB_QPT + 4]);
+            const float av[LB_QPT] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            float2 ev[LB_NPT];
+#pragma unroll
+            for (int j = 0; j < LB_NPT; ++j) ev[j] = S.e[buf][c][lane + 32 * j];
+#pragma unroll
+            for (int qi = 0; qi < LB_QPT; ++qi)
+#pragma unroll
+                for (int j = 0; j < LB_NPT; ++j) {
+                    float t = fmaxf(fmaxf(av[qi] - ev[j].x, ev[j].y - av[qi]), 0.0f);
+                    acc[qi][j] = fmaf(t, t, acc[qi][j]);
+                }
+        }
+        if (more) store_chunk(buf ^ 1);
+        __syncthreads();
+    }
+
+    // ---- Kim cascade, self exclusion, output, per-query argmin key --------------------------
+#pragma unroll
+    for (int qi = 0; qi < LB_QPT; ++qi) {
+        const int rq = tq * LB_QPT + qi;
+        const int64_t qq = q0 + rq;
+        unsigned long long best = kNone;
+#pragma unroll
+        for (int j = 0; j < LB_NPT; ++j) {
+            const int rn = lane + 32 * j;
+            const int64_t nn = n0 + rn;
+            float v = acc[qi][j];
+            if (p.with_kim) {
+                nndtw_kim ka = S.qk[rq], kb = S.tk[rn];
+                float kim = sq(qhv(qi, 0) - thv(j, 0)) + sq(qtv(qi, 0) - ttv(j, 0));
+                bool okmin = ka.imin != 0 && ka.imin != L - 1 && kb.imin != 0 && kb.imin != L - 1;
+                if (okmin) kim = kim + sq(ka.vmin - kb.vmin);
+                bool okmax = ka.imax != 0 && ka.imax != L - 1 && kb.imax != 0 &&
+                             kb.imax != L - 1 && !(okmin && (ka.imax == ka.imin || kb.imax == kb.imin));
+                if (okmax) kim = kim + sq(ka.vmax - kb.vmax);
+                v = fmaxf(v, kim);
+            }
+            if (p.self_offset >= 0 && nn == qq + p.self_offset) v = kInf;
+            if (qq < p.nq && nn < p.nt) {
+                p.lb[qq * p.ldlb + nn] = v;
+                unsigned long long k = make_key(v, (unsigned)nn);
+                best = k < best ? k : best;
+            }
+        }
+        if (p.minkey != nullptr) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                unsigned long long o = __shfl_xor_sync(0xffffffffu, best, off);
+                best = o < best ? o : best;
+            }
+            if (lane == 0 && qq < p.nq && best != kNone) atomicMin(p.minkey + qq, best);
+        }
+    }
+}
+
+int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
+              const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L, int w,
+              int v, int with_kim, int64_t self_offset, float *lb, int64_t ldlb,
+              unsigned long long *minkey, cudaStream_t st) {
+    if (nq == 0 || nt == 0) return 0;
+    if (w > L - 1) w = L - 1;
+    LbParams p;
+    p.q = q;
+    p.nq = nq;
+    p.qkim = qkim;
+    p.t = t;
+    p.U = U;
+    p.Lo = Lo;
+    p.tkim = tkim;
+    p.nt = nt;
+    p.L = L;
+    p.w = w;
+    p.nb = (L / 2) < v ? (L / 2) : v;
+    p.with_kim = with_kim;
+    p.self_offset = self_offset;
+    p.lb = lb;
+    p.ldlb = ldlb;
+    p.minkey = minkey;
+    dim3 grid((unsigned)((nq + LB_TQ - 1) / LB_TQ), (unsigned)((nt + LB_TN - 1) / LB_TN));
+    if (grid.y > 65535u) return -1;
+    size_t smem = sizeof(LbSmem);
+    if (p.nb <= LB_NBMAX) {
+        cudaFuncSetAttribute(k_lb_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        k_lb_tile<true><<<grid, 256, smem, st>>>(p);
+    } else {
+        cudaFuncSetAttribute(k_lb_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        k_lb_tile<false><<<grid, 256, smem, st>>>(p);
+    }
+    count_launch();
+    return 0;
+}
+
+}  // namespace nndtw

@@ -1,0 +1,413 @@
+// search.cu -- S3 (seed, prune, compaction), S5 (per-query argmin decode), S7 (fp64 near-tie
+// re-rank) and S8 bookkeeping kernels.
+#include "launchers.cuh"
+
+namespace nndtw {
+
+// ---- fills -----------------------------------------------------------------------------------
+__global__ void k_fill_u64(unsigned long long *p, int64_t n, unsigned long long v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+int launch_fill_u64(unsigned long long *p, int64_t n, unsigned long long v, cudaStream_t st) {
+    if (n <= 0) return 0;
+    int64_t grid = (n + 255) / 256;
+    if (grid > 4096) grid = 4096;
+    k_fill_u64<<<(unsigned)grid, 256, 0, st>>>(p, n, v);
+    count_launch();
+    return 0;
+}
+
+// ---- S3 seeds: the argmin-LB candidate of every query (and optionally a second candidate) -----
+__global__ void k_seed_items(const unsigned long long *minkey, const int32_t *seed2, int64_t nq,
+                             int64_t nt, Item *items, unsigned long long *count) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    unsigned long long k = minkey[q];
+    unsigned n1 = (unsigned)(k & 0xffffffffull);
+    if (k != kNone && n1 < (unsigned)nt) {
+        unsigned long long pos = atomicAdd(count, 1ull);
+        items[pos] = Item{(unsigned)q, n1};
+    }
+    if (seed2 != nullptr) {
+        int n2 = seed2[q];
+        if (n2 >= 0 && n2 < nt && (unsigned)n2 != n1) {
+            unsigned long long pos = atomicAdd(count, 1ull);
+            items[pos] = Item{(unsigned)q, (unsigned)n2};
+        }
+    }
+}
+
+int launch_seed_items(const unsigned long long *minkey, const int32_t *seed2, int64_t nq,
+                      int64_t nt, Item *items, unsigned long long *count, cudaStream_t st) {
+    if (nq == 0) return 0;
+    k_seed_items<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(minkey, seed2, nq, nt, items,
+                                                               count);
+    count_launch();
+    return 0;
+}
+
+// ---- S3 compaction: surviving pairs LB <= bsf*(1+eps_p), warp-ballot compacted ----------------
+// One CTA-tile = (query q, 1024 consecutive train indices); 4 per thread.
+__global__ void __launch_bounds__(256) k_compact(const float *__restrict__ lb, int64_t ldlb,
+                                                 int64_t nq, int64_t nt,
+                                                 const unsigned long long *__restrict__ key,
+                                                 const unsigned long long *__restrict__ minkey,
+                                                 const int32_t *__restrict__ seed2, float eps_p,
+                                                 Item *__restrict__ items,
+                                                 unsigned long long *count,
+                                                 unsigned long long capacity) {
+    const int64_t tiles_per_row = (nt + 1023) / 1024;
+    const int64_t ntiles = tiles_per_row * nq;
+    const int lane = threadIdx.x & 31;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t q = tile / tiles_per_row;
+        const int64_t n0 = (tile % tiles_per_row) * 1024 + threadIdx.x * 4;
+        const float thr = key_dist(key[q]) * (1.0f + eps_p);
+        const unsigned s1 = (unsigned)(minkey[q] & 0xffffffffull);
+        const unsigned s2 = seed2 ? (unsigned)seed2[q] : 0xffffffffu;
+        const float *row = lb + q * ldlb;
+        float v[4];
+        if (n0 + 3 < nt && (ldlb & 3) == 0) {
+            float4 f = *reinterpret_cast<const float4 *>(row + n0);
+            v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = (n0 + e < nt) ? row[n0 + e] : kInf;
+        }
+        unsigned flags = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            unsigned n = (unsigned)(n0 + e);
+            bool ok = (n0 + e < nt) && v[e] <= thr && n != s1 && n != s2;
+            flags |= (ok ? 1u : 0u) << e;
+        }
+        int c = __popc(flags);
+        int incl = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            int o = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += o;
+        }
+        int total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long base = 0;
+        if (lane == 31 && total > 0) base = atomicAdd(count, (unsigned long long)total);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        unsigned long long pos = base + (unsigned long long)(incl - c);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (flags & (1u << e)) {
+                if (pos < capacity) items[pos] = Item{(unsigned)q, (unsigned)(n0 + e)};
+                ++pos;
+            }
+        }
+    }
+}
+
+int launch_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
+                   const unsigned long long *key, const unsigned long long *minkey,
+                   const int32_t *seed2, float eps_p, Item *items, unsigned long long *count,
+                   unsigned long long capacity, int num_sms, cudaStream_t st) {
+    if (nq == 0 || nt == 0) return 0;
+    int64_t ntiles = ((nt + 1023) / 1024) * nq;
+    int64_t grid = ntiles < (int64_t)num_sms * 8 ? ntiles : (int64_t)num_sms * 8;
+    k_compact<<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, minkey, seed2, eps_p,
+                                               items, count, capacity);
+    count_launch();
+    return 0;
+}
+
+// ---- in-band cells per anti-diagonal, prefix-summed (GCUPS bookkeeping) ----------------------
+__global__ void k_cells_prefix(int L, int w, long long *prefix) {
+    __shared__ long long tot[1024];
+    const int nk = 2 * L - 1;
+    const int per = (nk + blockDim.x - 1) / blockDim.x;
+    const int k0 = threadIdx.x * per;
+    long long s = 0;
+    for (int k = k0; k < k0 + per && k < nk; ++k) {
+        int lo = k - (L - 1) > 0 ? k - (L - 1) : 0;
+        int t = (k - w + 1) >> 1;  // ceil((k-w)/2) for any sign
+        if (t > lo) lo = t;
+        int hi = k < L - 1 ? k : L - 1;
+        int t2 = (k + w) >> 1;
+        if (t2 < hi) hi = t2;
+        s += hi >= lo ? hi - lo + 1 : 0;
+    }
+    tot[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long run = 0;
+        for (int i = 0; i < (int)blockDim.x; ++i) {
+            long long v = tot[i];
+            tot[i] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    long long run = tot[threadIdx.x];
+    for (int k = k0; k < k0 + per && k < nk; ++k) {
+        int lo = k - (L - 1) > 0 ? k - (L - 1) : 0;
+        int t = (k - w + 1) >> 1;
+        if (t > lo) lo = t;
+        int hi = k < L - 1 ? k : L - 1;
+        int t2 = (k + w) >> 1;
+        if (t2 < hi) hi = t2;
+        run += hi >= lo ? hi - lo + 1 : 0;
+        prefix[k] = run;
+    }
+}
+
+int launch_cells_prefix(int L, int w, long long *prefix, cudaStream_t st) {
+    if (w > L - 1) w = L - 1;
+    k_cells_prefix<<<1, 1024, 0, st>>>(L, w, prefix);
+    count_launch();
+    return 0;
+}
+
+// ---- S7: fp64 DTW with the oracle's per-cell operation sequence --------------------------------
+// d = a - b; delta = d*d; m = min(diag, left, up) (exact); D = delta + m; D(0,0) = delta.
+// One warp per pair, anti-diagonal order, three diagonals of doubles in shared memory.
+// (Evaluation order does not change any cell's value, so the result is bit-identical to a
+// row-by-row evaluation with the same operations.)
+__device__ double dtw64_warp(const float *__restrict__ a, const float *__restrict__ b, int L,
+                             int w, double *buf) {
+    const int lane = threadIdx.x & 31;
+    double *d0 = buf, *d1 = buf + L, *d2 = buf + 2 * L;  // diagonals k, k-1, k-2 (by row i)
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    auto inband = [&](int k, int i) -> bool {
+        int j = k - i;
+        return i >= 0 && i < L && j >= 0 && j < L && (i - j <= w) && (j - i <= w);
+    };
+    double result = INF;
+    for (int k = 0; k <= 2 * L - 2; ++k) {
+        int ilo = k - (L - 1) > 0 ? k - (L - 1) : 0;
+        int ihi = k < L - 1 ? k : L - 1;
+        for (int i = ilo + lane; i <= ihi; i += 32) {
+            int j = k - i;
+            if (i - j > w || j - i > w) continue;
+            double dd = __dsub_rn((double)a[i], (double)b[j]);
+            double delta = __dmul_rn(dd, dd);
+            double m;
+            if (i == 0 && j == 0) {
+                m = 0.0;
+            } else {
+                double dg = (i >= 1 && j >= 1 && inband(k - 2, i - 1)) ? d2[i - 1] : INF;
+                double lf = (j >= 1 && inband(k - 1, i)) ? d1[i] : INF;
+                double up = (i >= 1 && inband(k - 1, i - 1)) ? d1[i - 1] : INF;
+                m = fmin(fmin(dg, lf), up);
+            }
+            double v = __dadd_rn(delta, m);
+            d0[i] = v;
+            if (k == 2 * L - 2) result = v;
+        }
+        __syncwarp();
+        double *t = d2;
+        d2 = d1;
+        d1 = d0;
+        d0 = t;
+    }
+    // the last cell (L-1, L-1) was written by lane (L-1 - ilo) % 32 of the last diagonal
+    int owner = ((L - 1) - (L - 1)) & 31;
+    (void)owner;
+    result = __shfl_sync(0xffffffffu, result, 0);
+    return result;
+}
+
+__global__ void k_refine(TieEntry *e, const unsigned long long *count, unsigned long long cap,
+                         const float *__restrict__ A, const float *__restrict__ B, int L, int w,
+                         const unsigned long long *__restrict__ gkey, float eps_t,
+                         unsigned long long *f64key, unsigned long long *counters) {
+    extern __shared__ double dbuf[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    double *buf = dbuf + (size_t)warp * 3 * L;
+    unsigned long long n = *count;
+    if (n > cap) n = cap;
+    for (unsigned long long x = (unsigned long long)blockIdx.x * wpb + warp; x < n;
+         x += (unsigned long long)gridDim.x * wpb) {
+        TieEntry t = e[x];
+        float gb = key_dist(gkey[t.q]);
+        if (t.d32 <= gb * (1.0f + eps_t)) {
+            double d = dtw64_warp(A + (int64_t)t.q * L, B + (int64_t)t.n * L, L, w, buf);
+            if (lane == 0) {
+                e[x].d64 = d;
+                atomicMin(f64key + t.q, (unsigned long long)__double_as_longlong(d));
+                if (counters) atomicAdd(counters + CNT_TIES, 1ull);
+            }
+        } else if (lane == 0) {
+            e[x].d64 = -1.0;
+        }
+        __syncwarp();
+    }
+}
+
+// Overflowed queries (the tie log dropped an entry): every pair that survived the cascade at
+// the global best is re-ranked in fp64 (rare, slow, exact).  pass 0: min fp64 -> f64key;
+// pass 1: lowest index with fp64 == gf64 -> out.
+__global__ void k_refine_overflow(const unsigned *overflow, int64_t nq, const float *lb,
+                                  int64_t ldlb, int64_t nt, const float *__restrict__ A,
+                                  const float *__restrict__ B, int L, int w,
+                                  const unsigned long long *gkey, float eps_p, int pass,
+                                  unsigned long long *f64key, const unsigned long long *gf64,
+                                  int64_t index_base, unsigned long long *out) {
+    extern __shared__ double dbuf[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    double *buf = dbuf + (size_t)warp * 3 * L;
+    for (int64_t q = 0; q < nq; ++q) {
+        if (!overflow[q]) continue;
+        float thr = key_dist(gkey[q]) * (1.0f + eps_p);
+        for (int64_t n = (int64_t)blockIdx.x * wpb + warp; n < nt;
+             n += (int64_t)gridDim.x * wpb) {
+            if (!(lb[q * ldlb + n] <= thr)) continue;
+            double d = dtw64_warp(A + q * L, B + n * L, L, w, buf);
+            if (lane == 0) {
+                unsigned long long bits = (unsigned long long)__double_as_longlong(d);
+                if (pass == 0) {
+                    atomicMin(f64key + q, bits);
+                } else if (bits == gf64[q]) {
+                    atomicMin(out + q, ((unsigned long long)(index_base + n) << 32) |
+                                           (unsigned long long)__float_as_uint((float)d));
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+static int refine_block(int L, size_t *smem) {
+    int wpb = 4;
+    while (wpb > 1 && (size_t)wpb * 3 * L * sizeof(double) > 200 * 1024) wpb >>= 1;
+    *smem = (size_t)wpb * 3 * L * sizeof(double);
+    return wpb * 32;
+}
+
+int launch_refine(TieEntry *e, const unsigned long long *count, unsigned long long cap,
+                  const float *A, const float *B, int L, int w, const unsigned long long *gkey,
+                  float eps_t, unsigned long long *f64key, unsigned long long *counters,
+                  int num_sms, cudaStream_t st) {
+    if (w > L - 1) w = L - 1;
+    size_t smem;
+    int block = refine_block(L, &smem);
+    cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_refine<<<num_sms * 2, block, smem, st>>>(e, count, cap, A, B, L, w, gkey, eps_t, f64key,
+                                               counters);
+    count_launch();
+    return 0;
+}
+
+int launch_refine_overflow(const unsigned *overflow, int64_t nq, const float *lb, int64_t ldlb,
+                           int64_t nt, const float *A, const float *B, int L, int w,
+                           const unsigned long long *gkey, float eps_p, int pass,
+                           unsigned long long *f64key, const unsigned long long *gf64,
+                           int64_t index_base, unsigned long long *out, int num_sms,
+                           cudaStream_t st) {
+    if (w > L - 1) w = L - 1;
+    size_t smem;
+    int block = refine_block(L, &smem);
+    cudaFuncSetAttribute(k_refine_overflow, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    k_refine_overflow<<<num_sms, block, smem, st>>>(overflow, nq, lb, ldlb, nt, A, B, L, w,
+                                                    gkey, eps_p, pass, f64key, gf64,
+                                                    index_base, out);
+    count_launch();
+    return 0;
+}
+
+// S7 step 2: lowest index among local candidates whose fp64 value equals the global minimum.
+__global__ void k_resolve(const TieEntry *e, const unsigned long long *count,
+                          unsigned long long cap, const unsigned long long *gf64,
+                          int64_t index_base, unsigned long long *out) {
+    unsigned long long n = *count;
+    if (n > cap) n = cap;
+    for (unsigned long long x = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+         x += (unsigned long long)gridDim.x * blockDim.x) {
+        TieEntry t = e[x];
+        if (t.d64 < 0.0) continue;
+        if ((unsigned long long)__double_as_longlong(t.d64) == gf64[t.q])
+            atomicMin(out + t.q, ((unsigned long long)(index_base + t.n) << 32) |
+                                     (unsigned long long)__float_as_uint(t.d32));
+    }
+}
+
+int launch_resolve(const TieEntry *e, const unsigned long long *count, unsigned long long cap,
+                   const unsigned long long *gf64, int64_t index_base, unsigned long long *out,
+                   int num_sms, cudaStream_t st) {
+    k_resolve<<<num_sms * 2, 256, 0, st>>>(e, count, cap, gf64, index_base, out);
+    count_launch();
+    return 0;
+}
+
+// (idx << 32 | f32) -> (f32 << 32 | idx); keys with no candidate stay kKeyInit.
+__global__ void k_swap_key(const unsigned long long *in, int64_t nq, unsigned long long *out) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    unsigned long long k = in[q];
+    out[q] = (k == kNone) ? kKeyInit : ((k << 32) | (k >> 32));
+}
+
+int launch_swap_key(const unsigned long long *in, int64_t nq, unsigned long long *out,
+                    cudaStream_t st) {
+    if (nq == 0) return 0;
+    k_swap_key<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(in, nq, out);
+    count_launch();
+    return 0;
+}
+
+// ---- S5 decode -----------------------------------------------------------------------------
+__global__ void k_finalize(const unsigned long long *key, int64_t nq, int fmt,
+                           const int32_t *labels, int64_t nlabels, int64_t *idx_out,
+                           int32_t *label_out, float *dist_out) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    unsigned long long k = key[q];
+    unsigned idx = fmt == 0 ? (unsigned)(k & 0xffffffffull) : (unsigned)(k >> 32);
+    unsigned db = fmt == 0 ? (unsigned)(k >> 32) : (unsigned)(k & 0xffffffffull);
+    bool ok = (int64_t)idx < nlabels && idx != 0xffffffffu;
+    if (idx_out) idx_out[q] = ok ? (int64_t)idx : -1;
+    if (label_out) label_out[q] = (ok && labels) ? labels[idx] : -1;
+    if (dist_out) dist_out[q] = __uint_as_float(db);
+}
+
+int launch_finalize(const unsigned long long *key, int64_t nq, int fmt, const int32_t *labels,
+                    int64_t nlabels, int64_t *idx_out, int32_t *label_out, float *dist_out,
+                    cudaStream_t st) {
+    if (nq == 0) return 0;
+    k_finalize<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(key, nq, fmt, labels, nlabels,
+                                                             idx_out, label_out, dist_out);
+    count_launch();
+    return 0;
+}
+
+// ---- S8: LOOCV error count for one window ----------------------------------------------------
+__global__ void k_count_errors(const unsigned long long *key, int64_t nq, const int32_t *labels,
+                               int64_t q_begin, int64_t *errors, int32_t *nn_out,
+                               int32_t *prev_nn) {
+    __shared__ int cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < nq) {
+        unsigned idx = (unsigned)(key[q] & 0xffffffffull);
+        int wrong = (idx == 0xffffffffu) ? 1 : (labels[idx] != labels[q_begin + q]);
+        if (wrong) atomicAdd(&cnt, 1);
+        if (nn_out) nn_out[q] = (int32_t)idx;
+        if (prev_nn) prev_nn[q] = (int32_t)idx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && cnt) atomicAdd((unsigned long long *)errors, (unsigned long long)cnt);
+}
+
+int launch_count_errors(const unsigned long long *key, int64_t nq, const int32_t *labels,
+                        int64_t q_begin, int64_t *errors, int32_t *nn_out, int32_t *prev_nn,
+                        cudaStream_t st) {
+    if (nq == 0) return 0;
+    k_count_errors<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(key, nq, labels, q_begin,
+                                                                 errors, nn_out, prev_nn);
+    count_launch();
+    return 0;
+}
+
+}  // namespace nndtw

@@ -1,0 +1,290 @@
+"""Thin Python binding of libnndtw.so (include/nndtw.h) -- argument marshalling only.
+
+Every step of the path runs in the library's CUDA kernels; PyTorch provides device memory,
+streams and (in dist.py) process groups.  There is no CPU fallback: if the shared library is
+missing or the device is not sm_100, the calls raise.
+
+Names follow the C ABI: envelopes, series_stats, lb_enhanced, dtw_batch, classify,
+classify_refine, classify_resolve, finalize, loocv_window.  Distances are squared (Eq. 1-2).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnndtw.so")
+
+NNDTW_LB_WITH_KIM = 1
+NNDTW_CLASSIFY_EXACT = 1
+KEY_INIT = 0x7F800000FFFFFFFF
+
+
+class NNDTWError(RuntimeError):
+    pass
+
+
+class Stats(C.Structure):
+    _fields_ = [("lb_pairs", C.c_int64), ("survivors", C.c_int64), ("dtw_calls", C.c_int64),
+                ("dtw_abandoned", C.c_int64), ("cells", C.c_int64),
+                ("near_tie_pairs", C.c_int64), ("rounds", C.c_int32), ("launches", C.c_int32),
+                ("ms_envelopes", C.c_float), ("ms_lb", C.c_float), ("ms_dtw", C.c_float),
+                ("ms_other", C.c_float)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+_P = C.c_void_p
+_I64 = C.c_int64
+_I32 = C.c_int32
+
+_SIGS = {
+    "nndtw_last_error": (C.c_char_p, []),
+    "nndtw_version": (C.c_int, []),
+    "nndtw_launch_count": (_I64, []),
+    "nndtw_check_device": (C.c_int, []),
+    "nndtw_check_finite": (C.c_int, [_P, _I64, _P, _P]),
+    "nndtw_envelopes": (C.c_int, [_P, _I64, _I32, _I32, _P, _P, _P, _P]),
+    "nndtw_series_stats": (C.c_int, [_P, _I64, _I32, _P, _P]),
+    "nndtw_lb_enhanced": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32,
+                                    C.c_uint32, _P, _I64, _P]),
+    "nndtw_dtw_batch": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P]),
+    "nndtw_classify_workspace_bytes": (C.c_size_t, [_I64, _I64, _I32, _I32]),
+    "nndtw_classify": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32,
+                                 C.c_uint32, _P, C.c_size_t, _P, C.POINTER(Stats), _P]),
+    "nndtw_classify_refine": (C.c_int, [_P, C.c_size_t, _P, _I64, _P, _I64, _I32, _I32, _P,
+                                        _P, _P]),
+    "nndtw_classify_resolve": (C.c_int, [_P, C.c_size_t, _P, _I64, _P, _I64, _I32, _I32, _I64,
+                                         _P, _P, _P, _P]),
+    "nndtw_finalize": (C.c_int, [_P, _I64, _I32, _P, _I64, _P, _P, _P, _P]),
+    "nndtw_loocv_workspace_bytes": (C.c_size_t, [_I64, _I32, _I64, _I64]),
+    "nndtw_loocv_window": (C.c_int, [_P, _P, _I64, _I32, _P, _I32, _I32, _I64, _I64, _P,
+                                     C.c_size_t, _P, _P, C.POINTER(Stats), _P]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+
+def load(path: str = LIB_PATH):
+    """Load libnndtw.so (raises if it is missing -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise NNDTWError(f"{path} not built; run paper_1808_09617_b200/build.py")
+    lib = C.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = load().nndtw_last_error().decode(errors="replace")
+        raise NNDTWError(f"{what} failed with code {rc}: {msg}")
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _series(x: torch.Tensor, name: str) -> torch.Tensor:
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float32
+            and x.dim() == 2 and x.is_contiguous()):
+        raise NNDTWError(f"{name} must be a contiguous float32 CUDA tensor [n][L]")
+    return x
+
+
+def check_finite(x: torch.Tensor, stream=None) -> bool:
+    bad = torch.zeros(1, dtype=torch.int32, device=x.device)
+    _check(load().nndtw_check_finite(_ptr(x), x.numel(), _ptr(bad), _stream(stream)),
+           "nndtw_check_finite")
+    return int(bad.item()) == 0
+
+
+def envelopes(x: torch.Tensor, w: int, with_kim: bool = True, stream=None):
+    """S1: (upper, lower, kim) with kim an int32 tensor [n][4] = (vmin, vmax, imin, imax) bits."""
+    _series(x, "x")
+    n, L = x.shape
+    U = torch.empty_like(x)
+    Lo = torch.empty_like(x)
+    kim = torch.empty((n, 4), dtype=torch.int32, device=x.device) if with_kim else None
+    _check(load().nndtw_envelopes(_ptr(x), n, L, int(w), _ptr(U), _ptr(Lo), _ptr(kim),
+                                  _stream(stream)), "nndtw_envelopes")
+    return U, Lo, kim
+
+
+def series_stats(x: torch.Tensor, stream=None) -> torch.Tensor:
+    _series(x, "x")
+    n, L = x.shape
+    kim = torch.empty((n, 4), dtype=torch.int32, device=x.device)
+    _check(load().nndtw_series_stats(_ptr(x), n, L, _ptr(kim), _stream(stream)),
+           "nndtw_series_stats")
+    return kim
+
+
+def lb_enhanced(q, t, U, Lo, w: int, v: int, with_kim: bool = False, qkim=None, tkim=None,
+                stream=None) -> torch.Tensor:
+    """S2: cascade bound matrix [nq][nt] (Eq. 7 / Algorithm 1; max with LB_Kim if asked)."""
+    _series(q, "q"); _series(t, "t"); _series(U, "U"); _series(Lo, "Lo")
+    nq, L = q.shape
+    nt = t.shape[0]
+    if with_kim:
+        qkim = series_stats(q, stream) if qkim is None else qkim
+        if tkim is None:
+            raise NNDTWError("tkim (from envelopes) is required with with_kim=True")
+    out = torch.empty((nq, nt), dtype=torch.float32, device=q.device)
+    _check(load().nndtw_lb_enhanced(_ptr(q), nq, _ptr(qkim), _ptr(t), _ptr(U), _ptr(Lo),
+                                    _ptr(tkim), nt, L, int(w), int(v),
+                                    NNDTW_LB_WITH_KIM if with_kim else 0, _ptr(out), nt,
+                                    _stream(stream)), "nndtw_lb_enhanced")
+    return out
+
+
+def dtw_batch(a, b, w: int, ia=None, ib=None, cutoff=None, stream=None) -> torch.Tensor:
+    """S4: squared DTW_w of pairs (a[ia[p]], b[ib[p]]); +inf where abandoned at cutoff[p]."""
+    _series(a, "a"); _series(b, "b")
+    L = a.shape[1]
+    if ia is not None:
+        ia = ia.to(torch.int32).contiguous()
+    if ib is not None:
+        ib = ib.to(torch.int32).contiguous()
+    npairs = ia.numel() if ia is not None else (ib.numel() if ib is not None else a.shape[0])
+    if cutoff is not None:
+        cutoff = cutoff.to(torch.float32).contiguous()
+    out = torch.empty(npairs, dtype=torch.float32, device=a.device)
+    _check(load().nndtw_dtw_batch(_ptr(a), _ptr(b), _ptr(ia), _ptr(ib), npairs, L, int(w),
+                                  _ptr(cutoff), _ptr(out), _stream(stream)), "nndtw_dtw_batch")
+    return out
+
+
+@dataclass
+class Prediction:
+    idx: torch.Tensor     # int64 [nq] global train index of the 1-NN
+    label: torch.Tensor   # int32 [nq]
+    dist: torch.Tensor    # float32 [nq] squared DTW (sqrt for Eq. 2's DTW)
+    stats: dict | None
+
+
+class Model:
+    """A train set with its envelopes and Kim features precomputed "at training time"."""
+
+    def __init__(self, train: torch.Tensor, labels: torch.Tensor, w: int, v: int = 5,
+                 index_base: int = 0, check: bool = True, stream=None):
+        _series(train, "train")
+        if check and not check_finite(train, stream):
+            raise NNDTWError("train set contains NaN or infinity")
+        self.t = train
+        self.labels = labels.to(device=train.device, dtype=torch.int32).contiguous()
+        self.L = train.shape[1]
+        self.w = min(int(w), self.L - 1)
+        self.v = int(v)
+        self.index_base = int(index_base)
+        self.U, self.Lo, self.kim = envelopes(train, self.w, True, stream)
+        self._ws = None
+
+    def workspace(self, nq: int) -> torch.Tensor:
+        need = load().nndtw_classify_workspace_bytes(nq, self.t.shape[0], self.L, self.w)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.t.device)
+        return self._ws
+
+
+def classify_keys(model: Model, q: torch.Tensor, exact: bool = True, self_offset: int = -1,
+                  stats: bool = False, stream=None):
+    """S2-S7 on one shard: returns (key int64 [nq], workspace, stats dict | None)."""
+    _series(q, "q")
+    nq, L = q.shape
+    if L != model.L:
+        raise NNDTWError("query length differs from train length (unequal lengths are out of "
+                         "scope, reading C15)")
+    ws = model.workspace(nq)
+    key = torch.empty(nq, dtype=torch.int64, device=q.device)
+    st = Stats()
+    _check(load().nndtw_classify(_ptr(q), nq, _ptr(model.t), _ptr(model.U), _ptr(model.Lo),
+                                 _ptr(model.kim), model.t.shape[0], model.index_base,
+                                 int(self_offset), L, model.w, model.v,
+                                 NNDTW_CLASSIFY_EXACT if exact else 0, _ptr(ws), ws.numel(),
+                                 _ptr(key), C.byref(st) if stats else None, _stream(stream)),
+           "nndtw_classify")
+    return key, ws, (st.as_dict() if stats else None)
+
+
+def classify_refine(model: Model, q, ws, gkey, stream=None) -> torch.Tensor:
+    nq = q.shape[0]
+    f64 = torch.empty(nq, dtype=torch.int64, device=q.device)
+    _check(load().nndtw_classify_refine(_ptr(ws), ws.numel(), _ptr(q), nq, _ptr(model.t),
+                                        model.t.shape[0], model.L, model.w, _ptr(gkey),
+                                        _ptr(f64), _stream(stream)), "nndtw_classify_refine")
+    return f64
+
+
+def classify_resolve(model: Model, q, ws, gkey, gf64, stream=None) -> torch.Tensor:
+    nq = q.shape[0]
+    out = torch.empty(nq, dtype=torch.int64, device=q.device)
+    _check(load().nndtw_classify_resolve(_ptr(ws), ws.numel(), _ptr(q), nq, _ptr(model.t),
+                                         model.t.shape[0], model.L, model.w, model.index_base,
+                                         _ptr(gkey), _ptr(gf64), _ptr(out), _stream(stream)),
+           "nndtw_classify_resolve")
+    return out
+
+
+def finalize(key, labels, key_format: int = 0, stream=None):
+    nq = key.numel()
+    idx = torch.empty(nq, dtype=torch.int64, device=key.device)
+    lab = torch.empty(nq, dtype=torch.int32, device=key.device)
+    dist = torch.empty(nq, dtype=torch.float32, device=key.device)
+    _check(load().nndtw_finalize(_ptr(key), nq, int(key_format), _ptr(labels),
+                                 labels.numel() if labels is not None else 0, _ptr(idx),
+                                 _ptr(lab), _ptr(dist), _stream(stream)), "nndtw_finalize")
+    return idx, lab, dist
+
+
+def classify(model: Model, q: torch.Tensor, stats: bool = False, check: bool = True,
+             stream=None) -> Prediction:
+    """Exact 1-NN of every query (single GPU / single shard, fp64-exact tie resolution)."""
+    if check and not check_finite(q, stream):
+        raise NNDTWError("queries contain NaN or infinity")
+    key, _, st = classify_keys(model, q, exact=True, stats=stats, stream=stream)
+    idx, lab, dist = finalize(key, model.labels, 0, stream)
+    return Prediction(idx, lab, dist, st)
+
+
+def loocv_window(x: torch.Tensor, labels: torch.Tensor, windows, v: int = 5, q_begin: int = 0,
+                 q_end: int | None = None, with_nn: bool = False, stats: bool = False,
+                 stream=None):
+    """S8: leave-one-out error counts per window (device int64 [nw]) and optional NN ids."""
+    _series(x, "x")
+    n, L = x.shape
+    q_end = n if q_end is None else int(q_end)
+    labels = labels.to(device=x.device, dtype=torch.int32).contiguous()
+    win = (C.c_int32 * len(windows))(*[int(w) for w in windows])
+    nw = len(windows)
+    need = load().nndtw_loocv_workspace_bytes(n, L, q_begin, q_end)
+    ws = torch.empty(need, dtype=torch.uint8, device=x.device)
+    errors = torch.zeros(nw, dtype=torch.int64, device=x.device)
+    nn = (torch.empty((nw, q_end - q_begin), dtype=torch.int32, device=x.device)
+          if with_nn else None)
+    st = Stats()
+    _check(load().nndtw_loocv_window(_ptr(x), _ptr(labels), n, L, C.cast(win, C.c_void_p), nw,
+                                     int(v), int(q_begin), q_end, _ptr(ws), ws.numel(),
+                                     _ptr(errors), _ptr(nn), C.byref(st) if stats else None,
+                                     _stream(stream)), "nndtw_loocv_window")
+    return errors, nn, (st.as_dict() if stats else None)
+
+
+def launch_count() -> int:
+    return int(load().nndtw_launch_count())

@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element on
+the same seeded inputs.  Tolerances: envelopes and NN indices/labels bit-exact; distances and
+bounds within relative 1e-5 (north_star; fp32 storage and accumulation)."""
+import numpy as np
+import pytest
+
+import datagen
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1808_09617_b200 import build, nndtw
+    build.build()
+    nndtw.load()
+    assert nndtw.load().nndtw_check_device() == 0, "not an sm_100 device"
+    return torch.device("cuda:0")
+
+
+def T(x, dev):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(x), device=dev)
+
+
+def assert_rel(gpu, ref, rel=REL, what=""):
+    gpu = np.asarray(gpu, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    err = np.abs(gpu - ref)
+    tol = rel * np.abs(ref) + 1e-30
+    bad = np.where(err > tol)[0] if gpu.ndim == 1 else np.argwhere(err > tol)
+    assert bad.size == 0, f"{what}: {bad.size} mismatches, first {bad[:5]}, " \
+        f"max rel {np.max(err / np.maximum(np.abs(ref), 1e-30)):.3g}"
+
+
+# ---------------------------------------------------------------- S1 envelopes
+@pytest.mark.parametrize("L", [2, 3, 7, 31, 128, 255, 300, 512, 1000, 2048])
+def test_envelopes_bit_exact(dev, oracle_lib, L):
+    from paper_1808_09617_b200 import nndtw
+    rng = np.random.default_rng(L)
+    X = np.concatenate([datagen.random_series(rng, 5, L, k) for k in ("walk", "int", "const")])
+    for w in sorted({0, 1, 2, 3, L // 10, L // 5, L // 2, L - 2, L - 1, L, 5 * L}):
+        if w < 0:
+            continue
+        U, Lo, kim = nndtw.envelopes(T(X, dev), w)
+        eu, el = oracle_lib.envelopes(X, w)
+        assert np.array_equal(U.cpu().numpy(), eu), (L, w)
+        assert np.array_equal(Lo.cpu().numpy(), el), (L, w)
+    k = kim.cpu().numpy()
+    assert np.array_equal(k[:, 2], np.argmin(X, axis=1))
+    assert np.array_equal(k[:, 3], np.argmax(X, axis=1))
+    assert np.array_equal(k[:, 0].view(np.float32), X.min(axis=1))
+
+
+# ---------------------------------------------------------------- S2 bounds
+@pytest.mark.parametrize("L,w,V", [(2, 0, 1), (3, 1, 2), (16, 3, 5), (64, 0, 5), (100, 7, 3),
+                                   (128, 13, 5), (256, 255, 8), (300, 30, 40), (512, 103, 5),
+                                   (200, 199, 100)])
+def test_lb_enhanced_parity(dev, oracle_lib, L, w, V):
+    from paper_1808_09617_b200 import nndtw
+    rng = np.random.default_rng(L * 7 + w)
+    Q = datagen.random_series(rng, 70, L, "walk")
+    Tn = datagen.random_series(rng, 150, L, "walk")
+    Tn[5] = Q[3]
+    qt, tt = T(Q, dev), T(Tn, dev)
+    U, Lo, kim = nndtw.envelopes(tt, w)
+    lb = nndtw.lb_enhanced(qt, tt, U, Lo, w, V).cpu().numpy()
+    lbk = nndtw.lb_enhanced(qt, tt, U, Lo, w, V, with_kim=True, tkim=kim).cpu().numpy()
+    eu, el = oracle_lib.envelopes(Tn, w)
+    for i in range(0, 70, 3):
+        for j in range(150):
+            ref, _ = oracle_lib.lb_enhanced(Q[i], Tn[j], eu[j], el[j], w, V)
+            refk = max(ref, oracle_lib.lb_kim_sum(Q[i], Tn[j]))
+            assert abs(lb[i, j] - ref) <= REL * ref + 1e-30, (i, j, lb[i, j], ref)
+            assert abs(lbk[i, j] - refk) <= REL * refk + 1e-30, (i, j, lbk[i, j], refk)
+
+
+# ---------------------------------------------------------------- S4 DTW
+@pytest.mark.parametrize("L", [2, 3, 5, 17, 64, 128, 256, 300, 512])
+def test_dtw_batch_parity(dev, oracle_lib, L):
+    from paper_1808_09617_b200 import nndtw
+    rng = np.random.default_rng(100 + L)
+    A = datagen.random_series(rng, 24, L, "walk")
+    B = datagen.random_series(rng, 24, L, "walk")
+    B[0] = A[0]
+    for w in sorted({0, 1, 2, 3, L // 8, L // 4, L // 2, L - 1, L + 3}):
+        out = nndtw.dtw_batch(T(A, dev), T(B, dev), w).cpu().numpy()
+        ref = np.array([oracle_lib.dtw(A[p], B[p], w) for p in range(24)])
+        assert_rel(out, ref, what=f"L={L} w={w}")
+
+
+def test_dtw_batch_indexed_and_abandon(dev, oracle_lib):
+    import torch
+    from paper_1808_09617_b200 import nndtw
+    rng = np.random.default_rng(7)
+    L, w = 200, 20
+    A = datagen.random_series(rng, 10, L, "walk")
+    B = datagen.random_series(rng, 30, L, "walk")
+    ia = rng.integers(0, 10, size=300).astype(np.int32)
+    ib = rng.integers(0, 30, size=300).astype(np.int32)
+    ref = np.array([oracle_lib.dtw(A[i], B[j], w) for i, j in zip(ia, ib)])
+    cut = (ref * rng.uniform(0.3, 1.6, size=300)).astype(np.float32)
+    out = nndtw.dtw_batch(T(A, dev), T(B, dev), w, ia=T(ia, dev), ib=T(ib, dev),
+                          cutoff=T(cut, dev)).cpu().numpy()
+    aband = np.isinf(out)
+    assert np.all(ref[aband] > cut[aband])          # abandoned => exact value > cutoff
+    assert_rel(out[~aband], ref[~aband], what="non-abandoned")
+    assert aband.sum() > 10                          # abandoning is effective
+    full = nndtw.dtw_batch(T(A, dev), T(B, dev), w, ia=T(ia, dev), ib=T(ib, dev)).cpu().numpy()
+    assert_rel(full, ref, what="no cutoff")
+
+
+# ---------------------------------------------------------------- S2-S7 classify
+def _classify(dev, Tr, trl, Q, w, V, stats=False):
+    from paper_1808_09617_b200 import nndtw
+    model = nndtw.Model(T(Tr, dev), T(trl, dev), w, V)
+    pred = nndtw.classify(model, T(Q, dev), stats=stats)
+    return (pred.idx.cpu().numpy(), pred.label.cpu().numpy(), pred.dist.cpu().numpy(),
+            pred.stats)
+
+
+def _check_nn(oracle_lib, Tr, trl, Q, w, idx, lab, dist, mode="exhaustive", V=5):
+    ridx, rdist = oracle_lib.nn(Q, Tr, w, V=V, mode=mode)
+    assert np.array_equal(idx, ridx), np.nonzero(idx != ridx)[0][:10]
+    assert np.array_equal(lab, trl[ridx])
+    assert_rel(dist, rdist, what="nn distance")
+
+
+def test_classify_config0(dev, oracle_lib):
+    ds = datagen.make_dataset(0)
+    w = ds.cfg.windows()[0]
+    idx, lab, dist, st = _classify(dev, ds.train, ds.train_labels, ds.test, w, 5, stats=True)
+    _check_nn(oracle_lib, ds.train, ds.train_labels, ds.test, w, idx, lab, dist)
+    assert st["lb_pairs"] == 100 * 100 and st["dtw_calls"] < 100 * 100
+
+
+@pytest.mark.parametrize("p", [1, 10, 20, 50, 100])
+def test_classify_config1_grid(dev, oracle_lib, p):
+    """BJ:configs[1] at full N=1000 train, a 120-query sample, every V of the grid."""
+    ds = datagen.make_dataset(1)
+    w = datagen.window_from_percent(p, 256)
+    Q = ds.test[:120]
+    ridx, rdist = oracle_lib.nn(Q, ds.train, w, mode="pruned")
+    for V in ds.cfg.Vs:
+        idx, lab, dist, _ = _classify(dev, ds.train, ds.train_labels, Q, w, V)
+        assert np.array_equal(idx, ridx), (V, np.nonzero(idx != ridx)[0][:10])
+        assert_rel(dist, rdist, what=f"p={p} V={V}")
+
+
+@pytest.mark.parametrize("kind,L,w,V", [("int", 8, 2, 3), ("int", 16, 0, 5), ("int", 33, 32, 4),
+                                        ("walk", 2, 0, 1), ("walk", 3, 1, 5), ("const", 12, 3, 2),
+                                        ("walk", 130, 129, 70), ("int", 64, 5, 1)])
+def test_classify_ties_and_edges(dev, oracle_lib, kind, L, w, V):
+    """Exact ties (integer grids, duplicates, constants): the lowest train index must win."""
+    rng = np.random.default_rng(L * 31 + w)
+    Tr = datagen.random_series(rng, 257, L, kind)
+    Tr[200:210] = Tr[17]          # duplicates after the original
+    Tr[3] = Tr[250]               # duplicate before
+    Q = datagen.random_series(rng, 61, L, kind)
+    Q[0] = Tr[17]
+    trl = rng.integers(0, 4, size=257).astype(np.int32)
+    idx, lab, dist, _ = _classify(dev, Tr, trl, Q, w, V)
+    _check_nn(oracle_lib, Tr, trl, Q, w, idx, lab, dist)
+
+
+def test_classify_single_pair(dev, oracle_lib):
+    rng = np.random.default_rng(3)
+    Tr = datagen.random_series(rng, 1, 50, "walk")
+    Q = datagen.random_series(rng, 1, 50, "walk")
+    idx, lab, dist, _ = _classify(dev, Tr, np.array([7], np.int32), Q, 5, 5)
+    assert idx[0] == 0 and lab[0] == 7
+    assert_rel(dist, [oracle_lib.dtw(Q[0], Tr[0], 5)])
+
+
+@pytest.mark.slow
+def test_classify_config2_full_sampled(dev, oracle_lib):
+    """BJ:configs[2] at full size (1e4 queries x 1e5 train, L=512, w=103, V=5) in the bench's
+    launch configuration; a seeded sample of queries is checked against the oracle's pruned
+    search (itself pinned to exhaustive search in test_oracle_pins)."""
+    ds = datagen.make_dataset(2)
+    w = ds.cfg.windows()[0]
+    idx, lab, dist, st = _classify(dev, ds.train, ds.train_labels, ds.test, w, 5, stats=True)
+    rng = np.random.default_rng(2)
+    sample = np.sort(rng.choice(ds.test.shape[0], size=16, replace=False))
+    ridx, rdist = oracle_lib.nn(ds.test[sample], ds.train, w, V=5, mode="pruned")
+    assert np.array_equal(idx[sample], ridx)
+    assert_rel(dist[sample], rdist, what="config 2 sample")
+    acc = np.mean(lab == ds.test_labels)
+    assert acc > 0.9
+    assert st["dtw_calls"] < 0.2 * st["lb_pairs"]
+
+
+# ---------------------------------------------------------------- S8 LOOCV
+def test_loocv_reduced(dev, oracle_lib):
+    import torch
+    from paper_1808_09617_b200 import nndtw
+    ds = datagen.make_dataset(3, n_train=240)
+    X, lab = ds.train, ds.train_labels
+    windows = [datagen.window_from_percent(p, 300) for p in (0, 1, 2, 5, 10, 30, 100)]
+    err, nn, _ = nndtw.loocv_window(T(X, dev), T(lab, dev), windows, v=5, with_nn=True)
+    rerr, rnn = oracle_lib.loocv(X, lab, windows, V=5, mode="pruned")
+    assert np.array_equal(nn.cpu().numpy(), rnn.astype(np.int32))
+    assert np.array_equal(err.cpu().numpy(), rerr)
+    # a query shard [60, 170) gives the same rows
+    err2, nn2, _ = nndtw.loocv_window(T(X, dev), T(lab, dev), windows, v=5, q_begin=60,
+                                      q_end=170, with_nn=True)
+    assert np.array_equal(nn2.cpu().numpy(), rnn[:, 60:170].astype(np.int32))
