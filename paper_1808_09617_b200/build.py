@@ -8,7 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libnndtw.so")
+DEBUG = os.environ.get("NNDTW_DEBUG", "0") == "1"
+LIB = os.path.join(HERE, "libnndtw_debug.so" if DEBUG else "libnndtw.so")
 SOURCES = ["abi.cu", "envelopes.cu", "lb.cu", "dtw_band.cu", "search.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-cudart", "static",
@@ -29,11 +30,13 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build_debug" if DEBUG else "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     extra = ["-Xptxas", "-v"] if verbose else []
+    if DEBUG:
+        extra += ["-DNNDTW_DEBUG"]
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(obj)

@@ -13,7 +13,19 @@
 namespace nndtw {
 
 static std::atomic<int64_t> g_launches{0};
-void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void count_launch(int n, const char *who) {
+    g_launches.fetch_add(n, std::memory_order_relaxed);
+#ifdef NNDTW_DEBUG
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "NNDTW_DEBUG: %s -> %s\n", who ? who : "?", cudaGetErrorString(e));
+        fflush(stderr);
+    }
+#else
+    (void)who;
+#endif
+}
 int64_t launches_total() { return g_launches.load(std::memory_order_relaxed); }
 
 // ---- finite check (input validation for the Python layer) -----------------------------------
@@ -30,7 +42,7 @@ int launch_check_finite(const float *x, int64_t n, int32_t *bad, cudaStream_t st
     int64_t grid = (n + 255) / 256;
     if (grid > 2048) grid = 2048;
     k_check_finite<<<(unsigned)grid, 256, 0, st>>>(x, n, bad);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 
@@ -220,7 +232,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     if (nt > 0) {
         // S3: seed round (argmin-LB candidate, plus seed2 if given)
         launch_seed_items(W.minkey, seed2, nq, nt, W.seed_items, W.seed_count, st);
-        rc = dispatch_dtw(q, t, W.seed_items, W.seed_count, 2 * (unsigned long long)nq + 1,
+        rc = dispatch_dtw(q, t, nq, nt, W.seed_items, W.seed_count, 2 * (unsigned long long)nq + 1,
                           nullptr, nullptr, 0, L, w, 0, key, index_base, eps_t, log, cnt,
                           W.cells_prefix, nullptr, nullptr, st, sms);
         if ((rc = dtw_fail(rc, L, w))) return rc;
@@ -228,7 +240,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         launch_compact(W.lb, W.ldlb, nq, nt, key, W.minkey, seed2, eps_p, W.items,
                        W.main_count, W.item_cap, sms, st);
         // S4/S5: DTW with early abandoning on the survivors
-        rc = dispatch_dtw(q, t, W.items, W.main_count, W.item_cap, nullptr, nullptr, 0, L, w, 0,
+        rc = dispatch_dtw(q, t, nq, nt, W.items, W.main_count, W.item_cap, nullptr, nullptr, 0, L, w, 0,
                           key, index_base, eps_t, log, cnt, W.cells_prefix, nullptr, nullptr,
                           st, sms);
         if ((rc = dtw_fail(rc, L, w))) return rc;
@@ -362,7 +374,7 @@ int nndtw_dtw_batch(const float *a, const float *b, const int32_t *ia, const int
     if (!a || !b || !out) return fail(NNDTW_E_ARG, "null pointer argument");
     if (w > L - 1) w = L - 1;
     TieLog log{nullptr, nullptr, 0, nullptr};
-    rc = dispatch_dtw(a, b, nullptr, nullptr, 0, ia, ib, npairs, L, w, 1, nullptr, 0,
+    rc = dispatch_dtw(a, b, INT64_MAX, INT64_MAX, nullptr, nullptr, 0, ia, ib, npairs, L, w, 1, nullptr, 0,
                       eps_tie(L), log, nullptr, nullptr, cutoff, out, (cudaStream_t)stream, sms);
     if ((rc = dtw_fail(rc, L, w))) return rc;
     return cuda_fail("nndtw_dtw_batch");

@@ -10,6 +10,22 @@
 
 #include "../../include/nndtw.h"
 
+#ifdef NNDTW_DEBUG
+#define NNDTW_ASSERT(cond, ...)                                                        \
+    do {                                                                               \
+        if (!(cond)) {                                                                 \
+            printf("NNDTW_ASSERT %s:%d %s | ", __FILE__, __LINE__, #cond);             \
+            printf(__VA_ARGS__);                                                       \
+            printf("\n");                                                              \
+            __trap();                                                                  \
+        }                                                                              \
+    } while (0)
+#else
+#define NNDTW_ASSERT(cond, ...) \
+    do {                        \
+    } while (0)
+#endif
+
 namespace nndtw {
 
 constexpr float kInf = __builtin_huge_valf();
@@ -23,7 +39,7 @@ inline float eps_prune(int L) { return (3.0f * (float)L + 8.0f) * 0x1p-24f; }
 inline float eps_tie(int L) { return (4.0f * (float)L + 8.0f) * 0x1p-24f; }
 
 // process-wide launch counter (bench bookkeeping; incremented by every launcher)
-void count_launch(int n = 1);
+void count_launch(int n = 1, const char *who = nullptr);
 int64_t launches_total();
 
 struct CudaCheck {

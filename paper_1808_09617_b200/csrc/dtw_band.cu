@@ -39,6 +39,7 @@ struct BandParams {
     const long long *cells_prefix;        // [2L-1], nullable iff counters null
     const float *cutoff;                  // batch, nullable
     float *out;                           // batch
+    int64_t dbg_na, dbg_nb;               // row counts of A and B (debug asserts)
 };
 
 template <int R, bool ALIGNED>
@@ -109,6 +110,9 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
             b_idx = p.ib ? (unsigned)p.ib[it] : (unsigned)it;
             thr_batch = p.cutoff ? p.cutoff[it] * (1.0f + p.eps_t) : kInf;
         }
+        NNDTW_ASSERT(a_idx < (unsigned)p.dbg_na && b_idx < (unsigned)p.dbg_nb,
+                     "band item oob: it=%lld a=%u b=%u na=%lld nb=%lld", (long long)it, a_idx,
+                     b_idx, (long long)p.dbg_na, (long long)p.dbg_nb);
         qcur = a_idx;
         ncur = b_idx;
         const float *ga = p.A + (int64_t)a_idx * L;
@@ -135,6 +139,10 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
         const int J0 = (kp - w + g * R) >> 1;
         const float *pa = sA + p.padl + I0 - (H - 1);
         const float *pb = sB + p.padl + J0;
+        NNDTW_ASSERT(p.padl + I0 - (H - 1) >= 0 && p.padl + I0 + H - 1 < p.seglen &&
+                         p.padl + J0 >= 0 && p.padl + J0 + R - 1 < p.seglen,
+                     "band smem oob: g=%d per=%d I0=%d J0=%d padl=%d seglen=%d", g, per, I0,
+                     J0, p.padl, p.seglen);
         float aw[R - 1], bw[R];
 #pragma unroll
         for (int x = 0; x < R - 1; ++x) aw[x] = pa[x];
@@ -160,7 +168,7 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
                 D[r] = fmaf(tt, tt, fminf(fminf(D[r], lo), hi));
             }
         }
-        ++per;
+        per = active ? per + 1 : 0;  // idle groups replay period 0 (stay in bounds)
 
         // ---- events: completion / early abandon --------------------------------------
         float lmin = D[0];
@@ -210,6 +218,7 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
             it += ngroups;
             active = it < nitems;
             if (active) setup();
+            else per = 0;  // idle groups replay period 0 (stay in bounds)
         }
         __syncwarp();
     }
@@ -222,84 +231,107 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
 
 // ---- host-side selection and launch ----------------------------------------------------------
 struct BandChoice {
-    int R, G, gpw;
+    int R, G, gpw, warps;   // warps per CTA
     bool aligned;
+    int k0, nper, padl, seglen;
 };
 
-static double band_cost(int R, int w, int G) {
-    int gpw = 32 / G;
-    double per_lane = (double)R * 1.5 * R + (2.0 * R - 1) + R + 15.0;
-    return per_lane / ((double)gpw * R * (w + 0.5));
+// Geometry of the padded shared-memory rows for slot width R and G lanes per group.
+static void band_geometry(int R, int G, int L, int w, BandChoice &c) {
+    const int H = R / 2;
+    c.k0 = (w & 1) ? -1 : 0;  // period starts satisfy (k + w) even
+    c.nper = (2 * L - 1 - c.k0 + R - 1) / R;
+    const int kp_last = c.k0 + (c.nper - 1) * R;
+    const int amin = ((c.k0 + w - (G - 1) * R) >> 1) - (H - 1);
+    const int amax = ((kp_last + w) >> 1) + H - 1 + 1;
+    const int bmin = (c.k0 - w) >> 1;
+    const int bmax = ((kp_last - w + (G - 1) * R) >> 1) + R - 1 + 1;
+    const int lo = amin < bmin ? amin : bmin;
+    const int hi = amax > bmax ? amax : bmax;
+    c.padl = (lo < 0 ? -lo : 0) + 1;
+    const int padr = (hi > L - 1 ? hi - (L - 1) : 0) + 1;
+    const int seg = c.padl + L + padr;
+    c.seglen = (seg + 3) / 4 * 4 + 1;  // odd stride: spreads groups over banks
 }
 
-BandChoice choose_band(int w) {
-    BandChoice best{0, 0, 0, false};
+// Model: warp-instructions per useful cell (1.5R^2 cell ops + 2R-1 LDS + R shuffles/selects
+// + ~15 bookkeeping per period, over gpw*R*(w+1/2) in-band cells per period), divided by an
+// occupancy factor (warps resident per SM / 16, limited by shared memory and registers).
+static BandChoice choose_band(int w, int L) {
+    BandChoice best{};
+    best.R = 0;
     double bc = 1e30;
     for (int R = 2; R <= 32; R += 2) {
         int G = (2 * w + 2 + R - 1) / R;
         if (G > 32) continue;
         bool aligned = (G * R == 2 * w + 2);
-        if (!aligned && R > 24) continue;      // register budget of the general variant
-        double c = band_cost(R, w, G) * (aligned ? 1.0 : 1.02);
-        if (c < bc) {
-            bc = c;
-            best = {R, G, 32 / G, aligned};
+        if (!aligned && R > 24) continue;  // register budget of the general variant
+        BandChoice c{};
+        c.R = R;
+        c.G = G;
+        c.gpw = 32 / G;
+        c.aligned = aligned;
+        band_geometry(R, G, L, w, c);
+        const double warp_smem = (double)c.gpw * 2 * c.seglen * sizeof(float);
+        int warps = (int)((200.0 * 1024) / warp_smem);
+        if (warps < 1) continue;
+        if (warps > 8) warps = 8;
+        c.warps = warps;
+        const int ctas_smem = (int)((227.0 * 1024) / (warps * warp_smem));
+        const int regs = aligned ? 56 + 2 * R : 56 + 3 * R;
+        const int ctas_regs = 65536 / (regs * 32 * warps);
+        int ctas = ctas_smem < ctas_regs ? ctas_smem : ctas_regs;
+        int wsm = ctas * warps;
+        if (wsm > 48) wsm = 48;
+        const double occ = wsm >= 16 ? 1.0 : (double)wsm / 16.0;
+        const double per_lane = (double)R * 1.5 * R + (2.0 * R - 1) + R + 15.0;
+        const double cost = per_lane / ((double)c.gpw * R * (w + 0.5)) / occ *
+                            (aligned ? 1.0 : 1.02);
+        if (cost < bc) {
+            bc = cost;
+            best = c;
         }
     }
     return best;
 }
 
-bool band_supported(int w) { return choose_band(w).R != 0; }
+bool band_supported(int w, int L) { return choose_band(w, L).R != 0; }
 
 template <int R, bool AL>
-static int launch_band_t(BandParams &p, cudaStream_t st, int num_sms) {
+static int launch_band_t(BandParams &p, const BandChoice &c, cudaStream_t st, int num_sms) {
     auto kern = k_dtw_band<R, AL>;
-    const int block = 256;
-    const int warps = block / 32;
-    size_t smem = (size_t)warps * p.gpw * 2 * p.seglen * sizeof(float);
-    if (smem > 220 * 1024) return -2;
+    const int block = 32 * c.warps;
+    size_t smem = (size_t)c.warps * p.gpw * 2 * p.seglen * sizeof(float);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem);
     if (occ < 1) occ = 1;
-    int64_t groups_per_block = (int64_t)warps * p.gpw;
+    int64_t groups_per_block = (int64_t)c.warps * p.gpw;
     int64_t want = (int64_t)num_sms * occ;
     if (p.mode == 1) {
         int64_t need = (p.nitems_host + groups_per_block - 1) / groups_per_block;
         if (need < want) want = need > 0 ? need : 1;
     }
     kern<<<(unsigned)want, block, smem, st>>>(p);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 
 #define BAND_CASE(RR)                                                         \
     case RR:                                                                  \
-        return c.aligned ? launch_band_t<RR, true>(p, st, num_sms)            \
-                         : launch_band_t<RR, false>(p, st, num_sms);
+        return c.aligned ? launch_band_t<RR, true>(p, c, st, num_sms)         \
+                         : launch_band_t<RR, false>(p, c, st, num_sms);
 
 int launch_dtw_band(BandParams p, cudaStream_t st, int num_sms) {
-    BandChoice c = choose_band(p.w);
+    BandChoice c = choose_band(p.w, p.L);
     if (c.R == 0) return -1;
     p.G = c.G;
     p.gpw = c.gpw;
-    const int R = c.R;
-    // phase: period starts must satisfy (k + w) even
-    p.k0 = (p.w & 1) ? -1 : 0;
-    p.nper = (2 * p.L - 1 - p.k0 + R - 1) / R;
-    const int H = R / 2;
-    const int kp_last = p.k0 + (p.nper - 1) * R;
-    const int amin = ((p.k0 + p.w - (c.G - 1) * R) >> 1) - (H - 1);
-    const int amax = ((kp_last + p.w) >> 1) + H - 1 + 1;
-    const int bmin = (p.k0 - p.w) >> 1;
-    const int bmax = ((kp_last - p.w + (c.G - 1) * R) >> 1) + R - 1 + 1;
-    int lo = amin < bmin ? amin : bmin;
-    int hi = amax > bmax ? amax : bmax;
-    p.padl = (lo < 0 ? -lo : 0) + 1;
-    int padr = (hi > p.L - 1 ? hi - (p.L - 1) : 0) + 1;
-    int seg = p.padl + p.L + padr;
-    p.seglen = (seg + 3) / 4 * 4 + 1;  // odd stride: spread groups over banks
-    switch (R) {
+    p.k0 = c.k0;
+    p.nper = c.nper;
+    p.padl = c.padl;
+    p.seglen = c.seglen;
+    switch (c.R) {
         BAND_CASE(2)
         BAND_CASE(4)
         BAND_CASE(6)
@@ -321,7 +353,77 @@ int launch_dtw_band(BandParams p, cudaStream_t st, int num_sms) {
     }
 }
 
-int dispatch_dtw(const float *A, const float *B, const Item *items,
+// ---- w = 0: DTW_0 is the squared Euclidean distance; one warp per item -------------
+__global__ void __launch_bounds__(256) k_dtw_w0(BandParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int64_t nitems = p.nitems_host;
+    if (p.mode == 0) {
+        unsigned long long c = *p.nitems_dev;
+        nitems = (int64_t)(c < p.item_cap ? c : p.item_cap);
+    }
+    for (int64_t it = wid; it < nitems; it += nw) {
+        unsigned a_idx, b_idx;
+        if (p.mode == 0) {
+            Item itm = p.items[it];
+            a_idx = itm.q;
+            b_idx = itm.n;
+        } else {
+            a_idx = p.ia ? (unsigned)p.ia[it] : (unsigned)it;
+            b_idx = p.ib ? (unsigned)p.ib[it] : (unsigned)it;
+        }
+        const float *ga = p.A + (int64_t)a_idx * p.L;
+        const float *gb = p.B + (int64_t)b_idx * p.L;
+        float s = 0.0f;
+        for (int i = lane; i < p.L; i += 32) {
+            float t = __ldg(ga + i) - __ldg(gb + i);
+            s = fmaf(t, t, s);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) {
+            if (p.mode == 0) {
+                unsigned long long old =
+                    atomicMin(p.key + a_idx, make_key(s, (unsigned)(p.index_base + b_idx)));
+                float best = fminf(s, key_dist(old));
+                if (s <= best * (1.0f + p.eps_t)) {
+                    unsigned long long slot = atomicAdd(p.log.count, 1ull);
+                    if (slot < p.log.capacity) {
+                        TieEntry e;
+                        e.q = a_idx;
+                        e.n = b_idx;
+                        e.d32 = s;
+                        e.pad = 0.0f;
+                        e.d64 = 0.0;
+                        p.log.e[slot] = e;
+                    } else {
+                        p.log.overflow[a_idx] = 1u;
+                    }
+                }
+                if (p.counters) {
+                    atomicAdd(p.counters + CNT_ITEMS, 1ull);
+                    atomicAdd(p.counters + CNT_CELLS, (unsigned long long)p.L);
+                }
+            } else {
+                p.out[it] = s;
+            }
+        }
+    }
+}
+
+static int launch_dtw_w0(BandParams &p, cudaStream_t st, int num_sms) {
+    int64_t grid = (int64_t)num_sms * 8;
+    if (p.mode == 1) {
+        int64_t need = (p.nitems_host + 7) / 8;
+        if (need < grid) grid = need > 0 ? need : 1;
+    }
+    k_dtw_w0<<<(unsigned)grid, 256, 0, st>>>(p);
+    count_launch(1, __func__);
+    return 0;
+}
+
+int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const Item *items,
                  const unsigned long long *nitems_dev, unsigned long long item_cap,
                  const int32_t *ia, const int32_t *ib, int64_t nitems_host, int L, int w,
                  int mode, unsigned long long *key, int64_t index_base, float eps_t, TieLog log,
@@ -348,7 +450,10 @@ int dispatch_dtw(const float *A, const float *B, const Item *items,
     p.cells_prefix = cells_prefix;
     p.cutoff = cutoff;
     p.out = out;
-    if (band_supported(w)) {
+    p.dbg_na = na;
+    p.dbg_nb = nb;
+    if (w == 0) return launch_dtw_w0(p, st, num_sms);
+    if (band_supported(w, L)) {
         int rc = launch_dtw_band(p, st, num_sms);
         if (rc == 0) return 0;
     }

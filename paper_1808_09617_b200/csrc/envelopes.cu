@@ -332,7 +332,7 @@ int launch_envelopes(const float *x, int64_t n, int L, int w, float *U, float *L
         cudaFuncSetAttribute(k_envelopes<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     k_envelopes<8><<<(unsigned)grid, block, smem, st>>>(x, n, L, w, tps, U, Lo, kim);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 
@@ -341,7 +341,7 @@ int launch_series_stats(const float *x, int64_t n, int L, nndtw_kim *kim, cudaSt
     int64_t threads = n * 32;
     int64_t grid = (threads + 255) / 256;
     k_series_stats<<<(unsigned)grid, 256, 0, st>>>(x, n, L, kim);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 

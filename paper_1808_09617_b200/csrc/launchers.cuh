@@ -45,7 +45,7 @@ int launch_count_errors(const unsigned long long *key, int64_t nq, const int32_t
 // S4 dispatch: picks the band-wavefront kernel (2w+2 <= 32*32 slots) or the row-strip kernel
 // (long windows).  mode 0 = search (items + device count, atomicMin into key, tie log),
 // mode 1 = batch (ia/ib/cutoff/out, nitems_host pairs).  Returns 0 or an NNDTW_E_* code.
-int dispatch_dtw(const float *A, const float *B, const Item *items,
+int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const Item *items,
                  const unsigned long long *nitems_dev, unsigned long long item_cap,
                  const int32_t *ia, const int32_t *ib, int64_t nitems_host, int L, int w,
                  int mode, unsigned long long *key, int64_t index_base, float eps_t, TieLog log,

@@ -293,7 +293,7 @@ int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
                              (int)smem);
         k_lb_tile<false><<<grid, 256, smem, st>>>(p);
     }
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 

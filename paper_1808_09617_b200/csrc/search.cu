@@ -16,7 +16,7 @@ int launch_fill_u64(unsigned long long *p, int64_t n, unsigned long long v, cuda
     int64_t grid = (n + 255) / 256;
     if (grid > 4096) grid = 4096;
     k_fill_u64<<<(unsigned)grid, 256, 0, st>>>(p, n, v);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 
@@ -45,7 +45,7 @@ int launch_seed_items(const unsigned long long *minkey, const int32_t *seed2, in
     if (nq == 0) return 0;
     k_seed_items<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(minkey, seed2, nq, nt, items,
                                                                count);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 
@@ -115,7 +115,7 @@ int launch_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
     int64_t grid = ntiles < (int64_t)num_sms * 8 ? ntiles : (int64_t)num_sms * 8;
     k_compact<<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, minkey, seed2, eps_p,
                                                items, count, capacity);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 
@@ -162,7 +162,7 @@ __global__ void k_cells_prefix(int L, int w, long long *prefix) {
 int launch_cells_prefix(int L, int w, long long *prefix, cudaStream_t st) {
     if (w > L - 1) w = L - 1;
     k_cells_prefix<<<1, 1024, 0, st>>>(L, w, prefix);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 
@@ -294,7 +294,7 @@ int launch_refine(TieEntry *e, const unsigned long long *count, unsigned long lo
     cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_refine<<<num_sms * 2, block, smem, st>>>(e, count, cap, A, B, L, w, gkey, eps_t, f64key,
                                                counters);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 
@@ -312,7 +312,7 @@ int launch_refine_overflow(const unsigned *overflow, int64_t nq, const float *lb
     k_refine_overflow<<<num_sms, block, smem, st>>>(overflow, nq, lb, ldlb, nt, A, B, L, w,
                                                     gkey, eps_p, pass, f64key, gf64,
                                                     index_base, out);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 
@@ -336,7 +336,7 @@ int launch_resolve(const TieEntry *e, const unsigned long long *count, unsigned 
                    const unsigned long long *gf64, int64_t index_base, unsigned long long *out,
                    int num_sms, cudaStream_t st) {
     k_resolve<<<num_sms * 2, 256, 0, st>>>(e, count, cap, gf64, index_base, out);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 
@@ -352,7 +352,7 @@ int launch_swap_key(const unsigned long long *in, int64_t nq, unsigned long long
                     cudaStream_t st) {
     if (nq == 0) return 0;
     k_swap_key<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(in, nq, out);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 
@@ -377,7 +377,7 @@ int launch_finalize(const unsigned long long *key, int64_t nq, int fmt, const in
     if (nq == 0) return 0;
     k_finalize<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(key, nq, fmt, labels, nlabels,
                                                              idx_out, label_out, dist_out);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 
@@ -406,7 +406,7 @@ int launch_count_errors(const unsigned long long *key, int64_t nq, const int32_t
     if (nq == 0) return 0;
     k_count_errors<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(key, nq, labels, q_begin,
                                                                  errors, nn_out, prev_nn);
-    count_launch();
+    count_launch(1, __func__);
     return 0;
 }
 

@@ -16,7 +16,8 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnndtw.so")
+LIB_PATH = os.path.join(_HERE, "libnndtw_debug.so" if os.environ.get("NNDTW_DEBUG") == "1"
+                        else "libnndtw.so")
 
 NNDTW_LB_WITH_KIM = 1
 NNDTW_CLASSIFY_EXACT = 1
