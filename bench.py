@@ -1,0 +1,383 @@
+"""Benchmark: NN-DTW queries/s with the LB_Kim -> LB_Enhanced^V cascade (BASELINE.json metric).
+
+Workload (default): BASELINE.json configs[2] "Large search" -- N=100,000 train, Q=10,000
+queries, L=512, W=0.2*L (w=103), V=5, 20 classes -- the config whose train set is sharded over
+GPUs.  One step = the whole hot path S1-S7: train envelopes + Kim features
+(S1), the cascade bound of all Q x N pairs (S2), seed / prune / compaction (S3), DTW with early
+abandoning (S4), argmin + fp64 near-tie re-rank (S5, S7) and, for N>1 GPUs, the MIN
+all-reduce shard combine (S6).  Inputs are resident in HBM when the timed region starts; the
+working set (4 GB LB matrix, 600 MB series + envelopes) is larger than the 126 MB L2.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import datagen  # noqa: E402
+
+METRIC = "NN-DTW queries/s (LB_Enhanced^V cascade) at 1/2/4/8 B200; DTW GCUPS"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def dtw_cell_peak_gcups(num_sms: int, sm_mhz: float) -> float:
+    """ALU-issue roof of the DTW recurrence: each SM issues 4 warp
+    instructions per clock = 128 thread-instructions; one DP cell needs at least 3 (FADD or
+    FFMA for a-b, FMNMX3 for the 3-way min, FFMA for (a-b)^2 + min)."""
+    return num_sms * 128.0 * sm_mhz * 1e6 / 3.0 / 1e9
+
+
+def lb_pair_col_peak(num_sms: int, sm_mhz: float) -> float:
+    """ALU-issue roof of the LB bridge: 4 thread-instructions per (pair, column)."""
+    return num_sms * 128.0 * sm_mhz * 1e6 / 4.0 / 1e9
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower().startswith("active"):
+                        reasons.add(nm)
+            except Exception:
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def cpu_baseline_oracle(ds, w, V, target_s=15.0):
+    """The fp64 oracle's paper-pruned search (mode ii: ED order, Algorithm 1, DTW with
+    abandoning), as it stands, on a bounded query sample, all host cores."""
+    import oracle
+    oracle.build()
+    cores = oracle.default_threads()
+    U, Lo = oracle.envelopes(ds.train, w)
+    n = cores
+    t0 = time.perf_counter()
+    oracle.nn(ds.test[:n], ds.train, w, V=V, mode="pruned", envelopes_UL=(U, Lo))
+    el = time.perf_counter() - t0
+    # scale the sample to about target_s seconds (bounded)
+    n2 = int(min(ds.test.shape[0] - n, max(0, (target_s - el) / max(el, 1e-3) * n)))
+    n2 = (n2 // cores) * cores
+    if n2 > 0:
+        t0 = time.perf_counter()
+        oracle.nn(ds.test[n:n + n2], ds.train, w, V=V, mode="pruned", envelopes_UL=(U, Lo))
+        el += time.perf_counter() - t0
+    total = n + n2
+    return {"value": total / el, "unit": "queries/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {total} queries of the {ds.test.shape[0]} against all "
+                      f"{ds.train.shape[0]} train series (fp64 oracle, paper-pruned mode ii, "
+                      f"{el:.1f} s; envelopes precomputed, not timed, as P:583)"}
+
+
+def run_reference(args, cfg, ds, w, V):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    cores = oracle.default_threads()
+    U, Lo = oracle.envelopes(ds.train, w)
+    nper = max(cores, int(args.ref_queries))
+    Q = ds.test
+    off = 0
+
+    def step():
+        nonlocal off
+        sel = np.arange(off, off + nper) % Q.shape[0]
+        off += nper
+        oracle.nn(Q[sel], ds.train, w, V=V, mode="pruned", envelopes_UL=(U, Lo))
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    value = nper * args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_json(cfg, w, V, args.gpus),
+            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores,
+                             "kind": "oracle",
+                             "sample": f"{nper} queries per step (rolling through the "
+                                       f"{Q.shape[0]}) against all {ds.train.shape[0]} "
+                                       "train series, fp64 oracle paper-pruned search"},
+            "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_json(cfg, w, V, gpus):
+    return {"workload": f"config{cfg.idx}_{cfg.name}", "n_train": cfg.n_train,
+            "n_test": cfg.n_test, "L": cfg.L, "w": w, "V": V, "classes": cfg.classes,
+            "l2": "inputs larger than L2 (4 GB LB matrix + 600 MB series/envelopes per step)",
+            "parallelism": f"train-sharded x{gpus}, queries replicated, int64 MIN allreduce"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--queries", type=int, default=None, help="override Q (debug only)")
+    ap.add_argument("--train", type=int, default=None, help="override N (debug only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-queries", type=int, default=0)
+    args = ap.parse_args()
+
+    cfg = datagen.CONFIGS[args.config]
+    w = cfg.windows()[0] if args.config != 1 else datagen.window_from_percent(10, cfg.L)
+    V = cfg.Vs[-1] if args.config not in (1,) else 5
+    ds = datagen.make_dataset(args.config, n_train=args.train, n_test=args.queries)
+    if args.impl == "reference":
+        run_reference(args, cfg, ds, w, V)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1808_09617_b200 import build as nbuild
+    from paper_1808_09617_b200 import nndtw
+    from paper_1808_09617_b200.dist import classify_sharded, shard_range
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        nbuild.build()
+    if world > 1:
+        dist.barrier()
+    lib = nndtw.load()
+    if lib.nndtw_check_device() != 0:
+        raise SystemExit("libnndtw requires an sm_100 (B200) device")
+    N, L = ds.train.shape
+    Q = ds.test.shape[0]
+    lo, hi = shard_range(N, rank, world)
+    train_h = torch.from_numpy(np.ascontiguousarray(ds.train[lo:hi])).pin_memory()
+    test_h = torch.from_numpy(ds.test).pin_memory()
+    labels_h = torch.from_numpy(ds.train_labels).pin_memory()
+    train_d = train_h.to(dev)
+    test_d = test_h.to(dev)
+    labels_d = labels_h.to(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    acc = {"ms_lb": 0.0, "ms_dtw": 0.0, "cells": 0, "lb_pairs": 0, "dtw_calls": 0,
+           "survivors": 0, "near_tie_pairs": 0, "dtw_abandoned": 0}
+
+    def step(stats):
+        model = nndtw.Model(train_d, labels_d[lo:hi], w, V, index_base=lo, check=False)
+        if world == 1:
+            pred = nndtw.classify(model, test_d, stats=stats, check=False)
+        else:
+            pred = classify_sharded(model, test_d, labels_d, stats=stats)
+        if stats and pred.stats:
+            for k in acc:
+                acc[k] += pred.stats[k]
+        return pred
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region (device-side timing, max over ranks) -----------------------------
+    sampler = ClockSampler(local) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    l0 = nndtw.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        pred = step(True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    launches = nndtw.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms, float(launches)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms, launches = float(tmax[0]), int(tsum[1])
+        a = torch.tensor([acc["ms_dtw"], acc["ms_lb"], float(acc["cells"]),
+                          float(acc["lb_pairs"]), float(acc["dtw_calls"])],
+                         dtype=torch.float64, device=dev)
+        dist.all_reduce(a, op=dist.ReduceOp.SUM)
+        acc_tot = {"ms_dtw": float(a[0]), "ms_lb": float(a[1]), "cells": float(a[2]),
+                   "lb_pairs": float(a[3]), "dtw_calls": float(a[4])}
+    else:
+        acc_tot = dict(acc)
+    acc_tot["ms_dtw"] = acc_tot["ms_dtw"] / world
+    acc_tot["ms_lb"] = acc_tot["ms_lb"] / world
+    value = Q * args.steps / (ms / 1e3)
+
+    # ---- e2e through the public API with host buffers ---------------------------------
+    e2e = None
+    if not args.no_e2e:
+        def e2e_step():
+            tr = train_h.to(dev, non_blocking=True)
+            te = test_h.to(dev, non_blocking=True)
+            lb_ = labels_h.to(dev, non_blocking=True)
+            model = nndtw.Model(tr, lb_[lo:hi], w, V, index_base=lo)
+            if world == 1:
+                pred = nndtw.classify(model, te)
+            else:
+                pred = classify_sharded(model, te, lb_)
+            return pred.idx.cpu(), pred.label.cpu(), pred.dist.cpu()
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        ke = max(1, min(args.steps, 3))
+        for _ in range(ke):
+            e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            te_ = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(te_, op=dist.ReduceOp.MAX)
+            ems = float(te_[0])
+        h2d = train_h.numel() * 4 + test_h.numel() * 4 + labels_h.numel() * 4
+        d2h = Q * (8 + 4 + 4)
+        e2e = {"value": Q * ke / (ems / 1e3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    pk, src = peaks()
+    num_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    peak_cells = dtw_cell_peak_gcups(num_sms, sm_mhz)
+    dtw_gcups = acc_tot["cells"] / (acc_tot["ms_dtw"] * 1e-3) / 1e9 / world \
+        if acc_tot["ms_dtw"] > 0 else 0.0
+    # per-GPU dominant-kernel figure: each rank's cells / its own DTW kernel time
+    lb_cols = (L - 2 * min(L // 2, V))
+    lb_rate = (acc_tot["lb_pairs"] * lb_cols / (acc_tot["ms_lb"] * 1e-3) / 1e9 / world
+               if acc_tot["ms_lb"] > 0 else 0.0)
+    lb_peak = lb_pair_col_peak(num_sms, sm_mhz)
+    dominant = "dtw" if acc_tot["ms_dtw"] >= acc_tot["ms_lb"] else "lb"
+    roof_dtw = {"kernel": "k_dtw_band (S4 survivor round)", "bound": "alu",
+                "achieved": dtw_gcups, "peak": peak_cells, "unit": "Gcells/s",
+                "frac": dtw_gcups / peak_cells if peak_cells else None, "traffic": None,
+                "peak_source": f"{num_sms} SMs x 128 lanes x {sm_mhz:.0f} MHz ({src}) / 3 "
+                               "instr per cell",
+                "ms_per_step": acc_tot["ms_dtw"] / args.steps}
+    roof_lb = {"kernel": "k_lb_tile (S2 cascade)", "bound": "alu", "achieved": lb_rate,
+               "peak": lb_peak, "unit": "G pair-columns/s",
+               "frac": lb_rate / lb_peak if lb_peak else None, "traffic": None,
+               "peak_source": f"{num_sms} SMs x 128 lanes x {sm_mhz:.0f} MHz ({src}) / 4 "
+                              "instr per pair-column",
+               "ms_per_step": acc_tot["ms_lb"] / args.steps}
+    line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (datagen.py, BASELINE.json configs[%d])" %
+            args.config, "config": config_json(cfg, w, V, world),
+            "roofline": roof_dtw if dominant == "dtw" else roof_lb,
+            "roofline_other": roof_lb if dominant == "dtw" else roof_dtw,
+            "dtw_gcups": dtw_gcups,
+            "effective_gcups": Q * N * (L * (2 * w + 1) - w * (w + 1)) /
+            (ms / args.steps * 1e-3) / 1e9,
+            "counters_per_step": {k: acc_tot[k] / args.steps for k in
+                                  ("lb_pairs", "dtw_calls", "cells")},
+            "gpu_launches": launches, "clocks": clocks, "e2e": e2e}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_oracle(ds, w, V)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -61,12 +61,14 @@ typedef struct {
     int64_t lb_pairs;       /* (query, train) pairs whose cascade bound was computed */
     int64_t survivors;      /* pairs with LB <= bsf*(1+eps_p) after the seed round */
     int64_t dtw_calls;      /* DTW work items started (seeds + survivors) */
-    int64_t dtw_abandoned;  /* items stopped by early abandoning */
-    int64_t cells;          /* in-band DP cells on the diagonals actually processed */
+    int64_t dtw_abandoned;  /* survivor items stopped by early abandoning */
+    int64_t cells;          /* in-band DP cells on the diagonals the survivor round processed */
     int64_t near_tie_pairs; /* pairs re-ranked in fp64 (reading C16) */
     int32_t rounds;         /* DTW rounds run (seed round included) */
     int32_t launches;       /* kernel launches issued by the call */
-    float ms_envelopes, ms_lb, ms_dtw, ms_other; /* CUDA-event stage times (stats != NULL) */
+    /* CUDA-event stage times on the call's stream: ms_lb = the LB cascade kernel, ms_dtw = the
+     * survivor-round DTW kernel, ms_other = everything else (seed round, compaction, S7). */
+    float ms_envelopes, ms_lb, ms_dtw, ms_other;
 } nndtw_stats;
 
 /* Library identity and introspection. */
@@ -150,7 +152,8 @@ NNDTW_API int nndtw_classify(const float *q, int64_t nq, const float *t, const f
  * S7 (sharded) -- near-tie re-rank, step 1.  gkey: [nq] the MIN of all shards' keys.  For
  * every locally completed candidate whose fp32 distance is within gkey*(1+eps_t) of the global
  * best, recompute DTW in fp64 with the oracle's per-cell operation sequence (DESIGN.md
- * "fp64 re-rank"); f64key[i] = bits of the smallest such fp64 value (UINT64_MAX if none).
+ * "fp64 re-rank"); f64key[i] = bits of the smallest such fp64 value (INT64_MAX if none: keys stay < 2^63 so a signed int64 MIN
+ * reduction combines them).
  * Requires the ws of the preceding nndtw_classify call (same q, t).
  */
 NNDTW_API int nndtw_classify_refine(void *ws, size_t ws_bytes, const float *q, int64_t nq,
@@ -158,7 +161,7 @@ NNDTW_API int nndtw_classify_refine(void *ws, size_t ws_bytes, const float *q, i
                           const uint64_t *gkey, uint64_t *f64key, void *stream);
 /* S7 step 2.  gf64: [nq] MIN over shards of f64key; gkey as for refine.  out[i] = (global
  * index << 32) | fp32 bits of the local candidate with fp64 value == gf64[i] and the lowest
- * index (UINT64_MAX if none); a MIN over shards gives the final answer (key_format 1).
+ * index (INT64_MAX if none); a MIN over shards gives the final answer (key_format 1).
  * Same ws and arguments as the preceding refine call. */
 NNDTW_API int nndtw_classify_resolve(void *ws, size_t ws_bytes, const float *q, int64_t nq,
                            const float *t, int64_t nt, int32_t L, int32_t w,

@@ -215,8 +215,8 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     cudaMemsetAsync(W.counters, 0, sizeof(unsigned long long) * (CNT_N + 3), st);
     launch_fill_u64(key, nq, kKeyInit, st);
     cudaMemsetAsync(W.minkey, 0xff, 8 * (size_t)nq, st);
-    cudaMemsetAsync(W.f64key, 0xff, 8 * (size_t)nq, st);
-    cudaMemsetAsync(W.resolve_out, 0xff, 8 * (size_t)nq, st);
+    launch_fill_u64(W.f64key, nq, kNone64, st);
+    launch_fill_u64(W.resolve_out, nq, kNone64, st);
     cudaMemsetAsync(W.overflow, 0, 4 * (size_t)nq, st);
     if (stats) launch_cells_prefix(L, w, W.cells_prefix, st);
     // S2: cascade bound for all pairs + per-query argmin-LB candidate
@@ -233,23 +233,27 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         // S3: seed round (argmin-LB candidate, plus seed2 if given)
         launch_seed_items(W.minkey, seed2, nq, nt, W.seed_items, W.seed_count, st);
         rc = dispatch_dtw(q, t, nq, nt, W.seed_items, W.seed_count, 2 * (unsigned long long)nq + 1,
-                          nullptr, nullptr, 0, L, w, 0, key, index_base, eps_t, log, cnt,
+                          nullptr, nullptr, 0, L, w, 0, key, index_base, eps_t, log, nullptr,
                           W.cells_prefix, nullptr, nullptr, st, sms);
         if ((rc = dtw_fail(rc, L, w))) return rc;
         // S3: prune + compact the survivors against the seeded best-so-far
         launch_compact(W.lb, W.ldlb, nq, nt, key, W.minkey, seed2, eps_p, W.items,
                        W.main_count, W.item_cap, sms, st);
+        tm.mark();  // 3
         // S4/S5: DTW with early abandoning on the survivors
         rc = dispatch_dtw(q, t, nq, nt, W.items, W.main_count, W.item_cap, nullptr, nullptr, 0, L, w, 0,
                           key, index_base, eps_t, log, cnt, W.cells_prefix, nullptr, nullptr,
                           st, sms);
         if ((rc = dtw_fail(rc, L, w))) return rc;
     }
-    tm.mark();  // 3
+    else {
+        tm.mark();  // 3
+    }
+    tm.mark();  // 4
     if ((rc = cuda_fail("dtw"))) return rc;
     if ((flags & NNDTW_CLASSIFY_EXACT) && nt > 0)
         exact_local(W, q, nq, t, nt, L, w, index_base, key, cnt, sms, st);
-    tm.mark();  // 4
+    tm.mark();  // 5
     if ((rc = cuda_fail("classify"))) return rc;
     if (stats) {
         unsigned long long h[CNT_N + 3];
@@ -257,7 +261,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_fail("classify sync");
         stats->lb_pairs += nq * nt;
         stats->survivors += (int64_t)h[CNT_N + 1];
-        stats->dtw_calls += (int64_t)h[CNT_ITEMS];
+        stats->dtw_calls += (int64_t)h[CNT_ITEMS] + (int64_t)h[CNT_N];  // main + seed items
         stats->dtw_abandoned += (int64_t)h[CNT_ABANDONED];
         stats->cells += (int64_t)h[CNT_CELLS];
         stats->near_tie_pairs += (int64_t)h[CNT_TIES];
@@ -265,8 +269,8 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         stats->launches += (int32_t)(launches_total() - launches0);
         if (outer_tm == nullptr) {
             stats->ms_lb += tm.ms(1, 2);
-            stats->ms_dtw += tm.ms(2, 3);
-            stats->ms_other += tm.ms(0, 1) + tm.ms(3, 4);
+            stats->ms_dtw += tm.ms(3, 4);
+            stats->ms_other += tm.ms(0, 1) + tm.ms(2, 3) + tm.ms(4, 5);
         }
     }
     return NNDTW_OK;
@@ -406,7 +410,7 @@ int nndtw_classify_refine(void *ws, size_t ws_bytes, const float *q, int64_t nq,
     if (!ws || ws_bytes < W.bytes) return fail(NNDTW_E_WORKSPACE, "workspace too small");
     if (nq == 0) return NNDTW_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    cudaMemsetAsync(f64key, 0xff, 8 * (size_t)nq, st);
+    launch_fill_u64((unsigned long long *)f64key, nq, kNone64, st);
     if (nt > 0) {
         launch_refine(W.log, W.log_count, W.log_cap, q, t, L, w,
                       (const unsigned long long *)gkey, eps_tie(L),
@@ -430,7 +434,7 @@ int nndtw_classify_resolve(void *ws, size_t ws_bytes, const float *q, int64_t nq
     if (!ws || ws_bytes < W.bytes) return fail(NNDTW_E_WORKSPACE, "workspace too small");
     if (nq == 0) return NNDTW_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    cudaMemsetAsync(out, 0xff, 8 * (size_t)nq, st);
+    launch_fill_u64((unsigned long long *)out, nq, kNone64, st);
     if (nt > 0) {
         launch_resolve(W.log, W.log_count, W.log_cap, (const unsigned long long *)gf64,
                        index_base, (unsigned long long *)out, sms, st);

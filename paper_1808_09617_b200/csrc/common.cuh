@@ -31,6 +31,9 @@ namespace nndtw {
 constexpr float kInf = __builtin_huge_valf();
 constexpr unsigned long long kKeyInit = 0x7F800000FFFFFFFFull;  // (+inf bits << 32) | ~0
 constexpr unsigned long long kNone = ~0ull;
+// "no candidate" in keys exchanged between ranks: the largest signed int64, so that a signed
+// MIN reduction (NCCL / gloo on int64) treats it as +inf.
+constexpr unsigned long long kNone64 = 0x7FFFFFFFFFFFFFFFull;
 
 // Rounding-error margins of reading C16 (u = 2^-24, fp32 storage and accumulation):
 //  prune a pair only if LB > bsf*(1+eps_p), eps_p = (3L+8)u;

@@ -345,7 +345,7 @@ __global__ void k_swap_key(const unsigned long long *in, int64_t nq, unsigned lo
     int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
     unsigned long long k = in[q];
-    out[q] = (k == kNone) ? kKeyInit : ((k << 32) | (k >> 32));
+    out[q] = (k == kNone64) ? kKeyInit : ((k << 32) | (k >> 32));
 }
 
 int launch_swap_key(const unsigned long long *in, int64_t nq, unsigned long long *out,

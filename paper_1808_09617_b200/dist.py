@@ -1,0 +1,87 @@
+"""S6 -- train-set sharding over ranks (one process per GPU) with MIN-allreduce combines.
+
+The train set is split into contiguous index ranges, queries are replicated, and every rank
+runs S1-S5 on its shard (nndtw_classify without the EXACT flag).  Three int64 MIN all-reduces
+over NCCL (NVLink / NVSwitch) then give the exact answer:
+
+1. key   = (fp32 distance bits << 32) | global index  -> global fp32 best (reading C13);
+2. f64   = fp64 bits of each rank's near-tie candidates within the global fp32 best's band
+           (reading C16) -> global fp64 minimum;
+3. out   = (global index << 32) | fp32 bits of candidates whose fp64 value equals it
+           -> lowest index among exact fp64 ties.
+
+All keys are < 2^63 (non-negative floats, indices < 2^31, "none" = INT64_MAX), so a signed
+int64 MIN is the unsigned MIN.  Messages are Q x 8 bytes per step.
+
+The per-shard operations are injected (`ShardOps`) so that the combine protocol itself is
+tested on CPU with the gloo backend (tests/test_dist_gloo.py); `GpuShardOps` is the product
+path through the C ABI.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import nndtw
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous shard [lo, hi) of n train series for `rank` of `world`."""
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+class ShardOps:
+    """Interface of the per-shard steps (all tensors int64 [nq] on the rank's device)."""
+
+    def local_keys(self, q):
+        raise NotImplementedError
+
+    def refine(self, q, gkey):
+        raise NotImplementedError
+
+    def resolve(self, q, gkey, gf64):
+        raise NotImplementedError
+
+
+class GpuShardOps(ShardOps):
+    def __init__(self, model: nndtw.Model, stats: bool = False, stream=None):
+        self.model = model
+        self.stats = stats
+        self.stream = stream
+        self.ws = None
+        self.last_stats = None
+
+    def local_keys(self, q):
+        key, ws, st = nndtw.classify_keys(self.model, q, exact=False, stats=self.stats,
+                                          stream=self.stream)
+        self.ws = ws
+        self.last_stats = st
+        return key
+
+    def refine(self, q, gkey):
+        return nndtw.classify_refine(self.model, q, self.ws, gkey, self.stream)
+
+    def resolve(self, q, gkey, gf64):
+        return nndtw.classify_resolve(self.model, q, self.ws, gkey, gf64, self.stream)
+
+
+def combine(ops: ShardOps, q, group=None):
+    """Run the 3-step exact combine; returns the final key tensor in key format 1
+    ((global index << 32) | fp32 distance bits)."""
+    key = ops.local_keys(q)
+    dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
+    f64 = ops.refine(q, key)
+    dist.all_reduce(f64, op=dist.ReduceOp.MIN, group=group)
+    out = ops.resolve(q, key, f64)
+    dist.all_reduce(out, op=dist.ReduceOp.MIN, group=group)
+    return out
+
+
+def classify_sharded(model: nndtw.Model, q: torch.Tensor, labels_global: torch.Tensor,
+                     group=None, stats: bool = False, stream=None) -> nndtw.Prediction:
+    """Exact 1-NN of every query against the union of all ranks' shards.  `model` holds this
+    rank's shard with index_base = its first global index; labels_global is replicated."""
+    ops = GpuShardOps(model, stats=stats, stream=stream)
+    out = combine(ops, q, group)
+    idx, lab, d = nndtw.finalize(out, labels_global, key_format=1, stream=stream)
+    return nndtw.Prediction(idx, lab, d, ops.last_stats)
