@@ -56,6 +56,14 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
     return v;
 }
 
+// GPU-scope relaxed load: sees other SMs' atomics (L2 is the coherence point) without the
+// system-scope cost of ld.volatile.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ float key_dist(unsigned long long k) {
     return __uint_as_float((unsigned)(k >> 32));
 }
@@ -65,6 +73,19 @@ __device__ __forceinline__ unsigned long long make_key(float d, unsigned idx) {
 }
 
 __device__ __forceinline__ float sq(float x) { return x * x; }
+
+// cp.async global -> shared (LDGSTS), 4 or 16 bytes, and the wait for all of a thread's copies
+__device__ __forceinline__ void cp_async4(float *dst, const float *src) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(float *dst, const float *src) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
 
 // ---- work items ---------------------------------------------------------------------------
 // A DTW work item: query (row of A) and train (row of B), local indices.

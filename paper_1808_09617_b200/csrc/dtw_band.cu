@@ -18,6 +18,8 @@
 // beyond it stay +inf.  Early abandoning (reading C14): after every period the registers hold
 // two consecutive anti-diagonals, a cut of every warping path; the group abandons when every
 // lane's minimum exceeds bsf*(1+eps_t) (one warp ballot).
+#include <cstdlib>
+
 #include "launchers.cuh"
 
 namespace nndtw {
@@ -29,7 +31,7 @@ struct BandParams {
     unsigned long long item_cap;          // search mode: capacity of items
     const int32_t *ia, *ib;               // batch mode (nullable = identity)
     int64_t nitems_host;                  // batch mode count
-    int L, w, G, gpw, nper, k0, padl, seglen;
+    int L, w, G, gpw, nper, k0, padl, seglen, vec4;
     int mode;                             // 0 search, 1 batch
     unsigned long long *key;
     int64_t index_base;
@@ -42,8 +44,22 @@ struct BandParams {
     int64_t dbg_na, dbg_nb;               // row counts of A and B (debug asserts)
 };
 
-template <int R, bool ALIGNED>
+// An opaque copy: the compiler cannot rematerialise the value (it would otherwise recompute
+// the per-slot kill scales with ISETP+FSEL inside the unrolled period).
+__device__ __forceinline__ float pin_reg(float v) {
+    float r;
+    asm volatile("mov.b32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+}
+
+// KM (kill mode): 0 = general (kill slot anywhere: per-slot scale registers, edge masks);
+// 1 = aligned, G*R = 2w+2 (kill slot is the top lane's last register: one scale register,
+// edge masks); 2 = aligned and gpw*G = 32 (every lane used: rotating shuffles deliver the
+// neighbouring group's kill slot, so no edge masks are needed at all).
+template <int R, int KM>
 __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
+    constexpr bool ALIGNED = KM >= 1;
+    constexpr bool NOMASK = KM == 2;
     extern __shared__ __align__(16) float smem_f[];
     constexpr int H = R / 2;
     const int lane = threadIdx.x & 31;
@@ -77,10 +93,10 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
     const int skill = 2 * w + 1;                     // kill slot d = w+1
     float sc[ALIGNED ? 1 : R];
     if (ALIGNED) {
-        sc[0] = (g * R + R - 1 == skill) ? kInf : 1.0f;
+        sc[0] = pin_reg((g * R + R - 1 == skill) ? kInf : 1.0f);
     } else {
 #pragma unroll
-        for (int r = 0; r < R; ++r) sc[r] = (g * R + r == skill) ? kInf : 1.0f;
+        for (int r = 0; r < R; ++r) sc[r] = pin_reg((g * R + r == skill) ? kInf : 1.0f);
     }
     const float nbmask_lo = (g == 0) ? kInf : 0.0f;        // selects +inf at group edges
     const float nbmask_hi = (g == G - 1) ? kInf : 0.0f;
@@ -117,10 +133,20 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
         ncur = b_idx;
         const float *ga = p.A + (int64_t)a_idx * L;
         const float *gb = p.B + (int64_t)b_idx * L;
-        for (int x = g; x < L; x += G) {
-            sA[p.padl + x] = __ldg(ga + x);
-            sB[p.padl + x] = __ldg(gb + x);
+        // all copies in flight at once (cp.async), one wait: the rows arrive in about one
+        // memory round trip instead of L/G dependent load->store steps
+        if (p.vec4) {
+            for (int x = 4 * g; x < L; x += 4 * G) {
+                cp_async16(sA + p.padl + x, ga + x);
+                cp_async16(sB + p.padl + x, gb + x);
+            }
+        } else {
+            for (int x = g; x < L; x += G) {
+                cp_async4(sA + p.padl + x, ga + x);
+                cp_async4(sB + p.padl + x, gb + x);
+            }
         }
+        cp_async_wait_all();
 #pragma unroll
         for (int r = 0; r < R; ++r) D[r] = (g == g0 && r == r0) ? 0.0f : kInf;
         per = 0;
@@ -129,9 +155,12 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
     if (active) setup();
     __syncwarp();
 
+    // live best-so-far of the group's query, read one period ahead (the abandon test uses the
+    // value loaded during the previous period: never tighter than the true live value)
+    unsigned long long kprev = (p.mode == 0 && active) ? ld_relaxed_u64(p.key + qcur) : 0ull;
     while (__any_sync(0xffffffffu, active)) {
-        unsigned long long kraw = 0;
-        if (p.mode == 0 && active) kraw = ld_volatile_u64(p.key + qcur);
+        unsigned long long knext = 0;
+        if (p.mode == 0 && active) knext = ld_relaxed_u64(p.key + qcur);
 
         // ---- one period: R anti-diagonals, fully unrolled ----------------------------
         const int kp = p.k0 + per * R;
@@ -152,8 +181,13 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
         for (int t = 0; t < R; ++t) {
             const int phi = t & 1;
             float nlo = 0.0f, nhi = 0.0f;
-            if (phi == 0) nlo = __shfl_up_sync(0xffffffffu, D[R - 1], 1) + nbmask_lo;
-            else nhi = __shfl_down_sync(0xffffffffu, D[0], 1) + nbmask_hi;
+            if (NOMASK) {
+                if (phi == 0) nlo = __shfl_sync(0xffffffffu, D[R - 1], (lane + 31) & 31);
+                else nhi = __shfl_sync(0xffffffffu, D[0], (lane + 1) & 31);
+            } else {
+                if (phi == 0) nlo = __shfl_up_sync(0xffffffffu, D[R - 1], 1) + nbmask_lo;
+                else nhi = __shfl_down_sync(0xffffffffu, D[0], 1) + nbmask_hi;
+            }
 #pragma unroll
             for (int m = 0; m < H; ++m) {
                 const int r = phi + 2 * m;
@@ -174,51 +208,58 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
         float lmin = D[0];
 #pragma unroll
         for (int r = 1; r < R; ++r) lmin = fminf(lmin, D[r]);
-        float thr = p.mode == 0 ? key_dist(kraw) * (1.0f + p.eps_t) : thr_batch;
+        float thr = p.mode == 0 ? key_dist(kprev) * (1.0f + p.eps_t) : thr_batch;
+        kprev = knext;
         bool vote = !(lmin <= thr);
         unsigned ballot = __ballot_sync(0xffffffffu, vote);
         bool done = active && per == p.nper;
         bool abandon = active && !done && ((ballot & gbits) == gbits);
-        float res = D[0];
+        if (__any_sync(0xffffffffu, done || abandon)) {  // rare: once per item per group
+            float res = D[0];
 #pragma unroll
-        for (int r = 1; r < R; ++r)
-            if (r == r0) res = D[r];
-        if (done && g == g0) {
-            if (p.mode == 0) {
-                unsigned gidx = (unsigned)(p.index_base + ncur);
-                unsigned long long old = atomicMin(p.key + qcur, make_key(res, gidx));
-                float best = fminf(res, key_dist(old));
-                if (res <= best * (1.0f + p.eps_t)) {
-                    unsigned long long slot = atomicAdd(p.log.count, 1ull);
-                    if (slot < p.log.capacity) {
-                        TieEntry e;
-                        e.q = qcur;
-                        e.n = ncur;
-                        e.d32 = res;
-                        e.pad = 0.0f;
-                        e.d64 = 0.0;
-                        p.log.e[slot] = e;
-                    } else {
-                        p.log.overflow[qcur] = 1u;
+            for (int r = 1; r < R; ++r)
+                if (r == r0) res = D[r];
+            if (done && g == g0) {
+                if (p.mode == 0) {
+                    unsigned gidx = (unsigned)(p.index_base + ncur);
+                    unsigned long long old = atomicMin(p.key + qcur, make_key(res, gidx));
+                    float best = fminf(res, key_dist(old));
+                    if (res <= best * (1.0f + p.eps_t)) {
+                        unsigned long long slot = atomicAdd(p.log.count, 1ull);
+                        if (slot < p.log.capacity) {
+                            TieEntry e;
+                            e.q = qcur;
+                            e.n = ncur;
+                            e.d32 = res;
+                            e.pad = 0.0f;
+                            e.d64 = 0.0;
+                            p.log.e[slot] = e;
+                        } else {
+                            p.log.overflow[qcur] = 1u;
+                        }
                     }
+                } else {
+                    p.out[it] = res;
                 }
-            } else {
-                p.out[it] = res;
             }
-        }
-        if (abandon && p.mode == 1 && g == 0) p.out[it] = kInf;
-        if (done || abandon) {
-            if (g == 0 && p.counters != nullptr) {
-                int klast = p.k0 + per * R - 1;
-                if (klast > 2 * L - 2) klast = 2 * L - 2;
-                my_items += 1;
-                my_aband += abandon ? 1 : 0;
-                my_cells += klast >= 0 ? p.cells_prefix[klast] : 0;
+            if (abandon && p.mode == 1 && g == 0) p.out[it] = kInf;
+            if (done || abandon) {
+                if (g == 0 && p.counters != nullptr) {
+                    int klast = p.k0 + per * R - 1;
+                    if (klast > 2 * L - 2) klast = 2 * L - 2;
+                    my_items += 1;
+                    my_aband += abandon ? 1 : 0;
+                    my_cells += klast >= 0 ? p.cells_prefix[klast] : 0;
+                }
+                it += ngroups;
+                active = it < nitems;
+                if (active) {
+                    setup();
+                    if (p.mode == 0) kprev = ld_relaxed_u64(p.key + qcur);
+                } else {
+                    per = 0;  // idle groups replay period 0 (stay in bounds)
+                }
             }
-            it += ngroups;
-            active = it < nitems;
-            if (active) setup();
-            else per = 0;  // idle groups replay period 0 (stay in bounds)
         }
         __syncwarp();
     }
@@ -232,7 +273,7 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
 // ---- host-side selection and launch ----------------------------------------------------------
 struct BandChoice {
     int R, G, gpw, warps;   // warps per CTA
-    bool aligned;
+    int km;                 // kill mode (see k_dtw_band)
     int k0, nper, padl, seglen;
 };
 
@@ -248,19 +289,29 @@ static void band_geometry(int R, int G, int L, int w, BandChoice &c) {
     const int bmax = ((kp_last - w + (G - 1) * R) >> 1) + R - 1 + 1;
     const int lo = amin < bmin ? amin : bmin;
     const int hi = amax > bmax ? amax : bmax;
-    c.padl = (lo < 0 ? -lo : 0) + 1;
+    c.padl = ((lo < 0 ? -lo : 0) + 1 + 3) / 4 * 4;  // 16-byte aligned row start
     const int padr = (hi > L - 1 ? hi - (L - 1) : 0) + 1;
     const int seg = c.padl + L + padr;
-    c.seglen = (seg + 3) / 4 * 4 + 1;  // odd stride: spreads groups over banks
+    // Lanes of a group read with stride R/2 words (distinct banks when R/2 is odd); the
+    // groups of a warp sit 2*seglen words apart -- make that 32/gpw' (mod 32) so that the
+    // groups' bank sets interleave instead of colliding (gpw' = gpw rounded up to 2^k).
+    int gpw = 32 / G, gp2 = 1;
+    while (gp2 < gpw) gp2 <<= 1;
+    const int want = (32 / gp2) / 2;  // seglen mod 16 (2*seglen mod 32 = 32/gp2)
+    int sl = seg;
+    while ((sl & 15) != (want & 15)) ++sl;
+    c.seglen = sl;
 }
 
-// Model: warp-instructions per useful cell (1.5R^2 cell ops + 2R-1 LDS + R shuffles/selects
-// + ~15 bookkeeping per period, over gpw*R*(w+1/2) in-band cells per period), divided by an
-// occupancy factor (warps resident per SM / 16, limited by shared memory and registers).
+// Model: per period a lane issues 1.5R^2 cell ops,
+// 2R-1 LDS, R shuffles (+R edge-mask adds unless KM=2) and ~20 bookkeeping instructions; the
+// edge-cell chain (shuffle + min + fma, ~38 cycles) bounds a warp to >= 38R cycles per
+// period.  Useful cells per SMSP-cycle = wps*gpw*R*(w+1/2)*slot_util / max(wps*issue, 38R),
+// wps = resident warps per scheduler (shared memory / register limited).
 static BandChoice choose_band(int w, int L) {
     BandChoice best{};
     best.R = 0;
-    double bc = 1e30;
+    double bt = 0;
     for (int R = 2; R <= 32; R += 2) {
         int G = (2 * w + 2 + R - 1) / R;
         if (G > 32) continue;
@@ -270,7 +321,7 @@ static BandChoice choose_band(int w, int L) {
         c.R = R;
         c.G = G;
         c.gpw = 32 / G;
-        c.aligned = aligned;
+        c.km = aligned ? ((c.gpw * G == 32) ? 2 : 1) : 0;
         band_geometry(R, G, L, w, c);
         const double warp_smem = (double)c.gpw * 2 * c.seglen * sizeof(float);
         int warps = (int)((200.0 * 1024) / warp_smem);
@@ -278,17 +329,21 @@ static BandChoice choose_band(int w, int L) {
         if (warps > 8) warps = 8;
         c.warps = warps;
         const int ctas_smem = (int)((227.0 * 1024) / (warps * warp_smem));
-        const int regs = aligned ? 56 + 2 * R : 56 + 3 * R;
+        const int regs = c.km >= 1 ? 48 + 2 * R : 48 + 3 * R;
         const int ctas_regs = 65536 / (regs * 32 * warps);
         int ctas = ctas_smem < ctas_regs ? ctas_smem : ctas_regs;
+        if (ctas < 1) continue;
         int wsm = ctas * warps;
         if (wsm > 48) wsm = 48;
-        const double occ = wsm >= 16 ? 1.0 : (double)wsm / 16.0;
-        const double per_lane = (double)R * 1.5 * R + (2.0 * R - 1) + R + 15.0;
-        const double cost = per_lane / ((double)c.gpw * R * (w + 0.5)) / occ *
-                            (aligned ? 1.0 : 1.02);
-        if (cost < bc) {
-            bc = cost;
+        const double wps = wsm / 4.0;
+        const double issue = 1.5 * R * R + (2.0 * R - 1) + R + (c.km == 2 ? 0 : R) + 20.0 +
+                             (((R / 2) & 1) ? 0.0 : 0.15 * R * R);  // even R/2: bank conflicts
+        const double chain = 38.0 * R;
+        const double util = (double)(2 * w + 1) / (double)(G * R);
+        const double thr = wps * c.gpw * R * (w + 0.5) * util /
+                           (wps * issue > chain ? wps * issue : chain);
+        if (thr > bt) {
+            bt = thr;
             best = c;
         }
     }
@@ -297,9 +352,9 @@ static BandChoice choose_band(int w, int L) {
 
 bool band_supported(int w, int L) { return choose_band(w, L).R != 0; }
 
-template <int R, bool AL>
+template <int R, int KM>
 static int launch_band_t(BandParams &p, const BandChoice &c, cudaStream_t st, int num_sms) {
-    auto kern = k_dtw_band<R, AL>;
+    auto kern = k_dtw_band<R, KM>;
     const int block = 32 * c.warps;
     size_t smem = (size_t)c.warps * p.gpw * 2 * p.seglen * sizeof(float);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -319,18 +374,25 @@ static int launch_band_t(BandParams &p, const BandChoice &c, cudaStream_t st, in
 
 #define BAND_CASE(RR)                                                         \
     case RR:                                                                  \
-        return c.aligned ? launch_band_t<RR, true>(p, c, st, num_sms)         \
-                         : launch_band_t<RR, false>(p, c, st, num_sms);
+        return c.km == 2   ? launch_band_t<RR, 2>(p, c, st, num_sms)          \
+               : c.km == 1 ? launch_band_t<RR, 1>(p, c, st, num_sms)          \
+                           : launch_band_t<RR, 0>(p, c, st, num_sms);
 
 int launch_dtw_band(BandParams p, cudaStream_t st, int num_sms) {
     BandChoice c = choose_band(p.w, p.L);
     if (c.R == 0) return -1;
+    static const bool verbose = getenv("NNDTW_VERBOSE") != nullptr;
+    if (verbose)
+        fprintf(stderr, "nndtw band: L=%d w=%d -> R=%d G=%d gpw=%d km=%d warps/cta=%d seglen=%d\n",
+                p.L, p.w, c.R, c.G, c.gpw, c.km, c.warps, c.seglen);
     p.G = c.G;
     p.gpw = c.gpw;
     p.k0 = c.k0;
     p.nper = c.nper;
     p.padl = c.padl;
     p.seglen = c.seglen;
+    p.vec4 = (p.L % 4 == 0 && c.seglen % 4 == 0 && c.padl % 4 == 0 &&
+              ((uintptr_t)p.A % 16) == 0 && ((uintptr_t)p.B % 16) == 0) ? 1 : 0;
     switch (c.R) {
         BAND_CASE(2)
         BAND_CASE(4)
