@@ -519,7 +519,9 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
         int rc = launch_dtw_band(p, st, num_sms);
         if (rc == 0) return 0;
     }
-    return -1;
+    return launch_dtw_strip(A, B, items, nitems_dev, item_cap, ia, ib, nitems_host, L, w, mode,
+                            key, index_base, eps_t, log, counters, cells_prefix, cutoff, out, st,
+                            num_sms);
 }
 
 }  // namespace nndtw

@@ -1,0 +1,263 @@
+// dtw_strip.cu -- S4 for long windows (w too wide for the band-register layout, e.g.
+// BJ:configs[4], L = 2048, w = L-1): windowed DTW (Eq. 1) by row strips.
+//
+// B200 design.  One warp per (query, train) pair.  The matrix is
+// cut into strips of H = 32*RR rows; lane l owns rows i0 + l*RR .. i0 + l*RR + RR-1 and sweeps
+// the columns with a one-lane skew (lane l is at column j = s - l on step s), so the value from
+// the row above (lane l-1's bottom row, one step earlier) arrives by one warp shuffle.  Inside a
+// lane the RR rows are evaluated top-down, keeping the previous column in registers:
+//     D(i,j) = (A_i - B_j)^2 + min(D(i,j-1), D(i-1,j-1), D(i-1,j))
+// The bottom row of a strip is written to shared memory (the next strip's "row above") and its
+// minimum -- a complete row, hence a cut of every warping path (reading C14) -- decides early
+// abandoning against the live best-so-far.  B and the strip rows live in shared memory; padded
+// B values (+/-2^64) make out-of-range columns +inf.  When w < L-1, cells with |i-j| > w are
+// masked to +inf (MASK variant).
+#include "launchers.cuh"
+
+namespace nndtw {
+
+constexpr int STRIP_PAD = 40;  // B pads on each side (>= 32 skew steps)
+
+struct StripParams {
+    const float *A, *B;
+    const Item *items;
+    const unsigned long long *nitems_dev;
+    unsigned long long item_cap;
+    const int32_t *ia, *ib;
+    int64_t nitems_host;
+    int L, w, mode;
+    unsigned long long *key;
+    int64_t index_base;
+    float eps_t;
+    TieLog log;
+    unsigned long long *counters;
+    const long long *cells_prefix;
+    const float *cutoff;
+    float *out;
+    int rowlen;  // floats per warp region: (L + 2*PAD) for B, then L + 1 for the row buffer
+};
+
+template <int RR, bool MASK>
+__global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
+    extern __shared__ __align__(16) float smem_s[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int L = p.L, w = p.w;
+    float *sB = smem_s + (size_t)warp * p.rowlen;           // B[j] at sB[PAD + j]
+    float *rb = sB + (L + 2 * STRIP_PAD);                    // rb[1 + j] = row above, column j
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int64_t nitems = p.nitems_host;
+    if (p.mode == 0) {
+        unsigned long long c = *p.nitems_dev;
+        nitems = (int64_t)(c < p.item_cap ? c : p.item_cap);
+    }
+    // B pads: -2^64*(k+1) before, +2^64*(k+1) after (distinct from the A pad below)
+    for (int x = lane; x < STRIP_PAD; x += 32) {
+        sB[STRIP_PAD - 1 - x] = -0x1p64f * (float)(x + 1);
+        sB[STRIP_PAD + L + x] = 0x1p64f * (float)(x + 1);
+    }
+    const int H = 32 * RR;
+    const int nstrips = (L + H - 1) / H;
+    const int nsteps = L + 31;
+    long long my_items = 0, my_aband = 0, my_cells = 0;
+
+    for (int64_t it = gw; it < nitems; it += nwarps) {
+        unsigned a_idx, b_idx;
+        float thr_batch = kInf;
+        if (p.mode == 0) {
+            Item itm = p.items[it];
+            a_idx = itm.q;
+            b_idx = itm.n;
+        } else {
+            a_idx = p.ia ? (unsigned)p.ia[it] : (unsigned)it;
+            b_idx = p.ib ? (unsigned)p.ib[it] : (unsigned)it;
+            thr_batch = p.cutoff ? p.cutoff[it] * (1.0f + p.eps_t) : kInf;
+        }
+        const float *ga = p.A + (int64_t)a_idx * L;
+        const float *gb = p.B + (int64_t)b_idx * L;
+        __syncwarp();
+        for (int x = lane; x < L; x += 32) cp_async4(sB + STRIP_PAD + x, gb + x);
+        for (int x = lane; x < L; x += 32) rb[1 + x] = kInf;  // D(-1, j) = +inf
+        if (lane == 0) rb[0] = 0.0f;                          // D(-1,-1) = 0
+        cp_async_wait_all();
+        __syncwarp();
+
+        float res = kInf;
+        bool abandoned = false;
+        int strips_done = 0;
+        for (int st = 0; st < nstrips; ++st) {
+            const int i0 = st * H + lane * RR;  // first row of this lane
+            float a[RR], Dl[RR];
+#pragma unroll
+            for (int r = 0; r < RR; ++r) {
+                const int i = i0 + r;
+                a[r] = i < L ? __ldg(ga + i) : 0x1p64f * 3.0f;  // rows past the end: +inf cells
+                Dl[r] = kInf;                                    // D(i, -1) = +inf
+            }
+            // the live best-so-far, used for the abandon test at the end of this strip
+            float thr = thr_batch;
+            if (p.mode == 0) thr = key_dist(ld_relaxed_u64(p.key + a_idx)) * (1.0f + p.eps_t);
+            float up_prev = (lane == 0) ? rb[0] : kInf;  // diagonal input of the top row
+            float bot = kInf;
+            float rowmin = kInf;
+            const bool last = (st == nstrips - 1);
+            const int rstar = (L - 1) - (st * H + lane * RR);  // row L-1 in this lane?
+            for (int s = 0; s < nsteps; ++s) {
+                const int j = s - lane;
+                const float b = sB[STRIP_PAD + j];
+                const float from_up = __shfl_up_sync(0xffffffffu, bot, 1);
+                const int jc = j < 0 ? 0 : (j > L - 1 ? L - 1 : j);
+                const float rbv = rb[1 + jc];
+                const float up = (lane == 0) ? ((j >= 0 && j < L) ? rbv : kInf) : from_up;
+                float dgv = up_prev, upv = up;
+#pragma unroll
+                for (int r = 0; r < RR; ++r) {
+                    const float t = a[r] - b;
+                    const float old = Dl[r];
+                    float nv = fmaf(t, t, fminf(fminf(old, dgv), upv));
+                    if (MASK) {
+                        const int i = i0 + r;
+                        if (j - i > w || i - j > w) nv = kInf;
+                    }
+                    Dl[r] = nv;
+                    dgv = old;
+                    upv = nv;
+                }
+                up_prev = up;
+                bot = Dl[RR - 1];
+                if (lane == 31 && j >= 0 && j < L) {
+                    rb[1 + j] = bot;
+                    rowmin = fminf(rowmin, bot);
+                }
+                if (last && j == L - 1 && rstar >= 0 && rstar < RR) {
+#pragma unroll
+                    for (int r = 0; r < RR; ++r)
+                        if (r == rstar) res = Dl[r];
+                }
+            }
+            __syncwarp();
+            // column -1 of the next strip's row above is +inf (only row -1 has the 0 corner)
+            if (lane == 0) rb[0] = kInf;
+            ++strips_done;
+            if (!last) {
+                const float rm = __shfl_sync(0xffffffffu, rowmin, 31);
+                if (!(rm <= thr)) {
+                    abandoned = true;
+                    break;
+                }
+            }
+            __syncwarp();
+        }
+        // the lane that owned row L-1 holds the result
+        const int owner = ((L - 1) % H) / RR;
+        res = __shfl_sync(0xffffffffu, res, owner);
+        if (lane == 0) {
+            if (p.mode == 0) {
+                if (!abandoned) {
+                    unsigned gidx = (unsigned)(p.index_base + b_idx);
+                    unsigned long long old = atomicMin(p.key + a_idx, make_key(res, gidx));
+                    float best = fminf(res, key_dist(old));
+                    if (res <= best * (1.0f + p.eps_t)) {
+                        unsigned long long slot = atomicAdd(p.log.count, 1ull);
+                        if (slot < p.log.capacity) {
+                            TieEntry e;
+                            e.q = a_idx;
+                            e.n = b_idx;
+                            e.d32 = res;
+                            e.pad = 0.0f;
+                            e.d64 = 0.0;
+                            p.log.e[slot] = e;
+                        } else {
+                            p.log.overflow[a_idx] = 1u;
+                        }
+                    }
+                }
+            } else {
+                p.out[it] = abandoned ? kInf : res;
+            }
+            if (p.counters) {
+                my_items += 1;
+                my_aband += abandoned ? 1 : 0;
+                // in-band cells of the completed rows (strips are row ranges), closed form
+                long long c;
+                if (!abandoned) {
+                    c = p.cells_prefix[2 * L - 2];
+                } else {
+                    const long long R = strips_done * H < L ? strips_done * H : L;
+                    long long t = L - w;  // rows i with i + w <= L-1
+                    t = t < 0 ? 0 : (t > R ? R : t);
+                    long long s1 = t * (t - 1) / 2 + t * (long long)w + (R - t) * (L - 1);
+                    long long m = R - 1 - w;
+                    long long s2 = m > 0 ? m * (m + 1) / 2 : 0;
+                    c = s1 - s2 + R;
+                }
+                my_cells += c;
+            }
+        }
+    }
+    if (p.counters && lane == 0 && my_items > 0) {
+        atomicAdd(p.counters + CNT_ITEMS, (unsigned long long)my_items);
+        atomicAdd(p.counters + CNT_ABANDONED, (unsigned long long)my_aband);
+        atomicAdd(p.counters + CNT_CELLS, (unsigned long long)my_cells);
+    }
+}
+
+template <int RR, bool MASK>
+static int launch_strip_t(StripParams &p, cudaStream_t st, int num_sms) {
+    auto kern = k_dtw_strip<RR, MASK>;
+    const int warps = 4;
+    size_t smem = (size_t)warps * p.rowlen * sizeof(float);
+    if (smem > 220 * 1024) return -2;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem);
+    if (occ < 1) occ = 1;
+    int64_t grid = (int64_t)num_sms * occ;
+    if (p.mode == 1) {
+        int64_t need = (p.nitems_host + warps - 1) / warps;
+        if (need < grid) grid = need > 0 ? need : 1;
+    }
+    kern<<<(unsigned)grid, warps * 32, smem, st>>>(p);
+    count_launch(1, __func__);
+    return 0;
+}
+
+int launch_dtw_strip(const float *A, const float *B, const Item *items,
+                     const unsigned long long *nitems_dev, unsigned long long item_cap,
+                     const int32_t *ia, const int32_t *ib, int64_t nitems_host, int L, int w,
+                     int mode, unsigned long long *key, int64_t index_base, float eps_t,
+                     TieLog log, unsigned long long *counters, const long long *cells_prefix,
+                     const float *cutoff, float *out, cudaStream_t st, int num_sms) {
+    StripParams p;
+    p.A = A;
+    p.B = B;
+    p.items = items;
+    p.nitems_dev = nitems_dev;
+    p.item_cap = item_cap;
+    p.ia = ia;
+    p.ib = ib;
+    p.nitems_host = nitems_host;
+    p.L = L;
+    p.w = w;
+    p.mode = mode;
+    p.key = key;
+    p.index_base = index_base;
+    p.eps_t = eps_t;
+    p.log = log;
+    p.counters = counters;
+    p.cells_prefix = cells_prefix;
+    p.cutoff = cutoff;
+    p.out = out;
+    p.rowlen = (L + 2 * STRIP_PAD) + (L + 1);
+    p.rowlen = (p.rowlen + 3) / 4 * 4;
+    const bool mask = w < L - 1;
+    if (L >= 1024) {
+        return mask ? launch_strip_t<16, true>(p, st, num_sms)
+                    : launch_strip_t<16, false>(p, st, num_sms);
+    }
+    return mask ? launch_strip_t<8, true>(p, st, num_sms)
+                : launch_strip_t<8, false>(p, st, num_sms);
+}
+
+}  // namespace nndtw

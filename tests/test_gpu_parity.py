@@ -210,3 +210,44 @@ def test_loocv_reduced(dev, oracle_lib):
     err2, nn2, _ = nndtw.loocv_window(T(X, dev), T(lab, dev), windows, v=5, q_begin=60,
                                       q_end=170, with_nn=True)
     assert np.array_equal(nn2.cpu().numpy(), rnn[:, 60:170].astype(np.int32))
+
+
+# ---------------------------------------------------------------- S4 long windows (strip kernel)
+@pytest.mark.parametrize("L,ws", [(1024, (1023, 600, 515)), (2048, (2047, 1500)),
+                                  (700, (699, 520)), (1100, (1099,))])
+def test_dtw_batch_long_windows(dev, oracle_lib, L, ws):
+    from paper_1808_09617_b200 import nndtw
+    rng = np.random.default_rng(L)
+    A = datagen.random_series(rng, 6, L, "walk")
+    B = datagen.random_series(rng, 6, L, "walk")
+    B[1] = A[1]
+    for w in ws:
+        out = nndtw.dtw_batch(T(A, dev), T(B, dev), w).cpu().numpy()
+        ref = np.array([oracle_lib.dtw(A[p], B[p], w) for p in range(6)])
+        assert_rel(out, ref, what=f"L={L} w={w}")
+        cut = (ref * np.array([0.3, 2.0, 0.9, 1.1, 0.5, 1.5])).astype(np.float32)
+        out2 = nndtw.dtw_batch(T(A, dev), T(B, dev), w, cutoff=T(cut, dev)).cpu().numpy()
+        ab = np.isinf(out2)
+        assert np.all(ref[ab] > cut[ab])
+        assert_rel(out2[~ab], ref[~ab], what=f"L={L} w={w} cutoff")
+
+
+def test_classify_long_window_small(dev, oracle_lib):
+    ds = datagen.make_dataset(4, n_train=300, n_test=12)
+    w = ds.cfg.windows()[0]
+    idx, lab, dist, st = _classify(dev, ds.train, ds.train_labels, ds.test, w, 8, stats=True)
+    _check_nn(oracle_lib, ds.train, ds.train_labels, ds.test, w, idx, lab, dist)
+
+
+@pytest.mark.slow
+def test_classify_config4_full_sampled(dev, oracle_lib):
+    """BJ:configs[4] at full size (1e3 queries x 1e4 train, L=2048, w=L-1, V=8); a seeded
+    sample of queries checked against the oracle's pruned search."""
+    ds = datagen.make_dataset(4)
+    w = ds.cfg.windows()[0]
+    idx, lab, dist, st = _classify(dev, ds.train, ds.train_labels, ds.test, w, 8, stats=True)
+    rng = np.random.default_rng(4)
+    sample = np.sort(rng.choice(ds.test.shape[0], size=6, replace=False))
+    ridx, rdist = oracle_lib.nn(ds.test[sample], ds.train, w, V=8, mode="pruned")
+    assert np.array_equal(idx[sample], ridx)
+    assert_rel(dist[sample], rdist, what="config 4 sample")
