@@ -93,6 +93,7 @@ struct ClassifyWs {
     nndtw_kim *qkim;
     unsigned long long *minkey, *f64key, *resolve_out;
     unsigned *overflow;
+    unsigned *tiecnt;
     float *lb;
     int64_t ldlb;
     Item *seed_items;
@@ -123,6 +124,7 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
     W.f64key = (unsigned long long *)take(8 * q1);
     W.resolve_out = (unsigned long long *)take(8 * q1);
     W.overflow = (unsigned *)take(4 * q1);
+    W.tiecnt = (unsigned *)take(4 * q1);
     W.ldlb = (nt + 3) / 4 * 4;
     W.lb = (float *)take(sizeof(float) * (size_t)nq * (size_t)W.ldlb);
     W.seed_items = (Item *)take(sizeof(Item) * (2 * q1 + 1));
@@ -177,7 +179,10 @@ static void exact_local(ClassifyWs &W, const float *q, int64_t nq, const float *
                         int L, int w, int64_t index_base, unsigned long long *key,
                         unsigned long long *cnt, int sms, cudaStream_t st) {
     const float eps_p = eps_prune(L), eps_t = eps_tie(L);
-    launch_refine(W.log, W.log_count, W.log_cap, q, t, L, w, key, eps_t, W.f64key, cnt, sms, st);
+    cudaMemsetAsync(W.tiecnt, 0, 4 * (size_t)nq, st);
+    launch_tie_count(W.log, W.log_count, W.log_cap, key, eps_t, W.tiecnt, sms, st);
+    launch_refine(W.log, W.log_count, W.log_cap, q, t, L, w, key, eps_t, W.f64key, cnt,
+                  W.tiecnt, W.overflow, sms, st);
     launch_refine_overflow(W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w, key, eps_p, 0,
                            W.f64key, nullptr, index_base, nullptr, sms, st);
     launch_resolve(W.log, W.log_count, W.log_cap, W.f64key, index_base, W.resolve_out, sms, st);
@@ -414,7 +419,7 @@ int nndtw_classify_refine(void *ws, size_t ws_bytes, const float *q, int64_t nq,
     if (nt > 0) {
         launch_refine(W.log, W.log_count, W.log_cap, q, t, L, w,
                       (const unsigned long long *)gkey, eps_tie(L),
-                      (unsigned long long *)f64key, nullptr, sms, st);
+                      (unsigned long long *)f64key, nullptr, nullptr, W.overflow, sms, st);
         launch_refine_overflow(W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w,
                                (const unsigned long long *)gkey, eps_prune(L), 0,
                                (unsigned long long *)f64key, nullptr, 0, nullptr, sms, st);

@@ -23,7 +23,11 @@ int launch_cells_prefix(int L, int w, long long *prefix, cudaStream_t st);
 int launch_refine(TieEntry *e, const unsigned long long *count, unsigned long long cap,
                   const float *A, const float *B, int L, int w, const unsigned long long *gkey,
                   float eps_t, unsigned long long *f64key, unsigned long long *counters,
-                  int num_sms, cudaStream_t st);
+                  const unsigned *tiecnt, const unsigned *overflow, int num_sms,
+                  cudaStream_t st);
+int launch_tie_count(const TieEntry *e, const unsigned long long *count, unsigned long long cap,
+                     const unsigned long long *gkey, float eps_t, unsigned *tiecnt, int num_sms,
+                     cudaStream_t st);
 int launch_refine_overflow(const unsigned *overflow, int64_t nq, const float *lb, int64_t ldlb,
                            int64_t nt, const float *A, const float *B, int L, int w,
                            const unsigned long long *gkey, float eps_p, int pass,

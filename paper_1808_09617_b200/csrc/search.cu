@@ -215,10 +215,33 @@ __device__ double dtw64_warp(const float *__restrict__ a, const float *__restric
     return result;
 }
 
+// Near-tie set sizes (single-shard EXACT mode): a query whose band holds one candidate needs no
+// fp64 re-rank -- that candidate is the unique minimum.
+__global__ void k_tie_count(const TieEntry *e, const unsigned long long *count,
+                            unsigned long long cap, const unsigned long long *gkey, float eps_t,
+                            unsigned *tiecnt) {
+    unsigned long long n = *count;
+    if (n > cap) n = cap;
+    for (unsigned long long x = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+         x += (unsigned long long)gridDim.x * blockDim.x) {
+        TieEntry t = e[x];
+        if (t.d32 <= key_dist(gkey[t.q]) * (1.0f + eps_t)) atomicAdd(tiecnt + t.q, 1u);
+    }
+}
+
+int launch_tie_count(const TieEntry *e, const unsigned long long *count, unsigned long long cap,
+                     const unsigned long long *gkey, float eps_t, unsigned *tiecnt, int num_sms,
+                     cudaStream_t st) {
+    k_tie_count<<<num_sms * 2, 256, 0, st>>>(e, count, cap, gkey, eps_t, tiecnt);
+    count_launch(1, __func__);
+    return 0;
+}
+
 __global__ void k_refine(TieEntry *e, const unsigned long long *count, unsigned long long cap,
                          const float *__restrict__ A, const float *__restrict__ B, int L, int w,
                          const unsigned long long *__restrict__ gkey, float eps_t,
-                         unsigned long long *f64key, unsigned long long *counters) {
+                         unsigned long long *f64key, unsigned long long *counters,
+                         const unsigned *tiecnt, const unsigned *overflow) {
     extern __shared__ double dbuf[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
@@ -230,6 +253,14 @@ __global__ void k_refine(TieEntry *e, const unsigned long long *count, unsigned 
         TieEntry t = e[x];
         float gb = key_dist(gkey[t.q]);
         if (t.d32 <= gb * (1.0f + eps_t)) {
+            if (tiecnt != nullptr && tiecnt[t.q] == 1u && !overflow[t.q]) {
+                if (lane == 0) {  // singleton band: the candidate is the answer
+                    e[x].d64 = 0.0;
+                    atomicMin(f64key + t.q, 0ull);
+                }
+                __syncwarp();
+                continue;
+            }
             double d = dtw64_warp(A + (int64_t)t.q * L, B + (int64_t)t.n * L, L, w, buf);
             if (lane == 0) {
                 e[x].d64 = d;
@@ -287,13 +318,14 @@ static int refine_block(int L, size_t *smem) {
 int launch_refine(TieEntry *e, const unsigned long long *count, unsigned long long cap,
                   const float *A, const float *B, int L, int w, const unsigned long long *gkey,
                   float eps_t, unsigned long long *f64key, unsigned long long *counters,
-                  int num_sms, cudaStream_t st) {
+                  const unsigned *tiecnt, const unsigned *overflow, int num_sms,
+                  cudaStream_t st) {
     if (w > L - 1) w = L - 1;
     size_t smem;
     int block = refine_block(L, &smem);
     cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_refine<<<num_sms * 2, block, smem, st>>>(e, count, cap, A, B, L, w, gkey, eps_t, f64key,
-                                               counters);
+                                               counters, tiecnt, overflow);
     count_launch(1, __func__);
     return 0;
 }
