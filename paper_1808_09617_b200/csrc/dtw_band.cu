@@ -110,6 +110,8 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
     bool active = valid_lane && it < nitems;
 
     float D[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) D[r] = kInf;  // idle lanes too (their values feed shuffles)
     int per = 0;
     unsigned qcur = 0, ncur = 0;
     float thr_batch = kInf;
@@ -214,6 +216,12 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
         unsigned ballot = __ballot_sync(0xffffffffu, vote);
         bool done = active && per == p.nper;
         bool abandon = active && !done && ((ballot & gbits) == gbits);
+#ifdef NNDTW_TRACE
+        if (active && p.mode == 0 && blockIdx.x == 0 && warp == 0 && lane < 2)
+            printf("TRACE lane=%d it=%lld q=%u n=%u per=%d/%d lmin=%g thr=%g D0=%g done=%d ab=%d\n",
+                   lane, (long long)it, qcur, ncur, per, p.nper, lmin, thr, D[0], (int)done,
+                   (int)abandon);
+#endif
         if (__any_sync(0xffffffffu, done || abandon)) {  // rare: once per item per group
             float res = D[0];
 #pragma unroll
