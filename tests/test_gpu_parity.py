@@ -251,3 +251,27 @@ def test_classify_config4_full_sampled(dev, oracle_lib):
     ridx, rdist = oracle_lib.nn(ds.test[sample], ds.train, w, V=8, mode="pruned")
     assert np.array_equal(idx[sample], ridx)
     assert_rel(dist[sample], rdist, what="config 4 sample")
+
+
+@pytest.mark.slow
+def test_loocv_config3_full_sampled(dev, oracle_lib):
+    """BJ:configs[3] at full size (2000 series, all 101 windows): per-window NN ids of a seeded
+    sample of held-out series are checked against the oracle (exhaustive over j != i)."""
+    import torch
+    from paper_1808_09617_b200 import nndtw
+    ds = datagen.make_dataset(3)
+    X, lab = ds.train, ds.train_labels
+    wins = ds.cfg.windows()
+    err, nn, _ = nndtw.loocv_window(T(X, dev), T(lab, dev), wins, v=5, with_nn=True)
+    nn = nn.cpu().numpy()
+    err = err.cpu().numpy()
+    # error counts are consistent with the reported neighbours
+    for p in range(len(wins)):
+        assert err[p] == int(np.sum(lab[nn[p]] != lab))
+    rng = np.random.default_rng(3)
+    sample = rng.choice(X.shape[0], size=4, replace=False)
+    widx = [0, 1, 7, 20, 50, 100]
+    for i in sample:
+        rerr, rnn = oracle_lib.loocv(X, lab, [wins[p] for p in widx], V=5, q_begin=int(i),
+                                     q_end=int(i) + 1, mode="pruned")
+        assert np.array_equal(nn[widx, i], rnn[:, 0].astype(np.int32)), (i, nn[widx, i], rnn[:, 0])
