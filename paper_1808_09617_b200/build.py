@@ -54,7 +54,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
         raise RuntimeError(f"nvcc failed for {failed}")
     tmp = LIB + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
-                           *objs, "-o", tmp, "-cudart", "static"])
+                           *objs, "-o", tmp, "-cudart", "static",
+                           "-Xlinker", "--no-undefined"])
     os.replace(tmp, LIB)
     return LIB
 

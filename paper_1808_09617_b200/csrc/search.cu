@@ -167,52 +167,72 @@ int launch_cells_prefix(int L, int w, long long *prefix, cudaStream_t st) {
 }
 
 // ---- S7: fp64 DTW with the oracle's per-cell operation sequence --------------------------------
-// d = a - b; delta = d*d; m = min(diag, left, up) (exact); D = delta + m; D(0,0) = delta.
-// One warp per pair, anti-diagonal order, three diagonals of doubles in shared memory.
-// (Evaluation order does not change any cell's value, so the result is bit-identical to a
-// row-by-row evaluation with the same operations.)
+// d = a - b; delta = d*d; m = min(diag, left, up) (exact); D = delta + m; D(0,0) = delta;
+// out-of-band cells are +inf.  Evaluation order does not change any cell's value, so the result
+// is bit-identical to the oracle's row-by-row evaluation with the same operations.
+// One warp per pair, row strips of 32*RR64 rows: lane l owns RR64 consecutive rows and sweeps the
+// columns with a one-lane skew; the row above a lane's top row arrives by shuffle (lane l-1's
+// bottom row one step earlier) or, for lane 0, from the previous strip's bottom row kept in
+// shared memory (buf: L+1 doubles; buf[1+j] = D(row above, j), buf[0] = D(row above, -1)).
+constexpr int RR64 = 8;
+
 __device__ double dtw64_warp(const float *__restrict__ a, const float *__restrict__ b, int L,
                              int w, double *buf) {
     const int lane = threadIdx.x & 31;
-    double *d0 = buf, *d1 = buf + L, *d2 = buf + 2 * L;  // diagonals k, k-1, k-2 (by row i)
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
-    auto inband = [&](int k, int i) -> bool {
-        int j = k - i;
-        return i >= 0 && i < L && j >= 0 && j < L && (i - j <= w) && (j - i <= w);
-    };
+    const int H = 32 * RR64;
+    for (int j = lane; j < L; j += 32) buf[1 + j] = INF;  // D(-1, j) = +inf
+    if (lane == 0) buf[0] = 0.0;                           // D(-1,-1) = 0
+    __syncwarp();
     double result = INF;
-    for (int k = 0; k <= 2 * L - 2; ++k) {
-        int ilo = k - (L - 1) > 0 ? k - (L - 1) : 0;
-        int ihi = k < L - 1 ? k : L - 1;
-        for (int i = ilo + lane; i <= ihi; i += 32) {
-            int j = k - i;
-            if (i - j > w || j - i > w) continue;
-            double dd = __dsub_rn((double)a[i], (double)b[j]);
-            double delta = __dmul_rn(dd, dd);
-            double m;
-            if (i == 0 && j == 0) {
-                m = 0.0;
-            } else {
-                double dg = (i >= 1 && j >= 1 && inband(k - 2, i - 1)) ? d2[i - 1] : INF;
-                double lf = (j >= 1 && inband(k - 1, i)) ? d1[i] : INF;
-                double up = (i >= 1 && inband(k - 1, i - 1)) ? d1[i - 1] : INF;
-                m = fmin(fmin(dg, lf), up);
+    for (int i0s = 0; i0s < L; i0s += H) {
+        const int i0 = i0s + lane * RR64;
+        double av[RR64], Dl[RR64];
+#pragma unroll
+        for (int r = 0; r < RR64; ++r) {
+            av[r] = (i0 + r < L) ? (double)a[i0 + r] : 0.0;
+            Dl[r] = INF;  // D(i, -1)
+        }
+        double up_prev = (lane == 0) ? buf[0] : INF;
+        double bot = INF;
+        for (int s = 0; s < L + 31; ++s) {
+            const int j = s - lane;
+            const double from_up = __shfl_up_sync(0xffffffffu, bot, 1);
+            const bool jin = j >= 0 && j < L;
+            const double bj = jin ? (double)b[j] : 0.0;
+            const double rbv = (lane == 0 && jin) ? buf[1 + j] : INF;
+            const double up = (lane == 0) ? rbv : from_up;
+            double dgv = up_prev, upv = up;
+#pragma unroll
+            for (int r = 0; r < RR64; ++r) {
+                const int i = i0 + r;
+                const double old = Dl[r];
+                double nv = INF;
+                if (jin && i < L && i - j <= w && j - i <= w) {
+                    const double dd = __dsub_rn(av[r], bj);
+                    const double delta = __dmul_rn(dd, dd);
+                    const double m = (i == 0 && j == 0) ? 0.0 : fmin(fmin(dgv, old), upv);
+                    nv = __dadd_rn(delta, m);
+                }
+                if (jin) Dl[r] = nv;
+                dgv = old;
+                upv = jin ? nv : INF;
             }
-            double v = __dadd_rn(delta, m);
-            d0[i] = v;
-            if (k == 2 * L - 2) result = v;
+            up_prev = up;
+            bot = jin ? Dl[RR64 - 1] : INF;
+            if (lane == 31 && jin) buf[1 + j] = bot;
+            if (j == L - 1 && L - 1 >= i0 && L - 1 < i0 + RR64) {
+#pragma unroll
+                for (int r = 0; r < RR64; ++r)
+                    if (i0 + r == L - 1) result = Dl[r];
+            }
         }
         __syncwarp();
-        double *t = d2;
-        d2 = d1;
-        d1 = d0;
-        d0 = t;
+        if (lane == 0) buf[0] = INF;  // D(row above, -1) for later strips
+        __syncwarp();
     }
-    // the last cell (L-1, L-1) was written by lane (L-1 - ilo) % 32 of the last diagonal
-    int owner = ((L - 1) - (L - 1)) & 31;
-    (void)owner;
-    result = __shfl_sync(0xffffffffu, result, 0);
-    return result;
+    const int owner = ((L - 1) % H) / RR64;
+    return __shfl_sync(0xffffffffu, result, owner);
 }
 
 // Near-tie set sizes (single-shard EXACT mode): a query whose band holds one candidate needs no
@@ -245,7 +265,7 @@ __global__ void k_refine(TieEntry *e, const unsigned long long *count, unsigned 
     extern __shared__ double dbuf[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
-    double *buf = dbuf + (size_t)warp * 3 * L;
+    double *buf = dbuf + (size_t)warp * (L + 1);
     unsigned long long n = *count;
     if (n > cap) n = cap;
     for (unsigned long long x = (unsigned long long)blockIdx.x * wpb + warp; x < n;
@@ -286,7 +306,7 @@ __global__ void k_refine_overflow(const unsigned *overflow, int64_t nq, const fl
     extern __shared__ double dbuf[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
-    double *buf = dbuf + (size_t)warp * 3 * L;
+    double *buf = dbuf + (size_t)warp * (L + 1);
     for (int64_t q = 0; q < nq; ++q) {
         if (!overflow[q]) continue;
         float thr = key_dist(gkey[q]) * (1.0f + eps_p);
@@ -310,8 +330,8 @@ __global__ void k_refine_overflow(const unsigned *overflow, int64_t nq, const fl
 
 static int refine_block(int L, size_t *smem) {
     int wpb = 4;
-    while (wpb > 1 && (size_t)wpb * 3 * L * sizeof(double) > 200 * 1024) wpb >>= 1;
-    *smem = (size_t)wpb * 3 * L * sizeof(double);
+    while (wpb > 1 && (size_t)wpb * (L + 1) * sizeof(double) > 200 * 1024) wpb >>= 1;
+    *smem = (size_t)wpb * (L + 1) * sizeof(double);
     return wpb * 32;
 }
 
