@@ -275,3 +275,43 @@ def test_loocv_config3_full_sampled(dev, oracle_lib):
         rerr, rnn = oracle_lib.loocv(X, lab, [wins[p] for p in widx], V=5, q_begin=int(i),
                                      q_end=int(i) + 1, mode="pruned")
         assert np.array_equal(nn[widx, i], rnn[:, 0].astype(np.int32)), (i, nn[widx, i], rnn[:, 0])
+
+
+# ---------------------------------------------------------------- S6 shard protocol (1 GPU)
+@pytest.mark.parametrize("nshards", [2, 3])
+def test_shard_protocol_through_abi(dev, oracle_lib, nshards):
+    """The sharded path of dist.py through the real C ABI, shards run one after another on one
+    GPU and combined with torch.minimum (= the int64 MIN all-reduce): refine and resolve must
+    give the exact global 1-NN, including exact ties split across shards."""
+    import torch
+    from paper_1808_09617_b200 import nndtw
+    from paper_1808_09617_b200.dist import shard_range
+    rng = np.random.default_rng(nshards)
+    L, w, V = 64, 6, 5
+    Tr = datagen.random_series(rng, 300, L, "int")
+    Tr[250] = Tr[20]      # duplicates in different shards
+    Tr[299] = Tr[120]
+    Q = datagen.random_series(rng, 40, L, "int")
+    Q[0] = Tr[20]
+    Q[1] = Tr[120]
+    labels = rng.integers(0, 5, size=300).astype(np.int32)
+    q = T(Q, dev)
+    models = []
+    for r in range(nshards):
+        lo, hi = shard_range(300, r, nshards)
+        models.append(nndtw.Model(T(Tr[lo:hi], dev), T(labels[lo:hi], dev), w, V, index_base=lo))
+    outs = [nndtw.classify_keys(m, q, exact=False) for m in models]
+    gkey = outs[0][0].clone()
+    for k, _, _ in outs[1:]:
+        gkey = torch.minimum(gkey, k)
+    f64 = [nndtw.classify_refine(m, q, ws, gkey) for m, (_, ws, _) in zip(models, outs)]
+    gf64 = f64[0].clone()
+    for x in f64[1:]:
+        gf64 = torch.minimum(gf64, x)
+    res = [nndtw.classify_resolve(m, q, ws, gkey, gf64) for m, (_, ws, _) in zip(models, outs)]
+    g = res[0].clone()
+    for x in res[1:]:
+        g = torch.minimum(g, x)
+    idx, lab, dist = nndtw.finalize(g, T(labels, dev), key_format=1)
+    _check_nn(oracle_lib, Tr, labels, Q, w, idx.cpu().numpy(), lab.cpu().numpy(),
+              dist.cpu().numpy())
