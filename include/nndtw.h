@@ -106,6 +106,9 @@ NNDTW_API int nndtw_series_stats(const float *x, int64_t n, int32_t L, nndtw_kim
  * else nullable); lb: [nq][ldlb], ldlb >= nt.  fp32 arithmetic.
  */
 #define NNDTW_LB_WITH_KIM 1u
+/* flags & NNDTW_LB_KEOGH: LB_Keogh (m = L, reading C6) over all L columns in place of
+ * LB_Enhanced -- the paper's comparison bound (Fig. 9 normalises by it). */
+#define NNDTW_LB_KEOGH 2u
 NNDTW_API int nndtw_lb_enhanced(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
                       const float *upper, const float *lower, const nndtw_kim *tkim,
                       int64_t nt, int32_t L, int32_t w, int32_t v, uint32_t flags, float *lb,
@@ -142,6 +145,9 @@ NNDTW_API int nndtw_dtw_batch(const float *a, const float *b, const int32_t *ia,
  * pass -1 otherwise.  stats: host, nullable (non-NULL synchronises).
  */
 #define NNDTW_CLASSIFY_EXACT 1u
+/* flags & NNDTW_CLASSIFY_BOUND_KEOGH: prune with max(LB_Kim, LB_Keogh) instead of
+ * max(LB_Kim, LB_Enhanced^V) (same exact answer; a baseline for the V-sweep). */
+#define NNDTW_CLASSIFY_BOUND_KEOGH 2u
 NNDTW_API size_t nndtw_classify_workspace_bytes(int64_t nq, int64_t nt, int32_t L, int32_t w);
 NNDTW_API int nndtw_classify(const float *q, int64_t nq, const float *t, const float *upper,
                    const float *lower, const nndtw_kim *tkim, int64_t nt, int64_t index_base,

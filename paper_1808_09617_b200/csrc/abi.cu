@@ -228,7 +228,8 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     launch_series_stats(q, nq, L, W.qkim, st);
     tm.mark();  // 1
     if (nt > 0 && launch_lb(q, nq, W.qkim, t, U, Lo, tkim, nt, L, w, v, 1, self_offset, W.lb,
-                            W.ldlb, W.minkey, st))
+                            W.ldlb, W.minkey, st,
+                            (flags & NNDTW_CLASSIFY_BOUND_KEOGH) ? 1 : 0))
         return fail(NNDTW_E_ARG, "too many train series for one launch");
     tm.mark();  // 2
     if ((rc = cuda_fail("lb"))) return rc;
@@ -368,7 +369,7 @@ int nndtw_lb_enhanced(const float *q, int64_t nq, const nndtw_kim *qkim, const f
     if (nq > 0 && nt > 0 && (!q || !t || !upper || !lower || !lb || (kim && (!qkim || !tkim))))
         return fail(NNDTW_E_ARG, "null pointer argument");
     if (launch_lb(q, nq, qkim, t, upper, lower, tkim, nt, L, w, v, kim ? 1 : 0, -1, lb, ldlb,
-                  nullptr, (cudaStream_t)stream))
+                  nullptr, (cudaStream_t)stream, (flags & NNDTW_LB_KEOGH) ? 1 : 0))
         return fail(NNDTW_E_ARG, "too many train series for one launch");
     return cuda_fail("nndtw_lb_enhanced");
 }

@@ -33,6 +33,7 @@ struct LbParams {
     const nndtw_kim *tkim;
     int64_t nt;
     int L, w, nb, with_kim;
+    int keogh;  // 1: LB_Keogh over all L columns instead of LB_Enhanced
     int64_t self_offset;
     float *lb;
     int64_t ldlb;
@@ -57,7 +58,9 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
     const int tq = tid >> 5;  // warp index: queries tq*8 .. tq*8+7 of the tile
     const int64_t q0 = (int64_t)blockIdx.x * LB_TQ;
     const int64_t n0 = (int64_t)blockIdx.y * LB_TN;
-    const int L = p.L, nb = p.nb, w = p.w;
+    const int L = p.L, w = p.w;
+    // bands use nb; the bridge covers [nbb, L - nbb): all columns for LB_Keogh
+    const int nb = p.nb, nbb = p.keogh ? 0 : p.nb;
 
     // ---- stage band values and Kim features -------------------------------------------
     if (SMEM_BANDS) {
@@ -88,8 +91,8 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
     }
 
     // ---- column-chunk loader (register prefetch) ------------------------------------------
-    const int ch_begin = nb / LB_CC;
-    const int ch_end = (L - nb + LB_CC - 1) / LB_CC;  // exclusive
+    const int ch_begin = nbb / LB_CC;
+    const int ch_end = (L - nbb + LB_CC - 1) / LB_CC;  // exclusive
     float ra[4];
     float2 re[8];
     auto load_chunk = [&](int ch) {
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
             int e = tid + 256 * k;
             int r = e >> 4, c = c0 + (e & 15);
             int64_t qq = q0 + r;
-            bool ok = qq < p.nq && c >= nb && c < L - nb;
+            bool ok = qq < p.nq && c >= nbb && c < L - nbb;
             ra[k] = ok ? __ldg(p.q + qq * (int64_t)L + c) : 0.0f;
         }
 #pragma unroll
@@ -107,7 +110,7 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
             int e = tid + 256 * k;
             int r = e >> 4, c = c0 + (e & 15);
             int64_t nn = n0 + r;
-            bool ok = nn < p.nt && c >= nb && c < L - nb;
+            bool ok = nn < p.nt && c >= nbb && c < L - nbb;
             int64_t off = nn * (int64_t)L + c;
             re[k] = ok ? make_float2(__ldg(p.U + off), __ldg(p.Lo + off))
                        : make_float2(kInf, -kInf);
@@ -158,9 +161,9 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
     for (int qi = 0; qi < LB_QPT; ++qi)
 #pragma unroll
         for (int j = 0; j < LB_NPT; ++j)
-            acc[qi][j] = sq(qhv(qi, 0) - thv(j, 0)) + sq(qtv(qi, 0) - ttv(j, 0));
+            acc[qi][j] = p.keogh ? 0.0f : sq(qhv(qi, 0) - thv(j, 0)) + sq(qtv(qi, 0) - ttv(j, 0));
 
-    for (int i = 1; i < nb; ++i) {
+    for (int i = 1; i < (p.keogh ? 0 : nb); ++i) {
         const int jlo = i - w > 0 ? i - w : 0;
 #pragma unroll
         for (int side = 0; side < 2; ++side) {
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
 int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
               const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L, int w,
               int v, int with_kim, int64_t self_offset, float *lb, int64_t ldlb,
-              unsigned long long *minkey, cudaStream_t st) {
+              unsigned long long *minkey, cudaStream_t st, int keogh) {
     if (nq == 0 || nt == 0) return 0;
     if (w > L - 1) w = L - 1;
     LbParams p;
@@ -277,6 +280,7 @@ int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
     p.w = w;
     p.nb = (L / 2) < v ? (L / 2) : v;
     p.with_kim = with_kim;
+    p.keogh = keogh;
     p.self_offset = self_offset;
     p.lb = lb;
     p.ldlb = ldlb;

@@ -20,7 +20,9 @@ LIB_PATH = os.path.join(_HERE, "libnndtw_debug.so" if os.environ.get("NNDTW_DEBU
                         else "libnndtw.so")
 
 NNDTW_LB_WITH_KIM = 1
+NNDTW_LB_KEOGH = 2
 NNDTW_CLASSIFY_EXACT = 1
+NNDTW_CLASSIFY_BOUND_KEOGH = 2
 KEY_INIT = 0x7F800000FFFFFFFF
 
 
@@ -138,7 +140,7 @@ def series_stats(x: torch.Tensor, stream=None) -> torch.Tensor:
 
 
 def lb_enhanced(q, t, U, Lo, w: int, v: int, with_kim: bool = False, qkim=None, tkim=None,
-                stream=None) -> torch.Tensor:
+                keogh: bool = False, stream=None) -> torch.Tensor:
     """S2: cascade bound matrix [nq][nt] (Eq. 7 / Algorithm 1; max with LB_Kim if asked)."""
     _series(q, "q"); _series(t, "t"); _series(U, "U"); _series(Lo, "Lo")
     nq, L = q.shape
@@ -150,7 +152,8 @@ def lb_enhanced(q, t, U, Lo, w: int, v: int, with_kim: bool = False, qkim=None, 
     out = torch.empty((nq, nt), dtype=torch.float32, device=q.device)
     _check(load().nndtw_lb_enhanced(_ptr(q), nq, _ptr(qkim), _ptr(t), _ptr(U), _ptr(Lo),
                                     _ptr(tkim), nt, L, int(w), int(v),
-                                    NNDTW_LB_WITH_KIM if with_kim else 0, _ptr(out), nt,
+                                    (NNDTW_LB_WITH_KIM if with_kim else 0) |
+                                    (NNDTW_LB_KEOGH if keogh else 0), _ptr(out), nt,
                                     _stream(stream)), "nndtw_lb_enhanced")
     return out
 
@@ -184,7 +187,7 @@ class Model:
     """A train set with its envelopes and Kim features precomputed "at training time"."""
 
     def __init__(self, train: torch.Tensor, labels: torch.Tensor, w: int, v: int = 5,
-                 index_base: int = 0, check: bool = True, stream=None):
+                 index_base: int = 0, check: bool = True, stream=None, bound: str = "enhanced"):
         _series(train, "train")
         if check and not check_finite(train, stream):
             raise NNDTWError("train set contains NaN or infinity")
@@ -194,6 +197,9 @@ class Model:
         self.w = min(int(w), self.L - 1)
         self.v = int(v)
         self.index_base = int(index_base)
+        if bound not in ("enhanced", "keogh"):
+            raise NNDTWError("bound must be 'enhanced' or 'keogh'")
+        self.bound = bound
         self.U, self.Lo, self.kim = envelopes(train, self.w, True, stream)
         self._ws = None
 
@@ -218,7 +224,9 @@ def classify_keys(model: Model, q: torch.Tensor, exact: bool = True, self_offset
     _check(load().nndtw_classify(_ptr(q), nq, _ptr(model.t), _ptr(model.U), _ptr(model.Lo),
                                  _ptr(model.kim), model.t.shape[0], model.index_base,
                                  int(self_offset), L, model.w, model.v,
-                                 NNDTW_CLASSIFY_EXACT if exact else 0, _ptr(ws), ws.numel(),
+                                 (NNDTW_CLASSIFY_EXACT if exact else 0) |
+                                 (NNDTW_CLASSIFY_BOUND_KEOGH if model.bound == "keogh" else 0),
+                                 _ptr(ws), ws.numel(),
                                  _ptr(key), C.byref(st) if stats else None, _stream(stream)),
            "nndtw_classify")
     return key, ws, (st.as_dict() if stats else None)

@@ -315,3 +315,30 @@ def test_shard_protocol_through_abi(dev, oracle_lib, nshards):
     idx, lab, dist = nndtw.finalize(g, T(labels, dev), key_format=1)
     _check_nn(oracle_lib, Tr, labels, Q, w, idx.cpu().numpy(), lab.cpu().numpy(),
               dist.cpu().numpy())
+
+
+# ---------------------------------------------------------------- NEXT-1: LB_Keogh baseline
+@pytest.mark.parametrize("L,w", [(16, 3), (128, 13), (300, 299), (512, 103)])
+def test_lb_keogh_parity(dev, oracle_lib, L, w):
+    from paper_1808_09617_b200 import nndtw
+    rng = np.random.default_rng(L + w)
+    Q = datagen.random_series(rng, 40, L, "walk")
+    Tn = datagen.random_series(rng, 130, L, "walk")
+    U, Lo, kim = nndtw.envelopes(T(Tn, dev), w)
+    lb = nndtw.lb_enhanced(T(Q, dev), T(Tn, dev), U, Lo, w, 5, keogh=True).cpu().numpy()
+    eu, el = oracle_lib.envelopes(Tn, w)
+    for i in range(0, 40, 3):
+        for j in range(130):
+            ref = oracle_lib.lb_keogh(Q[i], eu[j], el[j])
+            assert abs(lb[i, j] - ref) <= REL * ref + 1e-30, (i, j, lb[i, j], ref)
+
+
+def test_classify_keogh_bound_same_answer(dev, oracle_lib):
+    from paper_1808_09617_b200 import nndtw
+    for cfg, nq in ((0, 100), (1, 60)):
+        ds = datagen.make_dataset(cfg)
+        w = ds.cfg.windows()[0] if cfg == 0 else datagen.window_from_percent(20, 256)
+        model = nndtw.Model(T(ds.train, dev), T(ds.train_labels, dev), w, 5, bound="keogh")
+        pred = nndtw.classify(model, T(ds.test[:nq], dev), stats=True)
+        _check_nn(oracle_lib, ds.train, ds.train_labels, ds.test[:nq], w,
+                  pred.idx.cpu().numpy(), pred.label.cpu().numpy(), pred.dist.cpu().numpy())
