@@ -12,6 +12,8 @@
 // abandoning against the live best-so-far.  B and the strip rows live in shared memory; padded
 // B values (+/-2^64) make out-of-range columns +inf.  When w < L-1, cells with |i-j| > w are
 // masked to +inf (MASK variant).
+#include <type_traits>
+
 #include "launchers.cuh"
 
 namespace nndtw {
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
         const float *gb = p.B + (int64_t)b_idx * L;
         __syncwarp();
         for (int x = lane; x < L; x += 32) cp_async4(sB + STRIP_PAD + x, gb + x);
-        for (int x = lane; x < L; x += 32) rb[1 + x] = kInf;  // D(-1, j) = +inf
+        for (int x = lane; x < L + 32; x += 32) rb[1 + x] = kInf;  // D(-1, j) = +inf; pads
         if (lane == 0) rb[0] = 0.0f;                          // D(-1,-1) = 0
         cp_async_wait_all();
         __syncwarp();
@@ -103,13 +105,15 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
             float rowmin = kInf;
             const bool last = (st == nstrips - 1);
             const int rstar = (L - 1) - (st * H + lane * RR);  // row L-1 in this lane?
-            for (int s = 0; s < nsteps; ++s) {
+            // One column step of this lane's RR rows.  CHECK: ramp-up / ramp-down steps where
+            // some lane's column is outside [0, L) (range-checked); steady steps need no checks.
+            auto step = [&](int s, auto check_tag) {
+                constexpr bool CHECK = decltype(check_tag)::value;
                 const int j = s - lane;
-                const float b = sB[STRIP_PAD + j];
+                const float b = sB[STRIP_PAD + j];  // pads make out-of-range columns +inf
                 const float from_up = __shfl_up_sync(0xffffffffu, bot, 1);
-                const int jc = j < 0 ? 0 : (j > L - 1 ? L - 1 : j);
-                const float rbv = rb[1 + jc];
-                const float up = (lane == 0) ? ((j >= 0 && j < L) ? rbv : kInf) : from_up;
+                const float rbv = rb[1 + s];        // lane 0's column; rb padded with +inf
+                const float up = (lane == 0) ? rbv : from_up;
                 float dgv = up_prev, upv = up;
 #pragma unroll
                 for (int r = 0; r < RR; ++r) {
@@ -126,16 +130,29 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
                 }
                 up_prev = up;
                 bot = Dl[RR - 1];
-                if (lane == 31 && j >= 0 && j < L) {
+                const bool jin = !CHECK || (j >= 0 && j < L);
+                if (lane == 31 && jin) {
                     rb[1 + j] = bot;
                     rowmin = fminf(rowmin, bot);
                 }
-                if (last && j == L - 1 && rstar >= 0 && rstar < RR) {
+                if (CHECK && last && j == L - 1 && rstar >= 0 && rstar < RR) {
 #pragma unroll
                     for (int r = 0; r < RR; ++r)
                         if (r == rstar) res = Dl[r];
                 }
+            };
+            // steady phase: every lane's column in [0, L-1) <=> 31 <= s < L-1 (no lane reaches
+            // the last column, where the result is captured); the rest is range-checked
+            const bool has_steady = L >= 33;
+            const int s_lo = has_steady ? 31 : nsteps, s_hi = has_steady ? L - 1 : nsteps;
+            for (int s = 0; s < s_lo; ++s) step(s, std::true_type{});
+            int s = s_lo;
+            for (; s + 1 < s_hi; s += 2) {
+                step(s, std::false_type{});
+                step(s + 1, std::false_type{});
             }
+            for (; s < s_hi; ++s) step(s, std::false_type{});
+            for (s = s_hi; s < nsteps; ++s) step(s, std::true_type{});
             __syncwarp();
             // column -1 of the next strip's row above is +inf (only row -1 has the 0 corner)
             if (lane == 0) rb[0] = kInf;
@@ -249,7 +266,7 @@ int launch_dtw_strip(const float *A, const float *B, const Item *items,
     p.cells_prefix = cells_prefix;
     p.cutoff = cutoff;
     p.out = out;
-    p.rowlen = (L + 2 * STRIP_PAD) + (L + 1);
+    p.rowlen = (L + 2 * STRIP_PAD) + (L + 33);
     p.rowlen = (p.rowlen + 3) / 4 * 4;
     const bool mask = w < L - 1;
     if (L >= 1024) {
