@@ -74,6 +74,30 @@ __device__ __forceinline__ unsigned long long make_key(float d, unsigned idx) {
 
 __device__ __forceinline__ float sq(float x) { return x * x; }
 
+// ---- packed fp32 pairs (sm_100 FADD2): two IEEE round-to-nearest subtractions in one
+// instruction, bit-identical to two scalar FADDs.  Operands are 64-bit register pairs
+// (lo, hi); the pack/unpack moves vanish when the halves already sit in an aligned pair.
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(unsigned long long v, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+// shared-memory load the compiler may not merge with another load of the same address (used to
+// fill two differently aligned register-pair copies of one row without register moves)
+__device__ __forceinline__ float lds_distinct(const float *p) {
+    float v;
+    asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
+}
+__device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
 // cp.async global -> shared (LDGSTS), 4 or 16 bytes, and the wait for all of a thread's copies
 __device__ __forceinline__ void cp_async4(float *dst, const float *src) {
     unsigned d = (unsigned)__cvta_generic_to_shared(dst);

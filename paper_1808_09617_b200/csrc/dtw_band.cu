@@ -56,7 +56,7 @@ __device__ __forceinline__ float pin_reg(float v) {
 // 1 = aligned, G*R = 2w+2 (kill slot is the top lane's last register: one scale register,
 // edge masks); 2 = aligned and gpw*G = 32 (every lane used: rotating shuffles deliver the
 // neighbouring group's kill slot, so no edge masks are needed at all).
-template <int R, int KM>
+template <int R, int KM, bool PACK>
 __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
     constexpr bool ALIGNED = KM >= 1;
     constexpr bool NOMASK = KM == 2;
@@ -174,34 +174,81 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
                          p.padl + J0 >= 0 && p.padl + J0 + R - 1 < p.seglen,
                      "band smem oob: g=%d per=%d I0=%d J0=%d padl=%d seglen=%d", g, per, I0,
                      J0, p.padl, p.seglen);
-        float aw[R - 1], bw[R];
+        float aw[R - 1];
 #pragma unroll
         for (int x = 0; x < R - 1; ++x) aw[x] = pa[x];
+        if (ALIGNED && PACK) {
+            // Half-packed cells: on an even diagonal t, cell m reads (a[t/2-m+H-1], b[t/2+m]);
+            // on t+1 the same slot index m reads the same a and b one further.  One FADD2 with
+            // a broadcast operand gives both differences: (a, a) - (b[y], b[y+1]).  The b pairs
+            // come in two register copies -- pairs starting at even y (be) and at odd y (bo) --
+            // loaded separately so that every pair is an aligned 64-bit register pair.
+            unsigned long long be[H], bo[H > 1 ? H - 1 : 1];
 #pragma unroll
-        for (int y = 0; y < R; ++y) bw[y] = pb[y];
+            for (int k = 0; k < H; ++k) be[k] = f2_pack(pb[2 * k], pb[2 * k + 1]);
 #pragma unroll
-        for (int t = 0; t < R; ++t) {
-            const int phi = t & 1;
-            float nlo = 0.0f, nhi = 0.0f;
-            if (NOMASK) {
-                if (phi == 0) nlo = __shfl_sync(0xffffffffu, D[R - 1], (lane + 31) & 31);
-                else nhi = __shfl_sync(0xffffffffu, D[0], (lane + 1) & 31);
-            } else {
+            for (int k = 0; k < H - 1; ++k)
+                bo[k] = f2_pack(lds_distinct(pb + 2 * k + 1), lds_distinct(pb + 2 * k + 2));
+#pragma unroll
+            for (int t = 0; t < R; t += 2) {
+                unsigned long long T[H];
+#pragma unroll
+                for (int m = 0; m < H; ++m) {
+                    const float a = aw[(t >> 1) - m + H - 1];
+                    const int y = (t >> 1) + m;
+                    T[m] = f2_sub(f2_pack(a, a), (y & 1) ? bo[y >> 1] : be[y >> 1]);
+                }
+                {  // diagonal t (even offsets r = 2m)
+                    float nlo;
+                    if (NOMASK) nlo = __shfl_sync(0xffffffffu, D[R - 1], (lane + 31) & 31);
+                    else nlo = __shfl_up_sync(0xffffffffu, D[R - 1], 1) + nbmask_lo;
+#pragma unroll
+                    for (int m = 0; m < H; ++m) {
+                        const int r = 2 * m;
+                        float t0, t1;
+                        f2_unpack(T[m], t0, t1);
+                        const float lo = (r == 0) ? nlo : D[r - 1];
+                        D[r] = fmaf(t0, t0, fminf(fminf(D[r], lo), D[r + 1]));
+                    }
+                }
+                {  // diagonal t+1 (odd offsets r = 2m+1); r = R-1 carries the kill scale
+                    float nhi;
+                    if (NOMASK) nhi = __shfl_sync(0xffffffffu, D[0], (lane + 1) & 31);
+                    else nhi = __shfl_down_sync(0xffffffffu, D[0], 1) + nbmask_hi;
+#pragma unroll
+                    for (int m = 0; m < H; ++m) {
+                        const int r = 2 * m + 1;
+                        float t0, t1;
+                        f2_unpack(T[m], t0, t1);
+                        const float hi = (r == R - 1) ? nhi : D[r + 1];
+                        const float v = fmaf(t1, t1, fminf(fminf(D[r], D[r - 1]), hi));
+                        D[r] = (r == R - 1) ? v * sc[0] : v;
+                    }
+                }
+            }
+        } else {
+            float bw[R];
+#pragma unroll
+            for (int y = 0; y < R; ++y) bw[y] = pb[y];
+#pragma unroll
+            for (int t = 0; t < R; ++t) {
+                const int phi = t & 1;
+                float nlo = 0.0f, nhi = 0.0f;
                 if (phi == 0) nlo = __shfl_up_sync(0xffffffffu, D[R - 1], 1) + nbmask_lo;
                 else nhi = __shfl_down_sync(0xffffffffu, D[0], 1) + nbmask_hi;
-            }
 #pragma unroll
-            for (int m = 0; m < H; ++m) {
-                const int r = phi + 2 * m;
-                const float a = aw[(t >> 1) - m + H - 1];
-                const float b = bw[((t + 1) >> 1) + m];
-                float s;
-                if (ALIGNED) s = (r == R - 1) ? sc[0] : 1.0f;
-                else s = sc[r];
-                const float tt = (ALIGNED && r != R - 1) ? (a - b) : fmaf(a, s, -b);
-                const float lo = (r == 0) ? nlo : D[r - 1];
-                const float hi = (r == R - 1) ? nhi : D[r + 1];
-                D[r] = fmaf(tt, tt, fminf(fminf(D[r], lo), hi));
+                for (int m = 0; m < H; ++m) {
+                    const int r = phi + 2 * m;
+                    const float a = aw[(t >> 1) - m + H - 1];
+                    const float b = bw[((t + 1) >> 1) + m];
+                    float sr;
+                    if (ALIGNED) sr = (r == R - 1) ? sc[0] : 1.0f;
+                    else sr = sc[r];
+                    const float tt = (ALIGNED && r != R - 1) ? (a - b) : fmaf(a, sr, -b);
+                    const float lo = (r == 0) ? nlo : D[r - 1];
+                    const float hi = (r == R - 1) ? nhi : D[r + 1];
+                    D[r] = fmaf(tt, tt, fminf(fminf(D[r], lo), hi));
+                }
             }
         }
         per = active ? per + 1 : 0;  // idle groups replay period 0 (stay in bounds)
@@ -282,6 +329,8 @@ __global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
 struct BandChoice {
     int R, G, gpw, warps;   // warps per CTA
     int km;                 // kill mode (see k_dtw_band)
+    int ctas;               // resident CTAs per SM (model)
+    bool pack;              // half-packed FADD2 cells (aligned layouts only)
     int k0, nper, padl, seglen;
 };
 
@@ -320,7 +369,10 @@ static BandChoice choose_band(int w, int L) {
     BandChoice best{};
     best.R = 0;
     double bt = 0;
+    static const char *force = getenv("NNDTW_BAND_R");  // experiments: force the slot width
+    const int rforce = force ? atoi(force) : 0;
     for (int R = 2; R <= 32; R += 2) {
+        if (rforce && R != rforce) continue;
         int G = (2 * w + 2 + R - 1) / R;
         if (G > 32) continue;
         bool aligned = (G * R == 2 * w + 2);
@@ -341,6 +393,7 @@ static BandChoice choose_band(int w, int L) {
         const int ctas_regs = 65536 / (regs * 32 * warps);
         int ctas = ctas_smem < ctas_regs ? ctas_smem : ctas_regs;
         if (ctas < 1) continue;
+        c.ctas = ctas;
         int wsm = ctas * warps;
         if (wsm > 48) wsm = 48;
         const double wps = wsm / 4.0;
@@ -360,9 +413,9 @@ static BandChoice choose_band(int w, int L) {
 
 bool band_supported(int w, int L) { return choose_band(w, L).R != 0; }
 
-template <int R, int KM>
+template <int R, int KM, bool PACK>
 static int launch_band_t(BandParams &p, const BandChoice &c, cudaStream_t st, int num_sms) {
-    auto kern = k_dtw_band<R, KM>;
+    auto kern = k_dtw_band<R, KM, PACK>;
     const int block = 32 * c.warps;
     size_t smem = (size_t)c.warps * p.gpw * 2 * p.seglen * sizeof(float);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -380,19 +433,31 @@ static int launch_band_t(BandParams &p, const BandChoice &c, cudaStream_t st, in
     return 0;
 }
 
-#define BAND_CASE(RR)                                                         \
-    case RR:                                                                  \
-        return c.km == 2   ? launch_band_t<RR, 2>(p, c, st, num_sms)          \
-               : c.km == 1 ? launch_band_t<RR, 1>(p, c, st, num_sms)          \
-                           : launch_band_t<RR, 0>(p, c, st, num_sms);
+#define BAND_CASE(RR)                                                                   \
+    case RR:                                                                            \
+        return c.km == 2   ? (c.pack ? launch_band_t<RR, 2, true>(p, c, st, num_sms)    \
+                                     : launch_band_t<RR, 2, false>(p, c, st, num_sms))  \
+               : c.km == 1 ? (c.pack ? launch_band_t<RR, 1, true>(p, c, st, num_sms)    \
+                                     : launch_band_t<RR, 1, false>(p, c, st, num_sms))  \
+                           : launch_band_t<RR, 0, false>(p, c, st, num_sms);
 
 int launch_dtw_band(BandParams p, cudaStream_t st, int num_sms) {
     BandChoice c = choose_band(p.w, p.L);
     if (c.R == 0) return -1;
+    {
+        // Half-packed cells (measured, tools/band_sweep.sh): +7% at R=26, G=8 (config 2), but
+        // the packed kernel needs ~178 registers, so it loses wherever the unpacked one would
+        // run more than 8 warps per SM or the group is narrow.  Used for full-warp aligned
+        // layouts with wide slots whose shared memory already caps the SM at 8 warps.
+        static const char *pk = getenv("NNDTW_PACK");
+        const bool rule = c.km == 2 && c.G >= 4 && c.R >= 24 && c.warps * c.ctas <= 8;
+        c.pack = c.km >= 1 && (pk ? pk[0] == '1' : rule);
+    }
     static const bool verbose = getenv("NNDTW_VERBOSE") != nullptr;
     if (verbose)
-        fprintf(stderr, "nndtw band: L=%d w=%d -> R=%d G=%d gpw=%d km=%d warps/cta=%d seglen=%d\n",
-                p.L, p.w, c.R, c.G, c.gpw, c.km, c.warps, c.seglen);
+        fprintf(stderr,
+                "nndtw band: L=%d w=%d -> R=%d G=%d gpw=%d km=%d pack=%d warps/cta=%d seglen=%d\n",
+                p.L, p.w, c.R, c.G, c.gpw, c.km, (int)c.pack, c.warps, c.seglen);
     p.G = c.G;
     p.gpw = c.gpw;
     p.k0 = c.k0;

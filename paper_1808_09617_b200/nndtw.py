@@ -16,8 +16,8 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnndtw_debug.so" if os.environ.get("NNDTW_DEBUG") == "1"
-                        else "libnndtw.so")
+LIB_PATH = os.environ.get("NNDTW_LIB") or os.path.join(
+    _HERE, "libnndtw_debug.so" if os.environ.get("NNDTW_DEBUG") == "1" else "libnndtw.so")
 
 NNDTW_LB_WITH_KIM = 1
 NNDTW_LB_KEOGH = 2
