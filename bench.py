@@ -45,15 +45,29 @@ def peaks():
 
 
 def dtw_cell_peak_gcups(num_sms: int, sm_mhz: float) -> float:
-    """ALU-issue roof of the DTW recurrence: each SM issues 4 warp
-    instructions per clock = 128 thread-instructions; one DP cell needs at least 3 (FADD or
-    FFMA for a-b, FMNMX3 for the 3-way min, FFMA for (a-b)^2 + min)."""
-    return num_sms * 128.0 * sm_mhz * 1e6 / 3.0 / 1e9
+    """Pipe roof of the DTW recurrence: every DP cell needs one 3-way min.
+    FMNMX3 issues at half rate (tools/pipebench.cu on B200: 0.495 warp-instr/clk/SMSP, i.e.
+    16 lanes/clk), and the arithmetic (a-b, then (a-b)^2 + min) costs the FMA pipe the same 2
+    cycles per 32 cells; so each SM retires at most 4 x 16 = 64 cells per clock."""
+    return num_sms * 64.0 * sm_mhz * 1e6 / 1e9
 
 
 def lb_pair_col_peak(num_sms: int, sm_mhz: float) -> float:
-    """ALU-issue roof of the LB bridge: 4 thread-instructions per (pair, column)."""
-    return num_sms * 128.0 * sm_mhz * 1e6 / 4.0 / 1e9
+    """Pipe roof of the LB_Keogh bridge: per (pair, column) two subtractions and
+    one FFMA on the FMA pipe (32 lanes/clk/SMSP; packed FADD2 issues at half rate, so packing
+    saves issue slots, not pipe cycles) -> 4 x 32 / 3 = 42.7 pair-columns per SM per clock."""
+    return num_sms * 128.0 / 3.0 * sm_mhz * 1e6 / 1e9
+
+
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of each hot kernel, from the
+    committed `ncu --set full` capture of this command (profiles/ncu_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {}
 
 
 class ClockSampler:
@@ -238,8 +252,17 @@ def main():
     acc = {"ms_lb": 0.0, "ms_dtw": 0.0, "cells": 0, "lb_pairs": 0, "dtw_calls": 0,
            "survivors": 0, "near_tie_pairs": 0, "dtw_abandoned": 0}
 
+    env_ev = []
+    acc_env = [0.0]
+
     def step(stats):
+        if stats:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record(stream)
         model = nndtw.Model(train_d, labels_d[lo:hi], w, V, index_base=lo, check=False)
+        if stats:
+            ev[1].record(stream)
+            env_ev.append(ev)
         if world == 1:
             pred = nndtw.classify(model, test_d, stats=stats, check=False)
         else:
@@ -270,6 +293,8 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize(dev)
     launches = nndtw.launch_count() - l0
+    acc_env_ms = sum(a.elapsed_time(b) for a, b in env_ev)
+    env_bytes = (hi - lo) * L * 12.0  # read x, write U and L (S1 algorithmic bytes)
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
@@ -346,18 +371,32 @@ def main():
                if acc_tot["ms_lb"] > 0 else 0.0)
     lb_peak = lb_pair_col_peak(num_sms, sm_mhz)
     dominant = "dtw" if acc_tot["ms_dtw"] >= acc_tot["ms_lb"] else "lb"
+    traffic = ncu_traffic()
     roof_dtw = {"kernel": "k_dtw_band (S4 survivor round)", "bound": "alu",
                 "achieved": dtw_gcups, "peak": peak_cells, "unit": "Gcells/s",
-                "frac": dtw_gcups / peak_cells if peak_cells else None, "traffic": None,
-                "peak_source": f"{num_sms} SMs x 128 lanes x {sm_mhz:.0f} MHz ({src}) / 3 "
-                               "instr per cell",
+                "frac": dtw_gcups / peak_cells if peak_cells else None,
+                "traffic": traffic.get("k_dtw_band", {}).get("bytes_per_launch"),
+                "peak_source": f"{num_sms} SMs x 64 cells/clk (FMNMX3 at 16 lanes/clk/SMSP, "
+                               f"tools/pipebench.cu) x {sm_mhz:.0f} MHz ({src})",
                 "ms_per_step": acc_tot["ms_dtw"] / args.steps}
+    lb_bytes = (Q * L + (hi - lo) * (2 * L + 2 * min(L // 2, V)) + Q * (hi - lo)) * 4.0
     roof_lb = {"kernel": "k_lb_tile (S2 cascade)", "bound": "alu", "achieved": lb_rate,
                "peak": lb_peak, "unit": "G pair-columns/s",
-               "frac": lb_rate / lb_peak if lb_peak else None, "traffic": None,
-               "peak_source": f"{num_sms} SMs x 128 lanes x {sm_mhz:.0f} MHz ({src}) / 4 "
-                              "instr per pair-column",
+               "frac": lb_rate / lb_peak if lb_peak else None,
+               "traffic": traffic.get("k_lb_tile", {}).get("bytes_per_launch"),
+               "hbm_gbs": (lb_bytes / (acc_tot["ms_lb"] / args.steps * 1e-3) / 1e9
+                           if acc_tot["ms_lb"] > 0 else None),
+               "peak_source": f"{num_sms} SMs x 42.7 pair-cols/clk (3 FMA-pipe ops each) x "
+                              f"{sm_mhz:.0f} MHz ({src})",
                "ms_per_step": acc_tot["ms_lb"] / args.steps}
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    env_gbs = env_bytes / (acc_env_ms / args.steps * 1e-3) / 1e9 if acc_env_ms > 0 else None
+    roof_env = {"kernel": "k_envelopes (S1)", "bound": "hbm", "achieved": env_gbs, "peak": hbm,
+                "unit": "GB/s", "frac": env_gbs / hbm if env_gbs else None,
+                "traffic": traffic.get("k_envelopes", {}).get("bytes_per_launch"),
+                "algorithmic_bytes": env_bytes,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
+                "ms_per_step": acc_env_ms / args.steps}
     line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -365,6 +404,7 @@ def main():
             args.config, "config": config_json(cfg, w, V, world),
             "roofline": roof_dtw if dominant == "dtw" else roof_lb,
             "roofline_other": roof_lb if dominant == "dtw" else roof_dtw,
+            "roofline_envelopes": roof_env,
             "dtw_gcups": dtw_gcups,
             "effective_gcups": Q * N * (L * (2 * w + 1) - w * (w + 1)) /
             (ms / args.steps * 1e-3) / 1e9,

@@ -110,6 +110,13 @@ __device__ __forceinline__ void cp_async16(float *dst, const float *src) {
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+// all but the most recently committed group of this thread's copies have landed
+__device__ __forceinline__ void cp_async_wait_group1() {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
 
 // ---- work items ---------------------------------------------------------------------------
 // A DTW work item: query (row of A) and train (row of B), local indices.

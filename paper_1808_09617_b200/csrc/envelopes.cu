@@ -1,250 +1,216 @@
 // envelopes.cu -- S1: upper/lower warping envelopes (Eq. 3-4) and LB_Kim features.
 //
-// Design: O(1) work per element independent of w, HBM-bound.  The clipped
-// window [i-w, i+w] has length k = 2w+1 in "padded" coordinates; cutting the padded axis into
-// segments of length k aligned at position -w (seg(p) = (p+w)/k), every window is the union of
-// a suffix of one segment and a prefix of the next (van Herk / Gil-Werman).  Each thread owns
-// E consecutive elements in registers; the segmented prefix (g) and suffix (h) max/min are
-// computed with a register scan + warp-shuffle segmented scan + cross-warp carry, staged in
-// shared memory, and combined as
-//   U_i = max(h[max(i-w,0)], seg(i+w) == seg(min(i+w,L-1)) ? g[min(i+w,L-1)] : -inf).
-// One "series group" of TPS = 32*ceil(L/(32E)) threads handles one series; several groups
-// share a CTA when L is short.
+// Design: O(1) work per element independent of w, so the kernel is HBM-bound
+// (12 B per element: read x, write U and L).  Van Herk / Gil-Werman: in padded coordinates the
+// clipped window [i-w, i+w] has length k = 2w+1; cutting the axis into segments of length k
+// aligned at padded position 0 (position p starts a segment iff (p+w) mod k == 0), every
+// window is a suffix of one segment plus a prefix of the next, so
+//   U_i = max(h[max(i-w,0)], (i+w <= L-1 || i < T) ? g[min(i+w,L-1)] : -inf),
+// g = prefix max within the segment, h = suffix max, T = (seg(L-1)+1)*k - 2w (the window's
+// right part lies in the same segment as L-1).  Likewise L_i with min.
+//
+// A group of TPS = 32*ceil(L/(32E)) threads owns one series; thread t holds the E contiguous
+// elements [tE, tE+E) in registers (float4 loads).  Segment starts inside a chunk are a bit
+// mask computed once per thread (one modulo per thread, none per element); the in-register
+// prefix/suffix runs are completed across threads by one segmented warp scan per direction
+// (shuffles) plus a carry over the group's warps.  g and h go to shared memory for the
+// windowed gather; U and L leave as float4 stores.  The Kim features (min/max and their
+// lowest indices) come from the same registers.
+#include <cstdlib>
+
 #include "launchers.cuh"
 
 namespace nndtw {
 
-template <int E>
-struct EnvCfg {
-    static constexpr int kBlock = 256;
-};
-
-struct MaxMin {
+struct Seg {  // running segmented value: (max, min) and "a segment boundary was crossed"
     float mx, mn;
+    int f;
 };
 
-__device__ __forceinline__ MaxMin mm_op(MaxMin a, MaxMin b) {
-    return {fmaxf(a.mx, b.mx), fminf(a.mn, b.mn)};
+__device__ __forceinline__ Seg seg_shfl_up(Seg v, int off) {
+    return {__shfl_up_sync(0xffffffffu, v.mx, off), __shfl_up_sync(0xffffffffu, v.mn, off),
+            __shfl_up_sync(0xffffffffu, v.f, off)};
 }
-
-// Segmented inclusive scan over the TPS threads of a series group, forward (DIR=+1, thread t
-// combines with t-1, t-2, ...) or backward (DIR=-1).  `pass` = this element does not start a
-// segment (so it absorbs the running value of its predecessor in scan order).
-template <int DIR>
-__device__ __forceinline__ MaxMin seg_scan(MaxMin v, bool pass, int lane, int wig, int nwarps,
-                                           MaxMin *s_val, int *s_pass) {
-    // warp level: predecessor in scan order is lane-1 (forward) or lane+1 (backward)
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        float pmx, pmn;
-        int ppass;
-        if (DIR > 0) {
-            pmx = __shfl_up_sync(0xffffffffu, v.mx, off);
-            pmn = __shfl_up_sync(0xffffffffu, v.mn, off);
-            ppass = __shfl_up_sync(0xffffffffu, (int)pass, off);
-        } else {
-            pmx = __shfl_down_sync(0xffffffffu, v.mx, off);
-            pmn = __shfl_down_sync(0xffffffffu, v.mn, off);
-            ppass = __shfl_down_sync(0xffffffffu, (int)pass, off);
-        }
-        bool valid = DIR > 0 ? (lane >= off) : (lane + off < 32);
-        if (valid) {
-            if (pass) v = mm_op(v, {pmx, pmn});
-            pass = pass && ppass;
-        }
-    }
-    if (nwarps > 1) {
-        // warp totals (last element in scan order) -> smem, sequential combine by one thread
-        int last_lane = DIR > 0 ? 31 : 0;
-        if (lane == last_lane) {
-            s_val[wig] = v;
-            s_pass[wig] = pass;
-        }
-        __syncthreads();
-        if (lane == 0 && wig == 0) {
-            // exclusive prefix over warps in scan order, stored back in place
-            MaxMin run = {-kInf, kInf};
-            bool have = false;
-            for (int s = 0; s < nwarps; ++s) {
-                int wi = DIR > 0 ? s : nwarps - 1 - s;
-                MaxMin tot = s_val[wi];
-                int tp = s_pass[wi];
-                s_val[wi] = run;          // carry INTO warp wi
-                s_pass[wi] = have;
-                // running value after warp wi: if wi is all-pass, combine with previous
-                if (tp && have) run = mm_op(run, tot);
-                else run = tot;
-                have = true;
-            }
-        }
-        __syncthreads();
-        MaxMin carry = s_val[wig];
-        bool has = s_pass[wig];
-        // elements of this warp that are still "passing" at the warp start absorb the carry
-        if (has && pass) v = mm_op(v, carry);
-        __syncthreads();
-    }
-    return v;
+__device__ __forceinline__ Seg seg_shfl_down(Seg v, int off) {
+    return {__shfl_down_sync(0xffffffffu, v.mx, off), __shfl_down_sync(0xffffffffu, v.mn, off),
+            __shfl_down_sync(0xffffffffu, v.f, off)};
+}
+// a then b in scan order: b restarts the segment if it crossed a boundary
+__device__ __forceinline__ Seg seg_cat(Seg a, Seg b) {
+    if (b.f) return b;
+    return {fmaxf(a.mx, b.mx), fminf(a.mn, b.mn), a.f};
 }
 
 template <int E>
-__global__ void __launch_bounds__(256) k_envelopes(const float *__restrict__ x, int64_t n,
-                                                   int L, int w, int tps, float *__restrict__ U,
+__global__ void __launch_bounds__(512) k_envelopes(const float *__restrict__ x, int64_t n,
+                                                   int L, int w, int tps, int vec, int T,
+                                                   float *__restrict__ U,
                                                    float *__restrict__ Lo,
                                                    nndtw_kim *__restrict__ kim) {
-    extern __shared__ float smem[];
+    extern __shared__ __align__(16) unsigned char env_smem[];
     const int groups = blockDim.x / tps;
     const int grp = threadIdx.x / tps;
-    const int t = threadIdx.x % tps;
+    const int t = threadIdx.x - grp * tps;
     const int lane = threadIdx.x & 31;
-    const int wig = t >> 5;             // warp within group
-    const int nwarps = tps >> 5;
+    const int wig = t >> 5;
+    const int nw = tps >> 5;
+    const int k = 2 * w + 1;
+    const int span = tps * E;
+    const int pspan = span + (span >> 4) + 1;  // one pad slot per 16: thread-strided access
+    auto pad = [](int q) { return q + (q >> 4); };  // is bank-conflict free
+
+    float2 *G = reinterpret_cast<float2 *>(env_smem) + (size_t)grp * 2 * pspan;
+    float2 *H = G + pspan;
+    Seg *tot = reinterpret_cast<Seg *>(reinterpret_cast<float2 *>(env_smem) +
+                                       (size_t)groups * 2 * pspan) + grp * 32;  // [0,16) fwd, [16,32) bwd
+    const int p0 = t * E;
     const int64_t s = (int64_t)blockIdx.x * groups + grp;
     const bool live = s < n;
-    const int k = 2 * w + 1;
 
-    float *gmx = smem + (size_t)grp * 4 * L;
-    float *gmn = gmx + L;
-    float *hmx = gmn + L;
-    float *hmn = hmx + L;
-    // scan scratch after the 4*L*groups floats
-    MaxMin *s_val = reinterpret_cast<MaxMin *>(smem + (size_t)groups * 4 * L) + grp * 32;
-    int *s_pass = reinterpret_cast<int *>(smem + (size_t)groups * 4 * L + groups * 64) + grp * 32;
-
+    // ---- load E contiguous elements -------------------------------------------------------
     const float *xs = x + (live ? s : 0) * (int64_t)L;
     float v[E];
-    const int p0 = t * E;
+    if (vec) {
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-        int p = p0 + e;
-        v[e] = (live && p < L) ? __ldg(xs + p) : 0.0f;
+        for (int j = 0; j < E / 4; ++j) {
+            float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (live && p0 + 4 * j < L) f = __ldg(reinterpret_cast<const float4 *>(xs + p0) + j);
+            v[4 * j] = f.x;
+            v[4 * j + 1] = f.y;
+            v[4 * j + 2] = f.z;
+            v[4 * j + 3] = f.w;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = (live && p0 + e < L) ? __ldg(xs + p0 + e) : 0.0f;
     }
-    auto seg = [&](int p) { return (p + w) / k; };
+    const int nvalid = L - p0;  // elements e < nvalid are real
 
-    // ---- forward (prefix within segment) --------------------------------------------
-    float fmx[E], fmn[E];
+    // ---- segment starts inside [p0, p0+E]: bit e set iff (p0+e+w) mod k == 0; position L
+    // also starts one (so no scan ever mixes padding into a real position) ----------------------
+    unsigned m = 0;
+    {
+        const int r0 = (p0 + w) % k;
+        for (int q = (r0 == 0) ? 0 : k - r0; q <= E; q += k) m |= 1u << q;
+        if (nvalid >= 0 && nvalid <= E) m |= 1u << nvalid;
+    }
+
+    // ---- forward: g = running max/min from the segment start ------------------------------------
+    float gx[E], gn[E];
+    gx[0] = v[0];
+    gn[0] = v[0];
+#pragma unroll
+    for (int e = 1; e < E; ++e) {
+        const bool st = (m >> e) & 1u;
+        gx[e] = st ? v[e] : fmaxf(gx[e - 1], v[e]);
+        gn[e] = st ? v[e] : fminf(gn[e - 1], v[e]);
+    }
+    // ---- backward: h = running max/min to the segment end ---------------------------------------
+    float hx[E], hn[E];
+    hx[E - 1] = v[E - 1];
+    hn[E - 1] = v[E - 1];
+#pragma unroll
+    for (int e = E - 2; e >= 0; --e) {
+        const bool en = (m >> (e + 1)) & 1u;
+        hx[e] = en ? v[e] : fmaxf(hx[e + 1], v[e]);
+        hn[e] = en ? v[e] : fminf(hn[e + 1], v[e]);
+    }
+
+    // ---- cross-thread completion: segmented scans (forward over t ascending, backward
+    // descending); a thread's aggregate restarts if its chunk contains a boundary ------------
+    const unsigned mfwd = m & ((1u << E) - 1u);   // starts at e in [0, E)
+    const unsigned mbwd = m >> 1;                 // ends at e in [0, E)
+    Seg af{gx[E - 1], gn[E - 1], mfwd != 0u};
+    Seg ab{hx[0], hn[0], mbwd != 0u};
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        Seg pf = seg_shfl_up(af, off);
+        Seg pb = seg_shfl_down(ab, off);
+        if (lane >= off) af = seg_cat(pf, af);
+        if (lane + off < 32) ab = seg_cat(pb, ab);
+    }
+    Seg cf{-kInf, kInf, 1}, cb{-kInf, kInf, 1};  // carries from earlier warps ("f=1": none)
+    if (nw > 1) {
+        if (lane == 31) tot[wig] = af;
+        if (lane == 0) tot[16 + wig] = ab;
+        __syncthreads();
+        for (int j = 0; j < wig; ++j) cf = (j == 0) ? tot[j] : seg_cat(cf, tot[j]);
+        for (int j = nw - 1; j > wig; --j) cb = (j == nw - 1) ? tot[16 + j] : seg_cat(cb, tot[16 + j]);
+        af = seg_cat(cf, af);
+        ab = seg_cat(cb, ab);
+    }
+    // exclusive carry into this thread = inclusive value of the previous thread in scan order
+    Seg inf{__shfl_up_sync(0xffffffffu, af.mx, 1), __shfl_up_sync(0xffffffffu, af.mn, 1), 0};
+    Seg inb{__shfl_down_sync(0xffffffffu, ab.mx, 1), __shfl_down_sync(0xffffffffu, ab.mn, 1), 0};
+    if (lane == 0) inf = {cf.mx, cf.mn, 0};   // identity when wig == 0
+    if (lane == 31) inb = {cb.mx, cb.mn, 0};
+    const int bf = mfwd ? __ffs(mfwd) - 1 : E;            // elements e < bf continue a segment
+    const int bb = mbwd ? 31 - __clz(mbwd) : -1;          // elements e > bb continue one
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        int p = p0 + e;
-        bool in = p < L;
-        float vx = in ? v[e] : -kInf, vn = in ? v[e] : kInf;
-        if (e > 0 && seg(p) == seg(p - 1)) {
-            fmx[e] = fmaxf(fmx[e - 1], vx);
-            fmn[e] = fminf(fmn[e - 1], vn);
-        } else {
-            fmx[e] = vx;
-            fmn[e] = vn;
+        if (e < bf) {
+            gx[e] = fmaxf(gx[e], inf.mx);
+            gn[e] = fminf(gn[e], inf.mn);
         }
-    }
-    {
-        bool pass = (t > 0) && seg(p0 - 1) == seg(p0 + E - 1);
-        MaxMin agg = seg_scan<1>({fmx[E - 1], fmn[E - 1]}, pass, lane, wig, nwarps, s_val,
-                                 s_pass);
-        // carry = inclusive result of thread t-1
-        float cmx = __shfl_up_sync(0xffffffffu, agg.mx, 1);
-        float cmn = __shfl_up_sync(0xffffffffu, agg.mn, 1);
-        if (nwarps > 1) {
-            // lane 0 needs the last lane of the previous warp
-            if (lane == 31) {
-                s_val[wig] = agg;
-            }
-            __syncthreads();
-            if (lane == 0 && wig > 0) {
-                cmx = s_val[wig - 1].mx;
-                cmn = s_val[wig - 1].mn;
-            }
-            __syncthreads();
-        }
-        bool carry_in = (t > 0) && seg(p0 - 1) == seg(p0);
-        if (carry_in) {
-            int s0 = seg(p0);
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                if (seg(p0 + e) == s0) {
-                    fmx[e] = fmaxf(fmx[e], cmx);
-                    fmn[e] = fminf(fmn[e], cmn);
-                }
-            }
-        }
-    }
-    // ---- backward (suffix within segment) -------------------------------------------
-    float bmx[E], bmn[E];
-#pragma unroll
-    for (int e = E - 1; e >= 0; --e) {
-        int p = p0 + e;
-        bool in = p < L;
-        float vx = in ? v[e] : -kInf, vn = in ? v[e] : kInf;
-        if (e < E - 1 && seg(p) == seg(p + 1)) {
-            bmx[e] = fmaxf(bmx[e + 1], vx);
-            bmn[e] = fminf(bmn[e + 1], vn);
-        } else {
-            bmx[e] = vx;
-            bmn[e] = vn;
-        }
-    }
-    {
-        bool pass = (t < tps - 1) && seg(p0) == seg(p0 + E);
-        MaxMin agg = seg_scan<-1>({bmx[0], bmn[0]}, pass, lane, wig, nwarps, s_val, s_pass);
-        float cmx = __shfl_down_sync(0xffffffffu, agg.mx, 1);
-        float cmn = __shfl_down_sync(0xffffffffu, agg.mn, 1);
-        if (nwarps > 1) {
-            if (lane == 0) s_val[wig] = agg;
-            __syncthreads();
-            if (lane == 31 && wig < nwarps - 1) {
-                cmx = s_val[wig + 1].mx;
-                cmn = s_val[wig + 1].mn;
-            }
-            __syncthreads();
-        }
-        bool carry_in = (t < tps - 1) && seg(p0 + E - 1) == seg(p0 + E);
-        if (carry_in) {
-            int s1 = seg(p0 + E - 1);
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                if (seg(p0 + e) == s1) {
-                    bmx[e] = fmaxf(bmx[e], cmx);
-                    bmn[e] = fminf(bmn[e], cmn);
-                }
-            }
+        if (e > bb) {
+            hx[e] = fmaxf(hx[e], inb.mx);
+            hn[e] = fminf(hn[e], inb.mn);
         }
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        int p = p0 + e;
-        if (p < L) {
-            gmx[p] = fmx[e];
-            gmn[p] = fmn[e];
-            hmx[p] = bmx[e];
-            hmn[p] = bmn[e];
-        }
+        G[pad(p0 + e)] = make_float2(gx[e], gn[e]);
+        H[pad(p0 + e)] = make_float2(hx[e], hn[e]);
     }
     __syncthreads();
+
+    // ---- gather the window extremes for this thread's own elements ------------------------------
+    // U_p = max(h[max(p-w,0)], g[min(p+w,L-1)] if p < Tg), Tg = max(L-w, T)
+    const int Tg = (L - w > T) ? L - w : T;
+    float ux[E], ln[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int p = p0 + e;
+        const int lo = max(p - w, 0);
+        const int hc = min(p + w, L - 1);
+        const float2 hv = H[pad(lo)];
+        const float2 gv = G[pad(hc)];
+        const bool useg = p < Tg;
+        ux[e] = useg ? fmaxf(hv.x, gv.x) : hv.x;
+        ln[e] = useg ? fminf(hv.y, gv.y) : hv.y;
+    }
     if (live) {
         float *Us = U + s * (int64_t)L;
         float *Ls = Lo + s * (int64_t)L;
-        for (int i = t; i < L; i += tps) {
-            int lo = i - w < 0 ? 0 : i - w;
-            int hi = i + w;
-            int hc = hi < L - 1 ? hi : L - 1;
-            float u = hmx[lo], l = hmn[lo];
-            if (seg(hi) == seg(hc)) {
-                u = fmaxf(u, gmx[hc]);
-                l = fminf(l, gmn[hc]);
+        if (vec) {
+#pragma unroll
+            for (int j = 0; j < E / 4; ++j) {
+                if (p0 + 4 * j < L) {
+                    reinterpret_cast<float4 *>(Us + p0)[j] =
+                        make_float4(ux[4 * j], ux[4 * j + 1], ux[4 * j + 2], ux[4 * j + 3]);
+                    reinterpret_cast<float4 *>(Ls + p0)[j] =
+                        make_float4(ln[4 * j], ln[4 * j + 1], ln[4 * j + 2], ln[4 * j + 3]);
+                }
             }
-            Us[i] = u;
-            Ls[i] = l;
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                if (e < nvalid) {
+                    Us[p0 + e] = ux[e];
+                    Ls[p0 + e] = ln[e];
+                }
         }
     }
+
+    // ---- LB_Kim features: min / max and their lowest indices (reading C7) ----------------------
     if (kim != nullptr) {
-        // LB_Kim features: min/max with the lowest index on ties (reading C7)
         float mn = kInf, mx = -kInf;
         int imn = 0x7fffffff, imx = 0x7fffffff;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            int p = p0 + e;
-            if (p < L) {
-                if (v[e] < mn) { mn = v[e]; imn = p; }
-                if (v[e] > mx) { mx = v[e]; imx = p; }
+            if (e < nvalid) {
+                if (v[e] < mn) { mn = v[e]; imn = p0 + e; }
+                if (v[e] > mx) { mx = v[e]; imx = p0 + e; }
             }
         }
 #pragma unroll
@@ -256,22 +222,22 @@ __global__ void __launch_bounds__(256) k_envelopes(const float *__restrict__ x, 
             if (omn < mn || (omn == mn && oimn < imn)) { mn = omn; imn = oimn; }
             if (omx > mx || (omx == mx && oimx < imx)) { mx = omx; imx = oimx; }
         }
-        __syncthreads();
-        float *red = gmx;  // reuse (envelope outputs already written)
-        if (lane == 0) {
-            red[wig * 4 + 0] = mn;
-            red[wig * 4 + 1] = __int_as_float(imn);
-            red[wig * 4 + 2] = mx;
-            red[wig * 4 + 3] = __int_as_float(imx);
-        }
-        __syncthreads();
-        if (t == 0 && live) {
-            for (int q = 1; q < nwarps; ++q) {
-                float omn = red[q * 4 + 0], omx = red[q * 4 + 2];
-                int oimn = __float_as_int(red[q * 4 + 1]), oimx = __float_as_int(red[q * 4 + 3]);
-                if (omn < mn || (omn == mn && oimn < imn)) { mn = omn; imn = oimn; }
-                if (omx > mx || (omx == mx && oimx < imx)) { mx = omx; imx = oimx; }
+        if (nw > 1) {
+            __syncthreads();  // tot[] reuse
+            float4 *red = reinterpret_cast<float4 *>(tot);
+            if (lane == 0) red[wig] = make_float4(mn, __int_as_float(imn), mx, __int_as_float(imx));
+            __syncthreads();
+            if (t == 0) {
+                for (int q = 1; q < nw; ++q) {
+                    float4 r = red[q];
+                    float omn = r.x, omx = r.z;
+                    int oimn = __float_as_int(r.y), oimx = __float_as_int(r.w);
+                    if (omn < mn || (omn == mn && oimn < imn)) { mn = omn; imn = oimn; }
+                    if (omx > mx || (omx == mx && oimx < imx)) { mx = omx; imx = oimx; }
+                }
             }
+        }
+        if (t == 0 && live) {
             nndtw_kim r;
             r.vmin = mn;
             r.vmax = mx;
@@ -320,18 +286,33 @@ int launch_envelopes(const float *x, int64_t n, int L, int w, float *U, float *L
                      nndtw_kim *kim, cudaStream_t st) {
     if (n == 0) return 0;
     if (w > L - 1) w = L - 1;
-    const int E = 8;
-    int tps = ((L + E - 1) / E + 31) / 32 * 32;
-    int block = tps >= 256 ? tps : 256 / tps * tps;
-    int groups = block / tps;
-    size_t smem = (size_t)groups * 4 * L * sizeof(float) + (size_t)groups * 64 * sizeof(float) +
-                  (size_t)groups * 32 * sizeof(int);
-    if (block > 1024 || smem > 200 * 1024) return -1;
-    int64_t grid = (n + groups - 1) / groups;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_envelopes<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    k_envelopes<8><<<(unsigned)grid, block, smem, st>>>(x, n, L, w, tps, U, Lo, kim);
+    static const char *ef = getenv("NNDTW_ENV_E");  // experiments: force elements per thread
+    int E = L <= 128 ? 4 : (L <= 256 ? 8 : 16);
+    if (ef) E = atoi(ef);
+    const int tps = (L + 32 * E - 1) / (32 * E) * 32;
+    if (tps > 512) return -1;  // L > 8192
+    const int block = tps >= 256 ? tps : 256;
+    const int groups = block / tps;
+    const int span = tps * E;
+    const int pspan = span + (span >> 4) + 1;
+    const size_t smem = (size_t)groups * 2 * pspan * sizeof(float2) + (size_t)groups * 32 * 16;
+    const int k = 2 * w + 1;
+    const int T = ((L - 1 + w) / k + 1) * k - 2 * w;
+    const int vec = (L % 4 == 0 && ((uintptr_t)x % 16) == 0 && ((uintptr_t)U % 16) == 0 &&
+                     ((uintptr_t)Lo % 16) == 0) ? 1 : 0;
+    const int64_t grid = (n + groups - 1) / groups;
+    if (grid > 0x7fffffffll) return -1;
+#define ENV_LAUNCH(EE)                                                                            \
+    do {                                                                                          \
+        if (smem > 48 * 1024)                                                                     \
+            cudaFuncSetAttribute(k_envelopes<EE>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                 (int)smem);                                                      \
+        k_envelopes<EE><<<(unsigned)grid, block, smem, st>>>(x, n, L, w, tps, vec, T, U, Lo, kim); \
+    } while (0)
+    if (E == 4) ENV_LAUNCH(4);
+    else if (E == 8) ENV_LAUNCH(8);
+    else ENV_LAUNCH(16);
+#undef ENV_LAUNCH
     count_launch(1, __func__);
     return 0;
 }

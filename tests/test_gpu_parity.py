@@ -39,7 +39,8 @@ def assert_rel(gpu, ref, rel=REL, what=""):
 
 
 # ---------------------------------------------------------------- S1 envelopes
-@pytest.mark.parametrize("L", [2, 3, 7, 31, 128, 255, 300, 512, 1000, 2048])
+@pytest.mark.parametrize("L", [2, 3, 4, 7, 31, 128, 129, 255, 256, 300, 512, 513, 1000, 2048,
+                               4100, 8192])
 def test_envelopes_bit_exact(dev, oracle_lib, L):
     from paper_1808_09617_b200 import nndtw
     rng = np.random.default_rng(L)

@@ -74,14 +74,16 @@ __global__ void __launch_bounds__(512) k(float *out, long long *cyc, float seed)
                 asm volatile("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(px[c]) : "l"(py[c]));
             } else if (V == 10) {  // LB bridge scalar: u=a-U, l=L-a, t=max(u,l,0), acc+=t*t
                 float u, l, t;
-                asm volatile("sub.f32 %0, %1, %2;" : "=f"(u) : "f"(y[c]), "f"(z[c]));
-                asm volatile("sub.f32 %0, %1, %2;" : "=f"(l) : "f"(z[(c + 1) % NCH]), "f"(y[c]));
+                const float a = x[(c + 1) % NCH];
+                asm volatile("sub.f32 %0, %1, %2;" : "=f"(u) : "f"(a), "f"(z[c]));
+                asm volatile("sub.f32 %0, %1, %2;" : "=f"(l) : "f"(y[c]), "f"(a));
                 asm volatile("max.f32 %0, %1, %2, 0f00000000;" : "=f"(t) : "f"(u), "f"(l));
                 asm volatile("fma.rn.f32 %0, %1, %1, %0;" : "+f"(x[c]) : "f"(t));
             } else if (V == 11) {  // LB bridge packed over two pairs
                 unsigned long long u, l;
-                asm volatile("sub.rn.f32x2 %0, %1, %2;" : "=l"(u) : "l"(py[c]), "l"(pz[c]));
-                asm volatile("sub.rn.f32x2 %0, %1, %2;" : "=l"(l) : "l"(pz[(c + 1) % NCH]), "l"(py[c]));
+                const unsigned long long a2 = px[(c + 1) % NCH];
+                asm volatile("sub.rn.f32x2 %0, %1, %2;" : "=l"(u) : "l"(a2), "l"(pk(z[c], z[c])));
+                asm volatile("sub.rn.f32x2 %0, %1, %2;" : "=l"(l) : "l"(pk(y[c], y[c])), "l"(a2));
                 float u0, u1, l0, l1, t0, t1;
                 upk(u, u0, u1);
                 upk(l, l0, l1);
@@ -114,6 +116,28 @@ __global__ void __launch_bounds__(512) k(float *out, long long *cyc, float seed)
             } else if (V == 15) {  // FFMA + FMNMX3 alternating (pipe overlap test)
                 asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(y[c]), "f"(z[c]));
                 asm volatile("min.f32 %0, %0, %1, %2;" : "+f"(z[c]) : "f"(y[c]), "f"(x[(c + 1) % NCH]));
+            } else if (V == 17) {  // LB packed with scalar FFMA accumulation
+                unsigned long long u, l;
+                const unsigned long long a2 = px[(c + 1) % NCH];
+                asm volatile("sub.rn.f32x2 %0, %1, %2;" : "=l"(u) : "l"(a2), "l"(pk(z[c], z[c])));
+                asm volatile("sub.rn.f32x2 %0, %1, %2;" : "=l"(l) : "l"(pk(y[c], y[c])), "l"(a2));
+                float u0, u1, l0, l1, t0, t1, p0, p1;
+                upk(u, u0, u1);
+                upk(l, l0, l1);
+                asm volatile("max.f32 %0, %1, %2, 0f00000000;" : "=f"(t0) : "f"(u0), "f"(l0));
+                asm volatile("max.f32 %0, %1, %2, 0f00000000;" : "=f"(t1) : "f"(u1), "f"(l1));
+                upk(px[c], p0, p1);
+                asm volatile("fma.rn.f32 %0, %1, %1, %0;" : "+f"(p0) : "f"(t0));
+                asm volatile("fma.rn.f32 %0, %1, %1, %0;" : "+f"(p1) : "f"(t1));
+                px[c] = pk(p0, p1);
+            } else if (V == 18) {  // LB: u scalar FADD, l scalar FADD, FMNMX x2 (2-input), FFMA via max(t,0)*t
+                float u, l, t, r;
+                const float a = x[(c + 1) % NCH];
+                asm volatile("sub.f32 %0, %1, %2;" : "=f"(u) : "f"(a), "f"(z[c]));
+                asm volatile("sub.f32 %0, %1, %2;" : "=f"(l) : "f"(y[c]), "f"(a));
+                asm volatile("max.f32 %0, %1, %2;" : "=f"(t) : "f"(u), "f"(l));
+                asm volatile("max.f32 %0, %1, 0f00000000;" : "=f"(r) : "f"(t));
+                asm volatile("fma.rn.f32 %0, %1, %2, %0;" : "+f"(x[c]) : "f"(t), "f"(r));
             } else if (V == 16) {  // FFMA + FMNMX (2-in) alternating
                 asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(y[c]), "f"(z[c]));
                 asm volatile("min.f32 %0, %0, %1;" : "+f"(z[c]) : "f"(x[(c + 1) % NCH]));
@@ -175,6 +199,8 @@ int main() {
     run<13>("cell FADD+2FMNMX+FFMA", 4, 1, nsm, out, cyc);
     run<10>("LB scalar FADD,FADD,FMNMX3,FFMA", 4, 1, nsm, out, cyc);
     run<11>("LB packed 2FADD2,2FMNMX3,FFMA2", 5, 2, nsm, out, cyc);
+    run<17>("LB packed 2FADD2,2FMNMX3,2FFMA", 6, 2, nsm, out, cyc);
+    run<18>("LB FADD,FADD,FMNMX,FMNMX,FFMA", 5, 1, nsm, out, cyc);
     run<14>("FMNMX3 imm 0", 1, 0, nsm, out, cyc);
     run<15>("FFMA+FMNMX3", 2, 0, nsm, out, cyc);
     run<16>("FFMA+FMNMX", 2, 0, nsm, out, cyc);
