@@ -97,9 +97,38 @@ def full(path, out, jpath=None):
     print("\n".join(md))
 
 
+def traffic(path, out):
+    """profiles/ncu_traffic.json: dram read+write bytes of the longest captured launch of each
+    kernel (bench.py reads it for roofline.traffic)."""
+    raw = subprocess.run([NCU, "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h = rows[0]
+    units = dict(zip(h, rows[1]))
+    mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tmult = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3, "ns": 1e-6,
+             "us": 1e-3, "ms": 1.0, "s": 1e3}
+    best = {}
+    for r in rows[2:]:
+        d = dict(zip(h, r))
+        name = d["Kernel Name"].split("(")[0].replace("void ", "").split("<")[0]
+        name = name.split("::")[-1]
+        ms = float(d["gpu__time_duration.sum"]) * tmult[units["gpu__time_duration.sum"]]
+        b = sum(float(d[k]) * mult[units[k]] for k in ("dram__bytes_read.sum",
+                                                        "dram__bytes_write.sum"))
+        if b != b:  # metrics not collected for this launch
+            continue
+        if name not in best or ms > best[name]["ms"]:
+            best[name] = {"ms": ms, "bytes_per_launch": b, "report": path}
+    json.dump(best, open(out, "w"), indent=1)
+    print(json.dumps(best, indent=1))
+
+
 if __name__ == "__main__":
     mode = sys.argv[1]
-    if mode == "launches":
+    if mode == "traffic":
+        traffic(sys.argv[2], sys.argv[3])
+    elif mode == "launches":
         launches(sys.argv[2], sys.argv[3])
     else:
         jp = sys.argv[sys.argv.index("--json") + 1] if "--json" in sys.argv else None
