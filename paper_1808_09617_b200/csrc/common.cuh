@@ -98,6 +98,13 @@ __device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsig
     return r;
 }
 
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b,
+                                                     unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
 // cp.async global -> shared (LDGSTS), 4 or 16 bytes, and the wait for all of a thread's copies
 __device__ __forceinline__ void cp_async4(float *dst, const float *src) {
     unsigned d = (unsigned)__cvta_generic_to_shared(dst);

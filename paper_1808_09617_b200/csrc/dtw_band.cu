@@ -57,7 +57,7 @@ __device__ __forceinline__ float pin_reg(float v) {
 // edge masks); 2 = aligned and gpw*G = 32 (every lane used: rotating shuffles deliver the
 // neighbouring group's kill slot, so no edge masks are needed at all).
 template <int R, int KM, bool PACK>
-__global__ void __launch_bounds__(256) k_dtw_band(BandParams p) {
+__global__ void __launch_bounds__(352) k_dtw_band(BandParams p) {
     constexpr bool ALIGNED = KM >= 1;
     constexpr bool NOMASK = KM == 2;
     extern __shared__ __align__(16) float smem_f[];
@@ -384,9 +384,11 @@ static BandChoice choose_band(int w, int L) {
         c.km = aligned ? ((c.gpw * G == 32) ? 2 : 1) : 0;
         band_geometry(R, G, L, w, c);
         const double warp_smem = (double)c.gpw * 2 * c.seglen * sizeof(float);
-        int warps = (int)((200.0 * 1024) / warp_smem);
+        static const char *wcap_env = getenv("NNDTW_BAND_WARPS");  // experiments
+        const int wcap = wcap_env ? atoi(wcap_env) : 8;
+        int warps = (int)((226.0 * 1024) / warp_smem);
         if (warps < 1) continue;
-        if (warps > 8) warps = 8;
+        if (warps > wcap) warps = wcap;
         c.warps = warps;
         const int ctas_smem = (int)((227.0 * 1024) / (warps * warp_smem));
         const int regs = c.km >= 1 ? 48 + 2 * R : 48 + 3 * R;
