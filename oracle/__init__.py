@@ -73,6 +73,13 @@ def _load():
                                            C.c_double, C.c_double, ip]
         lib.oracle_lb_cascade.restype = C.c_double
         lib.oracle_lb_cascade.argtypes = [fp, fp, fp, fp, C.c_int, C.c_int, C.c_int]
+        lib.oracle_lb_improved.restype = C.c_double
+        lib.oracle_lb_improved.argtypes = [fp, fp, fp, fp, C.c_int, C.c_int]
+        lib.oracle_lb_new.restype = C.c_double
+        lib.oracle_lb_new.argtypes = [fp, fp, C.c_int, C.c_int]
+        lib.oracle_lb_enhanced_sym.restype = C.c_double
+        lib.oracle_lb_enhanced_sym.argtypes = [fp, fp, fp, fp, fp, fp, C.c_int, C.c_int,
+                                               C.c_int]
         lib.oracle_nn.restype = None
         lib.oracle_nn.argtypes = [fp, C.c_int64, fp, fp, fp, C.c_int64, C.c_int, C.c_int,
                                   C.c_int, C.c_int, C.c_int, i64p, dp, C.POINTER(Counts)]
@@ -165,6 +172,66 @@ def lb_cascade(a, b, U, Lo, w: int, V: int) -> float:
     return _load().oracle_lb_cascade(_ptr(a, C.c_float), _ptr(b, C.c_float),
                                      _ptr(U, C.c_float), _ptr(Lo, C.c_float), a.size, int(w),
                                      int(V))
+
+
+def lb_improved(a, b, w: int, UB=None, LB=None) -> float:
+    """LB_Improved_W(A, B); envelope of B computed here unless given."""
+    a, b = _f32(a), _f32(b)
+    if UB is None:
+        UB, LB = envelope(b, w)
+    UB, LB = _f32(UB), _f32(LB)
+    return _load().oracle_lb_improved(_ptr(a, C.c_float), _ptr(b, C.c_float),
+                                      _ptr(UB, C.c_float), _ptr(LB, C.c_float), a.size, int(w))
+
+
+def lb_new(a, b, w: int) -> float:
+    """LB_New_W(A, B) (P:284-297)."""
+    a, b = _f32(a), _f32(b)
+    return _load().oracle_lb_new(_ptr(a, C.c_float), _ptr(b, C.c_float), a.size, int(w))
+
+
+def lb_enhanced_sym(a, b, w: int, V: int) -> float:
+    """max(LB_Enhanced(A,B), LB_Enhanced(B,A)) (P:745-747)."""
+    a, b = _f32(a), _f32(b)
+    UA, LA = envelope(a, w)
+    UB, LB = envelope(b, w)
+    return _load().oracle_lb_enhanced_sym(_ptr(a, C.c_float), _ptr(b, C.c_float),
+                                          _ptr(UA, C.c_float), _ptr(LA, C.c_float),
+                                          _ptr(UB, C.c_float), _ptr(LB, C.c_float), a.size,
+                                          int(w), int(V))
+
+
+def bound_matrix(kind: str, Q, T, w: int, V: int = 5) -> np.ndarray:
+    """All-pairs bound matrix [nq][nt] (fp64) for kind in {keogh, enhanced, cascade, sym,
+    improved, new}; plain loops over the single-pair functions above (small inputs only)."""
+    Q, T = _f32(Q), _f32(T)
+    UT, LT = envelopes(T, w)
+    out = np.empty((Q.shape[0], T.shape[0]), dtype=np.float64)
+    for i, a in enumerate(Q):
+        for j, b in enumerate(T):
+            if kind == "keogh":
+                out[i, j] = lb_keogh(a, UT[j], LT[j])
+            elif kind == "enhanced":
+                out[i, j] = lb_enhanced(a, b, UT[j], LT[j], w, V)[0]
+            elif kind == "cascade":
+                out[i, j] = lb_cascade(a, b, UT[j], LT[j], w, V)
+            elif kind == "sym":
+                out[i, j] = lb_enhanced_sym(a, b, w, V)
+            elif kind == "improved":
+                out[i, j] = lb_improved(a, b, w, UT[j], LT[j])
+            elif kind == "new":
+                out[i, j] = lb_new(a, b, w)
+            else:
+                raise ValueError(kind)
+    return out
+
+
+def tightness(lb, dtw) -> tuple[float, int]:
+    """Mean tightness sqrt(LB)/sqrt(DTW^2) over pairs with DTW > 0 (reading C20)."""
+    lb = np.asarray(lb, dtype=np.float64).ravel()
+    d = np.asarray(dtw, dtype=np.float64).ravel()
+    m = d > 0
+    return float(np.mean(np.sqrt(lb[m]) / np.sqrt(d[m]))) if m.any() else 0.0, int(m.sum())
 
 
 def nn(Q, T, w: int, V: int = 5, mode: str = "exhaustive", threads: int | None = None,

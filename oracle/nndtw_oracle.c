@@ -208,6 +208,59 @@ double oracle_lb_enhanced(const float *A, const float *B, const float *U, const 
 #undef Bx
 }
 
+/* ---------------------------------------------------------------------------------------
+ * LB_Improved_W (Lemire; §2.3.3 "Improved Lower Bound"): LB_Keogh(A, env B) plus
+ * LB_Keogh(B, env A'), A' the projection of A onto the envelope of B (Eq. "projection",
+ * P:261-268).  UB/LB = envelope of B (Eq. 3-4).  The envelope of A' is the naive scan.
+ * (SURVEY §8(f) NEXT-4.)
+ * ------------------------------------------------------------------------------------- */
+double oracle_lb_improved(const float *A, const float *B, const float *UB, const float *LB,
+                          int L, int W) {
+    W = clamp_w(L, W);
+    float *Ap = (float *)malloc(sizeof(float) * (size_t)L);
+    float *Ua = (float *)malloc(sizeof(float) * (size_t)L);
+    float *La = (float *)malloc(sizeof(float) * (size_t)L);
+    for (int i = 0; i < L; ++i) {
+        if (A[i] > UB[i]) Ap[i] = UB[i];
+        else if (A[i] < LB[i]) Ap[i] = LB[i];
+        else Ap[i] = A[i];
+    }
+    oracle_envelope(Ap, L, W, Ua, La);
+    double res = oracle_lb_keogh(A, UB, LB, L) + oracle_lb_keogh(B, Ua, La, L);
+    free(Ap); free(Ua); free(La);
+    return res;
+}
+
+/* ---------------------------------------------------------------------------------------
+ * LB_New_W (Shen et al.; §2.3.4 "New Lower Bound"):
+ *   delta(A_1,B_1) + delta(A_L,B_L) + sum_{i=2}^{L-1} min_{j in [max(1,i-W), min(L,i+W)]}
+ *   delta(A_i, B_j).
+ * For L = 1 the two boundary terms are the same cell; the value is delta(A_1,B_1) (as C11).
+ * ------------------------------------------------------------------------------------- */
+double oracle_lb_new(const float *A, const float *B, int L, int W) {
+    W = clamp_w(L, W);
+    if (L == 1) return delta((double)A[0], (double)B[0]);
+    double res = delta((double)A[0], (double)B[0]) + delta((double)A[L - 1], (double)B[L - 1]);
+    for (int i = 2; i <= L - 1; ++i) {
+        int lo = i - W < 1 ? 1 : i - W;
+        int hi = i + W > L ? L : i + W;
+        double m = ORACLE_INF;
+        for (int j = lo; j <= hi; ++j) m = min2(m, delta((double)A[i - 1], (double)B[j - 1]));
+        res = res + m;
+    }
+    return res;
+}
+
+/* Symmetric LB_Enhanced: max(LB_Enh(A,B), LB_Enh(B,A)); UB/LB
+ * = envelope of B, UA/LA = envelope of A.  Both are admissible (Thm 2 with the roles of A and
+ * B exchanged; DTW is symmetric), so their max is. */
+double oracle_lb_enhanced_sym(const float *A, const float *B, const float *UA, const float *LA,
+                              const float *UB, const float *LB, int L, int W, int V) {
+    double x = oracle_lb_enhanced(A, B, UB, LB, L, W, V, ORACLE_INF, 0.0, NULL);
+    double y = oracle_lb_enhanced(B, A, UA, LA, L, W, V, ORACLE_INF, 0.0, NULL);
+    return x > y ? x : y;
+}
+
 /* The cascade value used by the search (P:299-304 cascading, P:619-621 Kim):
  * max(LB_Kim_sum, LB_Enhanced) with no abort. */
 double oracle_lb_cascade(const float *A, const float *B, const float *U, const float *Lo,

@@ -354,3 +354,75 @@ def test_window_rule():
     assert datagen.window_from_percent(100, 2048) == 2047
     assert [datagen.window_from_percent(p, 256) for p in (1, 10, 20, 50, 100)] == \
         [3, 26, 52, 128, 255]
+
+
+# ---------------- LB_Improved, LB_New, symmetric LB_Enhanced ----------
+
+def test_next_bounds_hand_example(oracle_lib):
+    """Worked by hand (no code): A = (0, 3, 1), B = (1, 0, 2), W = 1.
+    Envelope of B (Eq. 3-4): U = (1, 2, 2), L = (0, 0, 0).  LB_Keogh(A,B) = (3-2)^2 = 1.
+    Projection (P:261-268): A' = (0, 2, 1); envelope of A': U = (2, 2, 2), L = (0, 0, 1);
+    LB_Keogh(B, A') = 0 (B = (1, 0, 2) lies inside), so LB_Improved = 1 + 0 = 1.
+    LB_New (P:292-296) = delta(0,1) + delta(1,2) + min_{b in {1,0,2}} delta(3,b) = 1 + 1 + 1 = 3.
+    DTW_1 by the recurrence: D11=1, D12=1, D21=5, D22=10, D23=2, D32=6, D33=1+min(10,2,6)=3.
+    LB_Enhanced^1 (Alg. 1, n_bands=1): 1 + 1 + bridge column 2: (3-2)^2 = 1 -> 3; the reverse
+    LB_Enhanced(B,A) with env A = (3,3,3)/(0,0,1): 1 + 1 + 0 = 2 -> symmetric = 3."""
+    o = oracle_lib
+    A = np.array([0, 3, 1], np.float32)
+    B = np.array([1, 0, 2], np.float32)
+    assert o.dtw(A, B, 1) == 3.0
+    assert o.lb_improved(A, B, 1) == 1.0
+    assert o.lb_new(A, B, 1) == 3.0
+    assert o.lb_enhanced_sym(A, B, 1, 1) == 3.0
+    UA, LA = o.envelope(A, 1)
+    assert o.lb_enhanced(B, A, UA, LA, 1, 1)[0] == 2.0
+
+
+def test_next_bounds_admissible_and_ordered(oracle_lib):
+    """Every bound <= DTW_W (brute-force path enumeration, L <= 7, all W); LB_Improved and LB_New
+    >= LB_Keogh (both add non-negative terms / take mins over a subset of the envelope range);
+    symmetric >= each direction; W = 0 reduces LB_Improved and LB_New to the squared ED;
+    LB_New is non-increasing in W (its windows grow)."""
+    o = oracle_lib
+    for a, b in rng_pairs(21, 120, 7):
+        L = a.size
+        prev_new = None
+        for w in range(0, L):
+            d = brute_dtw(a, b, w)
+            tol = 1e-12 * max(1.0, d)
+            U, Lo = o.envelope(b, w)
+            keogh = o.lb_keogh(a, U, Lo)
+            imp = o.lb_improved(a, b, w)
+            new = o.lb_new(a, b, w)
+            assert imp <= d + tol and new <= d + tol, (a, b, w, imp, new, d)
+            assert imp >= keogh - tol and new >= keogh - tol
+            for V in range(1, L // 2 + 1):
+                s = o.lb_enhanced_sym(a, b, w, V)
+                f = o.lb_enhanced(a, b, U, Lo, w, V)[0]
+                UA, LA = o.envelope(a, w)
+                r = o.lb_enhanced(b, a, UA, LA, w, V)[0]
+                assert s == max(f, r) and s <= d + tol
+            if prev_new is not None:
+                assert new <= prev_new + tol
+            prev_new = new
+        ed = o.sqed(a, b)
+        assert o.lb_improved(a, b, 0) == pytest.approx(ed, rel=1e-12, abs=1e-300)
+        assert o.lb_new(a, b, 0) == pytest.approx(ed, rel=1e-12, abs=1e-300)
+
+
+def test_lb_new_is_min_over_window_cells(oracle_lib):
+    """LB_New's inner term is the minimum over the band cells of row i: for
+    integer series the nearest-value search equals an explicit sort-based nearest neighbour."""
+    o = oracle_lib
+    rng = np.random.default_rng(23)
+    for _ in range(200):
+        L = int(rng.integers(3, 30))
+        w = int(rng.integers(0, L))
+        a, b = datagen.random_series(rng, 2, L, "int")
+        tot = (float(a[0]) - float(b[0])) ** 2 + (float(a[-1]) - float(b[-1])) ** 2
+        for i in range(1, L - 1):
+            win = np.sort(b[max(0, i - w):min(L, i + w + 1)].astype(np.float64))
+            k = np.searchsorted(win, float(a[i]))
+            cand = [win[j] for j in (k - 1, k) if 0 <= j < win.size]
+            tot += min((float(a[i]) - c) ** 2 for c in cand)
+        assert o.lb_new(a, b, w) == tot
