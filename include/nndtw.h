@@ -115,6 +115,50 @@ NNDTW_API int nndtw_lb_enhanced(const float *q, int64_t nq, const nndtw_kim *qki
                       int64_t ldlb, void *stream);
 
 /*
+ * S2, symmetric variant:
+ *   lb[i*ldlb + j] = max(LB(q_i, t_j), LB(t_j, q_i))  [then max with LB_Kim under WITH_KIM]
+ * with LB = LB_Enhanced^V_W (or LB_Keogh under NNDTW_LB_KEOGH).  The boundary terms and the
+ * bands of Algorithm 1 are symmetric in (A, B), so only the LB_Keogh bridge differs: the
+ * second pass runs the tile kernel with the roles exchanged (queries' envelopes q_upper /
+ * q_lower, from nndtw_envelopes on q) and folds its value in with max.  Admissible: DTW is
+ * symmetric and each direction is a lower bound (Thm 2).  Same layouts as nndtw_lb_enhanced;
+ * q_upper, q_lower: [nq][L].  Cost: twice the bridge work.
+ */
+NNDTW_API int nndtw_lb_enhanced_symmetric(const float *q, const float *q_upper,
+                                          const float *q_lower, const nndtw_kim *qkim,
+                                          int64_t nq, const float *t, const float *t_upper,
+                                          const float *t_lower, const nndtw_kim *tkim,
+                                          int64_t nt, int32_t L, int32_t w, int32_t v,
+                                          uint32_t flags, float *lb, int64_t ldlb,
+                                          void *stream);
+
+/*
+ * Comparison bounds of the paper's evaluation, all pairs:
+ * nndtw_lb_improved: LB_Improved_W(q_i, t_j) = LB_Keogh(q_i, env t_j) + LB_Keogh(t_j, env q'),
+ *   q' the projection of q_i onto t_j's envelope (§2.3.3); t_upper / t_lower are
+ *   t's envelopes (nndtw_envelopes with the same w).
+ * nndtw_lb_new: LB_New_W(q_i, t_j) = delta(first) + delta(last) + sum over the inner i of the
+ *   minimum delta(q_i, t_j') over the window (§2.3.4).
+ * Measurement kernels (tightness tables, Fig. 1/2, 10/11 analogues): O(L*w) per pair.
+ * q: [nq][L]; t: [nt][L]; lb: [nq][ldlb] out, ldlb >= nt.  fp32.  Asynchronous.
+ */
+NNDTW_API int nndtw_lb_improved(const float *q, int64_t nq, const float *t,
+                                const float *t_upper, const float *t_lower, int64_t nt,
+                                int32_t L, int32_t w, float *lb, int64_t ldlb, void *stream);
+NNDTW_API int nndtw_lb_new(const float *q, int64_t nq, const float *t, int64_t nt, int32_t L,
+                           int32_t w, float *lb, int64_t ldlb, void *stream);
+
+/*
+ * Tightness (reading C20): over the n pairs with 0 < dtw[p] <
+ * +inf, accumulate sum[0] += sum of sqrt(lb[p] / dtw[p]) (fp64), count[0] += #pairs and
+ * max_bits[0] = max(max_bits[0], float bits of the largest ratio).  lb and dtw are squared
+ * values (fp32 device arrays [n]); sum (double[1]), count (uint64[1]) and max_bits
+ * (uint32[1]) are device pointers the caller zeroes.  Asynchronous.
+ */
+NNDTW_API int nndtw_tightness(const float *lb, const float *dtw, int64_t n, double *sum,
+                              uint64_t *count, uint32_t *max_bits, void *stream);
+
+/*
  * S4 -- batched windowed DTW, Eq. 1 inside |i-j| <= w, with early
  * abandoning.  Pair p compares a[ia[p]] with b[ib[p]] (ia/ib nullable = p).
  * cutoff: [npairs] squared cutoffs, nullable (= +inf).  out[p] = squared DTW in fp32, or +inf
@@ -148,6 +192,10 @@ NNDTW_API int nndtw_dtw_batch(const float *a, const float *b, const int32_t *ia,
 /* flags & NNDTW_CLASSIFY_BOUND_KEOGH: prune with max(LB_Kim, LB_Keogh) instead of
  * max(LB_Kim, LB_Enhanced^V) (same exact answer; a baseline for the V-sweep). */
 #define NNDTW_CLASSIFY_BOUND_KEOGH 2u
+/* flags & NNDTW_CLASSIFY_BOUND_SYMMETRIC: prune with the symmetric bound max(LB(q,t), LB(t,q))
+ * (see nndtw_lb_enhanced_symmetric); the queries' envelopes are built in ws.
+ * Same exact answer; tighter bound, twice the bridge work. */
+#define NNDTW_CLASSIFY_BOUND_SYMMETRIC 4u
 NNDTW_API size_t nndtw_classify_workspace_bytes(int64_t nq, int64_t nt, int32_t L, int32_t w);
 NNDTW_API int nndtw_classify(const float *q, int64_t nq, const float *t, const float *upper,
                    const float *lower, const nndtw_kim *tkim, int64_t nt, int64_t index_base,

@@ -102,6 +102,7 @@ struct ClassifyWs {
     TieEntry *log;
     unsigned long long log_cap;
     long long *cells_prefix;
+    float *qU, *qL;  // query envelopes (symmetric bound)
     size_t bytes;
 };
 
@@ -133,6 +134,8 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
     W.log_cap = (unsigned long long)(64 * nq > 65536 ? 64 * nq : 65536);
     W.log = (TieEntry *)take(sizeof(TieEntry) * (size_t)W.log_cap);
     W.cells_prefix = (long long *)take(sizeof(long long) * (size_t)(2 * L));
+    W.qU = (float *)take(sizeof(float) * q1 * (size_t)L);  // symmetric bound: query envelopes
+    W.qL = (float *)take(sizeof(float) * q1 * (size_t)L);
     W.bytes = off;
     return W;
 }
@@ -227,10 +230,18 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     // S2: cascade bound for all pairs + per-query argmin-LB candidate
     launch_series_stats(q, nq, L, W.qkim, st);
     tm.mark();  // 1
+    const int keogh = (flags & NNDTW_CLASSIFY_BOUND_KEOGH) ? 1 : 0;
+    const bool sym = (flags & NNDTW_CLASSIFY_BOUND_SYMMETRIC) != 0;
     if (nt > 0 && launch_lb(q, nq, W.qkim, t, U, Lo, tkim, nt, L, w, v, 1, self_offset, W.lb,
-                            W.ldlb, W.minkey, st,
-                            (flags & NNDTW_CLASSIFY_BOUND_KEOGH) ? 1 : 0))
+                            W.ldlb, sym ? nullptr : W.minkey, st, keogh))
         return fail(NNDTW_E_ARG, "too many train series for one launch");
+    if (nt > 0 && sym) {  // second direction of the symmetric bound, then the seed argmin
+        launch_envelopes(q, nq, L, w, W.qU, W.qL, nullptr, st);
+        if (launch_lb(t, nt, nullptr, q, W.qU, W.qL, nullptr, nq, L, w, v, 0, -1, W.lb, W.ldlb,
+                      nullptr, st, keogh, 1))
+            return fail(NNDTW_E_ARG, "too many queries for one launch");
+        launch_row_argmin(W.lb, W.ldlb, nq, nt, W.minkey, st);
+    }
     tm.mark();  // 2
     if ((rc = cuda_fail("lb"))) return rc;
     TieLog log{W.log, W.log_count, W.log_cap, W.overflow};
@@ -372,6 +383,72 @@ int nndtw_lb_enhanced(const float *q, int64_t nq, const nndtw_kim *qkim, const f
                   nullptr, (cudaStream_t)stream, (flags & NNDTW_LB_KEOGH) ? 1 : 0))
         return fail(NNDTW_E_ARG, "too many train series for one launch");
     return cuda_fail("nndtw_lb_enhanced");
+}
+
+int nndtw_lb_enhanced_symmetric(const float *q, const float *q_upper, const float *q_lower,
+                                const nndtw_kim *qkim, int64_t nq, const float *t,
+                                const float *t_upper, const float *t_lower,
+                                const nndtw_kim *tkim, int64_t nt, int32_t L, int32_t w,
+                                int32_t v, uint32_t flags, float *lb, int64_t ldlb,
+                                void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if ((rc = check_common(nq, L, w))) return rc;
+    if (nt < 0) return fail(NNDTW_E_ARG, "negative nt");
+    if (v < 1) return fail(NNDTW_E_V, "V must be >= 1");
+    if (ldlb < nt) return fail(NNDTW_E_ARG, "ldlb < nt");
+    bool kim = (flags & NNDTW_LB_WITH_KIM) != 0;
+    if (nq > 0 && nt > 0 && (!q || !q_upper || !q_lower || !t || !t_upper || !t_lower || !lb ||
+                             (kim && (!qkim || !tkim))))
+        return fail(NNDTW_E_ARG, "null pointer argument");
+    const int keogh = (flags & NNDTW_LB_KEOGH) ? 1 : 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (launch_lb(q, nq, qkim, t, t_upper, t_lower, tkim, nt, L, w, v, kim ? 1 : 0, -1, lb,
+                  ldlb, nullptr, st, keogh) ||
+        launch_lb(t, nt, nullptr, q, q_upper, q_lower, nullptr, nq, L, w, v, 0, -1, lb, ldlb,
+                  nullptr, st, keogh, 1))
+        return fail(NNDTW_E_ARG, "too many series for one launch");
+    return cuda_fail("nndtw_lb_enhanced_symmetric");
+}
+
+int nndtw_lb_improved(const float *q, int64_t nq, const float *t, const float *t_upper,
+                      const float *t_lower, int64_t nt, int32_t L, int32_t w, float *lb,
+                      int64_t ldlb, void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if ((rc = check_common(nq, L, w))) return rc;
+    if (nt < 0) return fail(NNDTW_E_ARG, "negative nt");
+    if (ldlb < nt) return fail(NNDTW_E_ARG, "ldlb < nt");
+    if (nq > 0 && nt > 0 && (!q || !t || !t_upper || !t_lower || !lb))
+        return fail(NNDTW_E_ARG, "null pointer argument");
+    if (launch_lb_pairs(1, q, nq, t, t_upper, t_lower, nt, L, w, lb, ldlb, (cudaStream_t)stream))
+        return fail(NNDTW_E_LENGTH, "L too long for the LB_Improved kernel's shared memory");
+    return cuda_fail("nndtw_lb_improved");
+}
+
+int nndtw_lb_new(const float *q, int64_t nq, const float *t, int64_t nt, int32_t L, int32_t w,
+                 float *lb, int64_t ldlb, void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if ((rc = check_common(nq, L, w))) return rc;
+    if (nt < 0) return fail(NNDTW_E_ARG, "negative nt");
+    if (ldlb < nt) return fail(NNDTW_E_ARG, "ldlb < nt");
+    if (nq > 0 && nt > 0 && (!q || !t || !lb)) return fail(NNDTW_E_ARG, "null pointer argument");
+    if (launch_lb_pairs(0, q, nq, t, nullptr, nullptr, nt, L, w, lb, ldlb, (cudaStream_t)stream))
+        return fail(NNDTW_E_LENGTH, "L too long for the LB_New kernel's shared memory");
+    return cuda_fail("nndtw_lb_new");
+}
+
+int nndtw_tightness(const float *lb, const float *dtw, int64_t n, double *sum, uint64_t *count,
+                    uint32_t *max_bits, void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if (n < 0) return fail(NNDTW_E_ARG, "negative count");
+    if (n > 0 && (!lb || !dtw || !sum || !count || !max_bits))
+        return fail(NNDTW_E_ARG, "null pointer argument");
+    launch_tightness(lb, dtw, n, sum, (unsigned long long *)count, max_bits, sms,
+                     (cudaStream_t)stream);
+    return cuda_fail("nndtw_tightness");
 }
 
 int nndtw_dtw_batch(const float *a, const float *b, const int32_t *ia, const int32_t *ib,

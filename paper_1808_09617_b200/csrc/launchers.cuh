@@ -11,7 +11,16 @@ int launch_check_finite(const float *x, int64_t n, int32_t *bad, cudaStream_t st
 int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
               const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L, int w,
               int v, int with_kim, int64_t self_offset, float *lb, int64_t ldlb,
-              unsigned long long *minkey, cudaStream_t st, int keogh = 0);
+              unsigned long long *minkey, cudaStream_t st, int keogh = 0, int transposed = 0);
+// S2 extras (bounds_next.cu): kind 0 = LB_New, 1 = LB_Improved (all pairs, measurement kernels)
+int launch_lb_pairs(int kind, const float *q, int64_t nq, const float *t, const float *U,
+                    const float *Lo, int64_t nt, int L, int w, float *lb, int64_t ldlb,
+                    cudaStream_t st);
+int launch_row_argmin(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
+                      unsigned long long *minkey, cudaStream_t st);
+int launch_tightness(const float *lb, const float *d, int64_t n, double *sum,
+                     unsigned long long *count, unsigned *max_bits, int num_sms,
+                     cudaStream_t st);
 int launch_fill_u64(unsigned long long *p, int64_t n, unsigned long long v, cudaStream_t st);
 int launch_seed_items(const unsigned long long *minkey, const int32_t *seed2, int64_t nq,
                       int64_t nt, Item *items, unsigned long long *count, cudaStream_t st);

@@ -39,6 +39,8 @@ struct LbParams {
     int64_t nt;
     int L, w, nb, with_kim;
     int keogh;  // 1: LB_Keogh over all L columns instead of LB_Enhanced
+    int transposed;  // 1: q/t roles exchanged -- write lb[t-row][q-col] = max(existing, value)
+                     // (second pass of the symmetric bound)
     int64_t self_offset;
     float *lb;
     int64_t ldlb;
@@ -269,6 +271,13 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
                 if (okmax) kim = kim + sq(ka.vmax - kb.vmax);
                 v = fmaxf(v, kim);
             }
+            if (p.transposed) {
+                if (qq < p.nq && nn < p.nt) {
+                    float *dst = p.lb + nn * p.ldlb + qq;
+                    *dst = fmaxf(*dst, v);
+                }
+                continue;
+            }
             if (p.self_offset >= 0 && nn == qq + p.self_offset) v = kInf;
             if (qq < p.nq && nn < p.nt) {
                 p.lb[qq * p.ldlb + nn] = v;
@@ -290,7 +299,7 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
 int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
               const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L, int w,
               int v, int with_kim, int64_t self_offset, float *lb, int64_t ldlb,
-              unsigned long long *minkey, cudaStream_t st, int keogh) {
+              unsigned long long *minkey, cudaStream_t st, int keogh, int transposed) {
     if (nq == 0 || nt == 0) return 0;
     if (w > L - 1) w = L - 1;
     LbParams p;
@@ -307,6 +316,12 @@ int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
     p.nb = (L / 2) < v ? (L / 2) : v;
     p.with_kim = with_kim;
     p.keogh = keogh;
+    p.transposed = transposed;
+    if (transposed) {
+        with_kim = 0;
+        p.with_kim = 0;
+        minkey = nullptr;
+    }
     p.self_offset = self_offset;
     p.lb = lb;
     p.ldlb = ldlb;

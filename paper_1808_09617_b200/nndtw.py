@@ -23,6 +23,7 @@ NNDTW_LB_WITH_KIM = 1
 NNDTW_LB_KEOGH = 2
 NNDTW_CLASSIFY_EXACT = 1
 NNDTW_CLASSIFY_BOUND_KEOGH = 2
+NNDTW_CLASSIFY_BOUND_SYMMETRIC = 4
 KEY_INIT = 0x7F800000FFFFFFFF
 
 
@@ -56,6 +57,11 @@ _SIGS = {
     "nndtw_series_stats": (C.c_int, [_P, _I64, _I32, _P, _P]),
     "nndtw_lb_enhanced": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32,
                                     C.c_uint32, _P, _I64, _P]),
+    "nndtw_lb_enhanced_symmetric": (C.c_int, [_P, _P, _P, _P, _I64, _P, _P, _P, _P, _I64, _I32,
+                                              _I32, _I32, C.c_uint32, _P, _I64, _P]),
+    "nndtw_lb_improved": (C.c_int, [_P, _I64, _P, _P, _P, _I64, _I32, _I32, _P, _I64, _P]),
+    "nndtw_lb_new": (C.c_int, [_P, _I64, _P, _I64, _I32, _I32, _P, _I64, _P]),
+    "nndtw_tightness": (C.c_int, [_P, _P, _I64, _P, _P, _P, _P]),
     "nndtw_dtw_batch": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P]),
     "nndtw_classify_workspace_bytes": (C.c_size_t, [_I64, _I64, _I32, _I32]),
     "nndtw_classify": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32,
@@ -158,6 +164,62 @@ def lb_enhanced(q, t, U, Lo, w: int, v: int, with_kim: bool = False, qkim=None, 
     return out
 
 
+def lb_enhanced_symmetric(q, t, w: int, v: int, with_kim: bool = False, keogh: bool = False,
+                          q_env=None, t_env=None, stream=None) -> torch.Tensor:
+    """S2 symmetric bound matrix [nq][nt]: max(LB(q,t), LB(t,q))."""
+    _series(q, "q"); _series(t, "t")
+    nq, L = q.shape
+    nt = t.shape[0]
+    qU, qL, qk = q_env if q_env is not None else envelopes(q, w, with_kim, stream)
+    tU, tL, tk = t_env if t_env is not None else envelopes(t, w, with_kim, stream)
+    out = torch.empty((nq, nt), dtype=torch.float32, device=q.device)
+    _check(load().nndtw_lb_enhanced_symmetric(
+        _ptr(q), _ptr(qU), _ptr(qL), _ptr(qk if with_kim else None), nq, _ptr(t), _ptr(tU),
+        _ptr(tL), _ptr(tk if with_kim else None), nt, L, int(w), int(v),
+        (NNDTW_LB_WITH_KIM if with_kim else 0) | (NNDTW_LB_KEOGH if keogh else 0), _ptr(out),
+        nt, _stream(stream)), "nndtw_lb_enhanced_symmetric")
+    return out
+
+
+def lb_improved(q, t, w: int, t_env=None, stream=None) -> torch.Tensor:
+    """LB_Improved_W for all pairs [nq][nt]."""
+    _series(q, "q"); _series(t, "t")
+    nq, L = q.shape
+    nt = t.shape[0]
+    tU, tL = (t_env[0], t_env[1]) if t_env is not None else envelopes(t, w, False, stream)[:2]
+    out = torch.empty((nq, nt), dtype=torch.float32, device=q.device)
+    _check(load().nndtw_lb_improved(_ptr(q), nq, _ptr(t), _ptr(tU), _ptr(tL), nt, L, int(w),
+                                    _ptr(out), nt, _stream(stream)), "nndtw_lb_improved")
+    return out
+
+
+def lb_new(q, t, w: int, stream=None) -> torch.Tensor:
+    """LB_New_W for all pairs [nq][nt]."""
+    _series(q, "q"); _series(t, "t")
+    nq, L = q.shape
+    nt = t.shape[0]
+    out = torch.empty((nq, nt), dtype=torch.float32, device=q.device)
+    _check(load().nndtw_lb_new(_ptr(q), nq, _ptr(t), nt, L, int(w), _ptr(out), nt,
+                               _stream(stream)), "nndtw_lb_new")
+    return out
+
+
+def tightness(lb: torch.Tensor, d: torch.Tensor, stream=None):
+    """(mean of sqrt(lb/d) over pairs with 0 < d < inf, pair count, max ratio) -- P:37."""
+    lb = lb.reshape(-1).contiguous()
+    d = d.reshape(-1).contiguous()
+    if lb.numel() != d.numel():
+        raise NNDTWError("lb and dtw must have the same number of pairs")
+    s = torch.zeros(1, dtype=torch.float64, device=lb.device)
+    c = torch.zeros(1, dtype=torch.int64, device=lb.device)
+    m = torch.zeros(1, dtype=torch.int32, device=lb.device)
+    _check(load().nndtw_tightness(_ptr(lb), _ptr(d), lb.numel(), _ptr(s), _ptr(c), _ptr(m),
+                                  _stream(stream)), "nndtw_tightness")
+    cnt = int(c.item())
+    mx = float(m.view(torch.float32).item())
+    return (float(s.item()) / cnt if cnt else 0.0), cnt, mx
+
+
 def dtw_batch(a, b, w: int, ia=None, ib=None, cutoff=None, stream=None) -> torch.Tensor:
     """S4: squared DTW_w of pairs (a[ia[p]], b[ib[p]]); +inf where abandoned at cutoff[p]."""
     _series(a, "a"); _series(b, "b")
@@ -187,7 +249,8 @@ class Model:
     """A train set with its envelopes and Kim features precomputed "at training time"."""
 
     def __init__(self, train: torch.Tensor, labels: torch.Tensor, w: int, v: int = 5,
-                 index_base: int = 0, check: bool = True, stream=None, bound: str = "enhanced"):
+                 index_base: int = 0, check: bool = True, stream=None, bound: str = "enhanced",
+                 symmetric: bool = False):
         _series(train, "train")
         if check and not check_finite(train, stream):
             raise NNDTWError("train set contains NaN or infinity")
@@ -200,6 +263,7 @@ class Model:
         if bound not in ("enhanced", "keogh"):
             raise NNDTWError("bound must be 'enhanced' or 'keogh'")
         self.bound = bound
+        self.symmetric = bool(symmetric)
         self.U, self.Lo, self.kim = envelopes(train, self.w, True, stream)
         self._ws = None
 
@@ -225,7 +289,8 @@ def classify_keys(model: Model, q: torch.Tensor, exact: bool = True, self_offset
                                  _ptr(model.kim), model.t.shape[0], model.index_base,
                                  int(self_offset), L, model.w, model.v,
                                  (NNDTW_CLASSIFY_EXACT if exact else 0) |
-                                 (NNDTW_CLASSIFY_BOUND_KEOGH if model.bound == "keogh" else 0),
+                                 (NNDTW_CLASSIFY_BOUND_KEOGH if model.bound == "keogh" else 0) |
+                                 (NNDTW_CLASSIFY_BOUND_SYMMETRIC if model.symmetric else 0),
                                  _ptr(ws), ws.numel(),
                                  _ptr(key), C.byref(st) if stats else None, _stream(stream)),
            "nndtw_classify")
