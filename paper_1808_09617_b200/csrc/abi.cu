@@ -8,6 +8,8 @@
 #include <mutex>
 #include <string>
 
+#include <cstdlib>
+
 #include "launchers.cuh"
 
 namespace nndtw {
@@ -132,6 +134,10 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
     W.item_cap = (unsigned long long)nq * (unsigned long long)nt + 1;
     W.items = (Item *)take(sizeof(Item) * (size_t)W.item_cap);
     W.log_cap = (unsigned long long)(64 * nq > 65536 ? 64 * nq : 65536);
+    if (const char *cap = getenv("NNDTW_TIE_LOG_CAP")) {  // tests: force the overflow path
+        const long long c = atoll(cap);
+        if (c > 0 && (unsigned long long)c < W.log_cap) W.log_cap = (unsigned long long)c;
+    }
     W.log = (TieEntry *)take(sizeof(TieEntry) * (size_t)W.log_cap);
     W.cells_prefix = (long long *)take(sizeof(long long) * (size_t)(2 * L));
     W.qU = (float *)take(sizeof(float) * q1 * (size_t)L);  // symmetric bound: query envelopes
@@ -186,10 +192,10 @@ static void exact_local(ClassifyWs &W, const float *q, int64_t nq, const float *
     launch_tie_count(W.log, W.log_count, W.log_cap, key, eps_t, W.tiecnt, sms, st);
     launch_refine(W.log, W.log_count, W.log_cap, q, t, L, w, key, eps_t, W.f64key, cnt,
                   W.tiecnt, W.overflow, sms, st);
-    launch_refine_overflow(W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w, key, eps_p, 0,
+    launch_refine_overflow(W.log_count, W.log_cap, W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w, key, eps_p, 0,
                            W.f64key, nullptr, index_base, nullptr, sms, st);
     launch_resolve(W.log, W.log_count, W.log_cap, W.f64key, index_base, W.resolve_out, sms, st);
-    launch_refine_overflow(W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w, key, eps_p, 1,
+    launch_refine_overflow(W.log_count, W.log_cap, W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w, key, eps_p, 1,
                            W.f64key, W.f64key, index_base, W.resolve_out, sms, st);
     launch_swap_key(W.resolve_out, nq, key, st);
 }
@@ -498,7 +504,7 @@ int nndtw_classify_refine(void *ws, size_t ws_bytes, const float *q, int64_t nq,
         launch_refine(W.log, W.log_count, W.log_cap, q, t, L, w,
                       (const unsigned long long *)gkey, eps_tie(L),
                       (unsigned long long *)f64key, nullptr, nullptr, W.overflow, sms, st);
-        launch_refine_overflow(W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w,
+        launch_refine_overflow(W.log_count, W.log_cap, W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w,
                                (const unsigned long long *)gkey, eps_prune(L), 0,
                                (unsigned long long *)f64key, nullptr, 0, nullptr, sms, st);
     }
@@ -521,7 +527,7 @@ int nndtw_classify_resolve(void *ws, size_t ws_bytes, const float *q, int64_t nq
     if (nt > 0) {
         launch_resolve(W.log, W.log_count, W.log_cap, (const unsigned long long *)gf64,
                        index_base, (unsigned long long *)out, sms, st);
-        launch_refine_overflow(W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w,
+        launch_refine_overflow(W.log_count, W.log_cap, W.overflow, nq, W.lb, W.ldlb, nt, q, t, L, w,
                                (const unsigned long long *)gkey, eps_prune(L), 1, nullptr,
                                (const unsigned long long *)gf64, index_base,
                                (unsigned long long *)out, sms, st);

@@ -37,7 +37,8 @@ int launch_refine(TieEntry *e, const unsigned long long *count, unsigned long lo
 int launch_tie_count(const TieEntry *e, const unsigned long long *count, unsigned long long cap,
                      const unsigned long long *gkey, float eps_t, unsigned *tiecnt, int num_sms,
                      cudaStream_t st);
-int launch_refine_overflow(const unsigned *overflow, int64_t nq, const float *lb, int64_t ldlb,
+int launch_refine_overflow(const unsigned long long *log_count, unsigned long long log_cap,
+                           const unsigned *overflow, int64_t nq, const float *lb, int64_t ldlb,
                            int64_t nt, const float *A, const float *B, int L, int w,
                            const unsigned long long *gkey, float eps_p, int pass,
                            unsigned long long *f64key, const unsigned long long *gf64,

@@ -49,8 +49,13 @@ int launch_seed_items(const unsigned long long *minkey, const int32_t *seed2, in
     return 0;
 }
 
-// ---- S3 compaction: surviving pairs LB <= bsf*(1+eps_p), warp-ballot compacted ----------------
-// One CTA-tile = (query q, 1024 consecutive train indices); 4 per thread.
+// ---- S3 compaction: surviving pairs LB <= bsf*(1+eps_p), compacted with ballot/popc ----------
+// One CTA-tile = (query q, CT_N consecutive train indices), 16 consecutive ones per thread (4
+// float4 loads), so the items leave in train-index order within the tile.  Survivor counts are scanned within the warp (shuffles) and across the
+// CTA's warps (shared memory), so there is one atomicAdd on the global item counter per tile --
+// a per-warp atomic on that single address serialised the kernel at ~8M atomics per step.
+constexpr int CT_N = 4096;
+
 __global__ void __launch_bounds__(256) k_compact(const float *__restrict__ lb, int64_t ldlb,
                                                  int64_t nq, int64_t nt,
                                                  const unsigned long long *__restrict__ key,
@@ -59,50 +64,66 @@ __global__ void __launch_bounds__(256) k_compact(const float *__restrict__ lb, i
                                                  Item *__restrict__ items,
                                                  unsigned long long *count,
                                                  unsigned long long capacity) {
-    const int64_t tiles_per_row = (nt + 1023) / 1024;
+    __shared__ int wsum[8];
+    __shared__ unsigned long long sbase;
+    const int64_t tiles_per_row = (nt + CT_N - 1) / CT_N;
     const int64_t ntiles = tiles_per_row * nq;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool vec = (ldlb & 3) == 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t q = tile / tiles_per_row;
-        const int64_t n0 = (tile % tiles_per_row) * 1024 + threadIdx.x * 4;
+        const int64_t nbase = (tile % tiles_per_row) * CT_N;
         const float thr = key_dist(key[q]) * (1.0f + eps_p);
         const unsigned s1 = (unsigned)(minkey[q] & 0xffffffffull);
         const unsigned s2 = seed2 ? (unsigned)seed2[q] : 0xffffffffu;
         const float *row = lb + q * ldlb;
-        float v[4];
-        if (n0 + 3 < nt && (ldlb & 3) == 0) {
-            float4 f = *reinterpret_cast<const float4 *>(row + n0);
-            v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-        } else {
+        unsigned flags = 0;  // bit 4k+e: element nbase + 16*tid + 4k + e survives
 #pragma unroll
-            for (int e = 0; e < 4; ++e) v[e] = (n0 + e < nt) ? row[n0 + e] : kInf;
-        }
-        unsigned flags = 0;
+        for (int k = 0; k < 4; ++k) {
+            const int64_t n0 = nbase + 16 * threadIdx.x + 4 * k;
+            float v[4];
+            if (vec && n0 + 3 < nt) {
+                const float4 f = *reinterpret_cast<const float4 *>(row + n0);
+                v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+            } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            unsigned n = (unsigned)(n0 + e);
-            bool ok = (n0 + e < nt) && v[e] <= thr && n != s1 && n != s2;
-            flags |= (ok ? 1u : 0u) << e;
+                for (int e = 0; e < 4; ++e) v[e] = (n0 + e < nt) ? row[n0 + e] : kInf;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const unsigned n = (unsigned)(n0 + e);
+                const bool ok = (n0 + e < nt) && v[e] <= thr && n != s1 && n != s2;
+                flags |= (ok ? 1u : 0u) << (4 * k + e);
+            }
         }
-        int c = __popc(flags);
+        const int c = __popc(flags);
         int incl = c;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-            int o = __shfl_up_sync(0xffffffffu, incl, off);
+            const int o = __shfl_up_sync(0xffffffffu, incl, off);
             if (lane >= off) incl += o;
         }
-        int total = __shfl_sync(0xffffffffu, incl, 31);
-        unsigned long long base = 0;
-        if (lane == 31 && total > 0) base = atomicAdd(count, (unsigned long long)total);
-        base = __shfl_sync(0xffffffffu, base, 31);
-        unsigned long long pos = base + (unsigned long long)(incl - c);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if (flags & (1u << e)) {
-                if (pos < capacity) items[pos] = Item{(unsigned)q, (unsigned)(n0 + e)};
-                ++pos;
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int run = 0;
+            for (int i = 0; i < 8; ++i) {
+                const int t = wsum[i];
+                wsum[i] = run;
+                run += t;
             }
+            sbase = run > 0 ? atomicAdd(count, (unsigned long long)run) : 0ull;
         }
+        __syncthreads();
+        unsigned long long pos = sbase + (unsigned long long)(wsum[warp] + incl - c);
+        while (flags) {
+            const int bit = __ffs(flags) - 1;
+            flags &= flags - 1;
+            if (pos < capacity)
+                items[pos] = Item{(unsigned)q, (unsigned)(nbase + 16 * threadIdx.x + bit)};
+            ++pos;
+        }
+        __syncthreads();  // wsum / sbase are reused by the next tile
     }
 }
 
@@ -111,7 +132,7 @@ int launch_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
                    const int32_t *seed2, float eps_p, Item *items, unsigned long long *count,
                    unsigned long long capacity, int num_sms, cudaStream_t st) {
     if (nq == 0 || nt == 0) return 0;
-    int64_t ntiles = ((nt + 1023) / 1024) * nq;
+    int64_t ntiles = ((nt + CT_N - 1) / CT_N) * nq;
     int64_t grid = ntiles < (int64_t)num_sms * 8 ? ntiles : (int64_t)num_sms * 8;
     k_compact<<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, minkey, seed2, eps_p,
                                                items, count, capacity);
@@ -297,13 +318,15 @@ __global__ void k_refine(TieEntry *e, const unsigned long long *count, unsigned 
 // Overflowed queries (the tie log dropped an entry): every pair that survived the cascade at
 // the global best is re-ranked in fp64 (rare, slow, exact).  pass 0: min fp64 -> f64key;
 // pass 1: lowest index with fp64 == gf64 -> out.
-__global__ void k_refine_overflow(const unsigned *overflow, int64_t nq, const float *lb,
+__global__ void k_refine_overflow(const unsigned long long *log_count, unsigned long long log_cap,
+                                  const unsigned *overflow, int64_t nq, const float *lb,
                                   int64_t ldlb, int64_t nt, const float *__restrict__ A,
                                   const float *__restrict__ B, int L, int w,
                                   const unsigned long long *gkey, float eps_p, int pass,
                                   unsigned long long *f64key, const unsigned long long *gf64,
                                   int64_t index_base, unsigned long long *out) {
     extern __shared__ double dbuf[];
+    if (*log_count <= log_cap) return;  // no entry was dropped: nothing to re-rank here
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     double *buf = dbuf + (size_t)warp * (L + 1);
@@ -350,7 +373,8 @@ int launch_refine(TieEntry *e, const unsigned long long *count, unsigned long lo
     return 0;
 }
 
-int launch_refine_overflow(const unsigned *overflow, int64_t nq, const float *lb, int64_t ldlb,
+int launch_refine_overflow(const unsigned long long *log_count, unsigned long long log_cap,
+                           const unsigned *overflow, int64_t nq, const float *lb, int64_t ldlb,
                            int64_t nt, const float *A, const float *B, int L, int w,
                            const unsigned long long *gkey, float eps_p, int pass,
                            unsigned long long *f64key, const unsigned long long *gf64,
@@ -361,7 +385,8 @@ int launch_refine_overflow(const unsigned *overflow, int64_t nq, const float *lb
     int block = refine_block(L, &smem);
     cudaFuncSetAttribute(k_refine_overflow, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    k_refine_overflow<<<num_sms, block, smem, st>>>(overflow, nq, lb, ldlb, nt, A, B, L, w,
+    k_refine_overflow<<<num_sms, block, smem, st>>>(log_count, log_cap, overflow, nq, lb, ldlb,
+                                                    nt, A, B, L, w,
                                                     gkey, eps_p, pass, f64key, gf64,
                                                     index_base, out);
     count_launch(1, __func__);

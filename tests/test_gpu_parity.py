@@ -343,3 +343,20 @@ def test_classify_keogh_bound_same_answer(dev, oracle_lib):
         pred = nndtw.classify(model, T(ds.test[:nq], dev), stats=True)
         _check_nn(oracle_lib, ds.train, ds.train_labels, ds.test[:nq], w,
                   pred.idx.cpu().numpy(), pred.label.cpu().numpy(), pred.dist.cpu().numpy())
+
+
+def test_classify_tie_log_overflow(dev, oracle_lib, monkeypatch):
+    """Force the near-tie log to overflow (capacity 8 entries): the affected queries fall back
+    to re-ranking every surviving candidate in fp64 (k_refine_overflow), same exact answer."""
+    from paper_1808_09617_b200 import nndtw
+    monkeypatch.setenv("NNDTW_TIE_LOG_CAP", "8")
+    rng = np.random.default_rng(5)
+    Tr = datagen.random_series(rng, 60, 24, "int")
+    Tr = np.concatenate([Tr, Tr, Tr[:20]])          # every candidate has exact duplicates
+    Q = np.concatenate([Tr[:10], datagen.random_series(rng, 20, 24, "int")])
+    lab = (np.arange(Tr.shape[0]) % 5).astype(np.int32)
+    for w in (0, 3, 23):
+        model = nndtw.Model(T(Tr, dev), T(lab, dev), w, 3)
+        pred = nndtw.classify(model, T(Q, dev))
+        _check_nn(oracle_lib, Tr, lab, Q, w, pred.idx.cpu().numpy(), pred.label.cpu().numpy(),
+                  pred.dist.cpu().numpy(), V=3)
