@@ -138,6 +138,21 @@ __global__ void __launch_bounds__(512) k(float *out, long long *cyc, float seed)
                 asm volatile("max.f32 %0, %1, %2;" : "=f"(t) : "f"(u), "f"(l));
                 asm volatile("max.f32 %0, %1, 0f00000000;" : "=f"(r) : "f"(t));
                 asm volatile("fma.rn.f32 %0, %1, %2, %0;" : "+f"(x[c]) : "f"(t), "f"(r));
+            } else if (V == 19) {  // FADD2 + FFMA alternating (do they share a sub-pipe?)
+                asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(px[c]) : "l"(py[c]));
+                asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(y[c]), "f"(z[c]));
+            } else if (V == 20) {  // FADD2 + FFMA + FMNMX3
+                asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(px[c]) : "l"(py[c]));
+                asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(y[c]), "f"(z[c]));
+                asm volatile("min.f32 %0, %0, %1, %2;" : "+f"(z[c]) : "f"(y[c]), "f"(x[(c + 1) % NCH]));
+            } else if (V == 21) {  // FADD + FFMA alternating
+                asm volatile("add.f32 %0, %0, %1;" : "+f"(y[c]) : "f"(z[c]));
+                asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(y[c]), "f"(z[c]));
+            } else if (V == 22) {  // FADD2 + FMNMX3
+                asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(px[c]) : "l"(py[c]));
+                asm volatile("min.f32 %0, %0, %1, %2;" : "+f"(z[c]) : "f"(y[c]), "f"(x[(c + 1) % NCH]));
+            } else if (V == 23) {  // FADD2 with a broadcast scalar operand
+                asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(px[c]) : "l"(pk(y[c], y[c])));
             } else if (V == 16) {  // FFMA + FMNMX (2-in) alternating
                 asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(y[c]), "f"(z[c]));
                 asm volatile("min.f32 %0, %0, %1;" : "+f"(z[c]) : "f"(x[(c + 1) % NCH]));
@@ -202,6 +217,11 @@ int main() {
     run<17>("LB packed 2FADD2,2FMNMX3,2FFMA", 6, 2, nsm, out, cyc);
     run<18>("LB FADD,FADD,FMNMX,FMNMX,FFMA", 5, 1, nsm, out, cyc);
     run<14>("FMNMX3 imm 0", 1, 0, nsm, out, cyc);
+    run<19>("FADD2+FFMA", 2, 0, nsm, out, cyc);
+    run<20>("FADD2+FFMA+FMNMX3", 3, 0, nsm, out, cyc);
+    run<21>("FADD+FFMA", 2, 0, nsm, out, cyc);
+    run<22>("FADD2+FMNMX3", 2, 0, nsm, out, cyc);
+    run<23>("FADD2 broadcast", 1, 0, nsm, out, cyc);
     run<15>("FFMA+FMNMX3", 2, 0, nsm, out, cyc);
     run<16>("FFMA+FMNMX", 2, 0, nsm, out, cyc);
     return 0;
