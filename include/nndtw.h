@@ -196,6 +196,14 @@ NNDTW_API int nndtw_dtw_batch(const float *a, const float *b, const int32_t *ia,
  * (see nndtw_lb_enhanced_symmetric); the queries' envelopes are built in ws.
  * Same exact answer; tighter bound, twice the bridge work. */
 #define NNDTW_CLASSIFY_BOUND_SYMMETRIC 4u
+/* Two-phase call for a sharded search (dist.py): PHASE_SEED runs the initialisation, the S2
+ * bound and the S3 seed round and returns the seed keys in key (state kept in ws); the caller
+ * MIN-reduces key over the shards; PHASE_SEARCH (same ws, q, t, flags otherwise) takes that
+ * key as the starting best-so-far -- a valid upper bound on every query's global NN distance,
+ * so each shard prunes against the global seed instead of its own -- and runs S3 compaction
+ * and S4/S5.  Neither flag: both phases in one call.  The answer does not change. */
+#define NNDTW_CLASSIFY_PHASE_SEED 8u
+#define NNDTW_CLASSIFY_PHASE_SEARCH 16u
 NNDTW_API size_t nndtw_classify_workspace_bytes(int64_t nq, int64_t nt, int32_t L, int32_t w);
 NNDTW_API int nndtw_classify(const float *q, int64_t nq, const float *t, const float *upper,
                    const float *lower, const nndtw_kim *tkim, int64_t nt, int64_t index_base,

@@ -225,56 +225,68 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     StageTimer tm(stats != nullptr && outer_tm == nullptr, st);
     const float eps_p = eps_prune(L), eps_t = eps_tie(L);
 
-    tm.mark();  // 0
-    cudaMemsetAsync(W.counters, 0, sizeof(unsigned long long) * (CNT_N + 3), st);
-    launch_fill_u64(key, nq, kKeyInit, st);
-    cudaMemsetAsync(W.minkey, 0xff, 8 * (size_t)nq, st);
-    launch_fill_u64(W.f64key, nq, kNone64, st);
-    launch_fill_u64(W.resolve_out, nq, kNone64, st);
-    cudaMemsetAsync(W.overflow, 0, 4 * (size_t)nq, st);
-    if (stats) launch_cells_prefix(L, w, W.cells_prefix, st);
-    // S2: cascade bound for all pairs + per-query argmin-LB candidate
-    launch_series_stats(q, nq, L, W.qkim, st);
-    tm.mark();  // 1
+    // Phases (sharded search, dist.py): SEED = init + S2 bound + S3 seed round, leaving the state
+    // in ws; SEARCH = S3 compaction + S4/S5 survivors against the key passed in (the MIN over
+    // shards of the seed keys).  Neither flag: both, in one call.
+    const bool only_seed = (flags & NNDTW_CLASSIFY_PHASE_SEED) && !(flags & NNDTW_CLASSIFY_PHASE_SEARCH);
+    const bool only_search = (flags & NNDTW_CLASSIFY_PHASE_SEARCH) && !(flags & NNDTW_CLASSIFY_PHASE_SEED);
+    const bool do_seed = !only_search, do_search = !only_seed;
     const int keogh = (flags & NNDTW_CLASSIFY_BOUND_KEOGH) ? 1 : 0;
     const bool sym = (flags & NNDTW_CLASSIFY_BOUND_SYMMETRIC) != 0;
-    if (nt > 0 && launch_lb(q, nq, W.qkim, t, U, Lo, tkim, nt, L, w, v, 1, self_offset, W.lb,
-                            W.ldlb, sym ? nullptr : W.minkey, st, keogh))
-        return fail(NNDTW_E_ARG, "too many train series for one launch");
-    if (nt > 0 && sym) {  // second direction of the symmetric bound, then the seed argmin
-        launch_envelopes(q, nq, L, w, W.qU, W.qL, nullptr, st);
-        if (launch_lb(t, nt, nullptr, q, W.qU, W.qL, nullptr, nq, L, w, v, 0, -1, W.lb, W.ldlb,
-                      nullptr, st, keogh, 1))
-            return fail(NNDTW_E_ARG, "too many queries for one launch");
-        launch_row_argmin(W.lb, W.ldlb, nq, nt, W.minkey, st);
+    TieLog log{W.log, W.log_count, W.log_cap, W.overflow};
+    unsigned long long *cnt = stats ? W.counters : nullptr;
+
+    tm.mark();  // 0
+    if (do_seed) {
+        cudaMemsetAsync(W.counters, 0, sizeof(unsigned long long) * (CNT_N + 3), st);
+        launch_fill_u64(key, nq, kKeyInit, st);
+        cudaMemsetAsync(W.minkey, 0xff, 8 * (size_t)nq, st);
+        launch_fill_u64(W.f64key, nq, kNone64, st);
+        launch_fill_u64(W.resolve_out, nq, kNone64, st);
+        cudaMemsetAsync(W.overflow, 0, 4 * (size_t)nq, st);
+        launch_cells_prefix(L, w, W.cells_prefix, st);
+        launch_series_stats(q, nq, L, W.qkim, st);
+    }
+    tm.mark();  // 1
+    if (do_seed) {
+        // S2: cascade bound for all pairs + per-query argmin-LB candidate
+        if (nt > 0 && launch_lb(q, nq, W.qkim, t, U, Lo, tkim, nt, L, w, v, 1, self_offset,
+                                W.lb, W.ldlb, sym ? nullptr : W.minkey, st, keogh))
+            return fail(NNDTW_E_ARG, "too many train series for one launch");
+        if (nt > 0 && sym) {  // second direction of the symmetric bound, then the seed argmin
+            launch_envelopes(q, nq, L, w, W.qU, W.qL, nullptr, st);
+            if (launch_lb(t, nt, nullptr, q, W.qU, W.qL, nullptr, nq, L, w, v, 0, -1, W.lb,
+                          W.ldlb, nullptr, st, keogh, 1))
+                return fail(NNDTW_E_ARG, "too many queries for one launch");
+            launch_row_argmin(W.lb, W.ldlb, nq, nt, W.minkey, st);
+        }
     }
     tm.mark();  // 2
     if ((rc = cuda_fail("lb"))) return rc;
-    TieLog log{W.log, W.log_count, W.log_cap, W.overflow};
-    unsigned long long *cnt = stats ? W.counters : nullptr;
-    if (nt > 0) {
+    if (nt > 0 && do_seed) {
         // S3: seed round (argmin-LB candidate, plus seed2 if given)
         launch_seed_items(W.minkey, seed2, nq, nt, W.seed_items, W.seed_count, st);
         rc = dispatch_dtw(q, t, nq, nt, W.seed_items, W.seed_count, 2 * (unsigned long long)nq + 1,
                           nullptr, nullptr, 0, L, w, 0, key, index_base, eps_t, log, nullptr,
                           W.cells_prefix, nullptr, nullptr, st, sms);
         if ((rc = dtw_fail(rc, L, w))) return rc;
+    }
+    if (nt > 0 && do_search) {
         // S3: prune + compact the survivors against the seeded best-so-far
         launch_compact(W.lb, W.ldlb, nq, nt, key, W.minkey, seed2, eps_p, W.items,
                        W.main_count, W.item_cap, sms, st);
-        tm.mark();  // 3
+    }
+    tm.mark();  // 3
+    if (nt > 0 && do_search) {
         // S4/S5: DTW with early abandoning on the survivors
         rc = dispatch_dtw(q, t, nq, nt, W.items, W.main_count, W.item_cap, nullptr, nullptr, 0, L, w, 0,
                           key, index_base, eps_t, log, cnt, W.cells_prefix, nullptr, nullptr,
                           st, sms);
         if ((rc = dtw_fail(rc, L, w))) return rc;
     }
-    else {
-        tm.mark();  // 3
-    }
     tm.mark();  // 4
     if ((rc = cuda_fail("dtw"))) return rc;
-    if ((flags & NNDTW_CLASSIFY_EXACT) && nt > 0)
+    if ((flags & NNDTW_CLASSIFY_EXACT) && nt > 0 && do_search)
         exact_local(W, q, nq, t, nt, L, w, index_base, key, cnt, sms, st);
     tm.mark();  // 5
     if ((rc = cuda_fail("classify"))) return rc;
@@ -282,13 +294,18 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         unsigned long long h[CNT_N + 3];
         cudaMemcpyAsync(h, W.counters, sizeof h, cudaMemcpyDeviceToHost, st);
         if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_fail("classify sync");
-        stats->lb_pairs += nq * nt;
-        stats->survivors += (int64_t)h[CNT_N + 1];
-        stats->dtw_calls += (int64_t)h[CNT_ITEMS] + (int64_t)h[CNT_N];  // main + seed items
-        stats->dtw_abandoned += (int64_t)h[CNT_ABANDONED];
-        stats->cells += (int64_t)h[CNT_CELLS];
-        stats->near_tie_pairs += (int64_t)h[CNT_TIES];
-        stats->rounds += 2;
+        if (do_seed) {
+            stats->lb_pairs += nq * nt;
+            stats->rounds += 1;
+        }
+        if (do_search) {
+            stats->survivors += (int64_t)h[CNT_N + 1];
+            stats->dtw_calls += (int64_t)h[CNT_ITEMS] + (int64_t)h[CNT_N];  // main + seed items
+            stats->dtw_abandoned += (int64_t)h[CNT_ABANDONED];
+            stats->cells += (int64_t)h[CNT_CELLS];
+            stats->near_tie_pairs += (int64_t)h[CNT_TIES];
+            stats->rounds += 1;
+        }
         stats->launches += (int32_t)(launches_total() - launches0);
         if (outer_tm == nullptr) {
             stats->ms_lb += tm.ms(1, 2);

@@ -1,8 +1,12 @@
 """S6 -- train-set sharding over ranks (one process per GPU) with MIN-allreduce combines.
 
 The train set is split into contiguous index ranges, queries are replicated, and every rank
-runs S1-S5 on its shard (nndtw_classify without the EXACT flag).  Three int64 MIN all-reduces
-over NCCL (NVLink / NVSwitch) then give the exact answer:
+runs S1-S5 on its shard (nndtw_classify without the EXACT flag) in two phases: the seed phase
+(S2 bound, S3 seed DTW of each query's argmin-bound candidate) ends with an int64 MIN
+all-reduce of the seed keys, so that every shard prunes and abandons against the best seed of
+ALL shards (a valid upper bound on the global NN distance) instead of its own -- without it
+each shard's survivors grow as the shard shrinks.  Three more MIN all-reduces then give the
+exact answer:
 
 1. key   = (fp32 distance bits << 32) | global index  -> global fp32 best (reading C13);
 2. f64   = fp64 bits of each rank's near-tie candidates within the global fp32 best's band
@@ -36,6 +40,10 @@ class ShardOps:
     def local_keys(self, q):
         raise NotImplementedError
 
+    # optional two-phase form of local_keys (seed keys, MIN over ranks, then the search)
+    seed_keys = None
+    search_keys = None
+
     def refine(self, q, gkey):
         raise NotImplementedError
 
@@ -58,6 +66,20 @@ class GpuShardOps(ShardOps):
         self.last_stats = st
         return key
 
+    def seed_keys(self, q):
+        key, ws, st = nndtw.classify_keys(self.model, q, exact=False, stats=self.stats,
+                                          stream=self.stream, phase="seed")
+        self.ws = ws
+        self.last_stats = st
+        return key
+
+    def search_keys(self, q, gseed):
+        key, _, st = nndtw.classify_keys(self.model, q, exact=False, stats=self.stats,
+                                         stream=self.stream, phase="search", key=gseed,
+                                         ws=self.ws)
+        self.last_stats = nndtw.merge_stats(self.last_stats, st)
+        return key
+
     def refine(self, q, gkey):
         return nndtw.classify_refine(self.model, q, self.ws, gkey, self.stream)
 
@@ -68,7 +90,12 @@ class GpuShardOps(ShardOps):
 def combine(ops: ShardOps, q, group=None):
     """Run the 3-step exact combine; returns the final key tensor in key format 1
     ((global index << 32) | fp32 distance bits)."""
-    key = ops.local_keys(q)
+    if getattr(ops, "seed_keys", None) is not None:
+        key = ops.seed_keys(q)
+        dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)  # global seed best-so-far
+        key = ops.search_keys(q, key)
+    else:
+        key = ops.local_keys(q)
     dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
     f64 = ops.refine(q, key)
     dist.all_reduce(f64, op=dist.ReduceOp.MIN, group=group)

@@ -24,6 +24,8 @@ NNDTW_LB_KEOGH = 2
 NNDTW_CLASSIFY_EXACT = 1
 NNDTW_CLASSIFY_BOUND_KEOGH = 2
 NNDTW_CLASSIFY_BOUND_SYMMETRIC = 4
+NNDTW_CLASSIFY_PHASE_SEED = 8
+NNDTW_CLASSIFY_PHASE_SEARCH = 16
 KEY_INIT = 0x7F800000FFFFFFFF
 
 
@@ -275,26 +277,43 @@ class Model:
 
 
 def classify_keys(model: Model, q: torch.Tensor, exact: bool = True, self_offset: int = -1,
-                  stats: bool = False, stream=None):
-    """S2-S7 on one shard: returns (key int64 [nq], workspace, stats dict | None)."""
+                  stats: bool = False, stream=None, phase: str | None = None, key=None, ws=None):
+    """S2-S7 on one shard: returns (key int64 [nq], workspace, stats dict | None).
+
+    phase None runs everything; "seed" stops after the S3 seed round (keys = seed keys);
+    "search" continues from a "seed" call's workspace `ws` with `key` = the MIN over shards
+    of the seed keys (updated in place and returned)."""
     _series(q, "q")
     nq, L = q.shape
     if L != model.L:
         raise NNDTWError("query length differs from train length (unequal lengths are out of "
                          "scope, reading C15)")
-    ws = model.workspace(nq)
-    key = torch.empty(nq, dtype=torch.int64, device=q.device)
+    if phase == "search":
+        if ws is None or key is None:
+            raise NNDTWError("phase 'search' needs the seed call's ws and the combined key")
+    else:
+        ws = model.workspace(nq)
+        key = torch.empty(nq, dtype=torch.int64, device=q.device)
+    flags = ((NNDTW_CLASSIFY_EXACT if exact else 0) |
+             (NNDTW_CLASSIFY_BOUND_KEOGH if model.bound == "keogh" else 0) |
+             (NNDTW_CLASSIFY_BOUND_SYMMETRIC if model.symmetric else 0) |
+             {None: 0, "seed": NNDTW_CLASSIFY_PHASE_SEED,
+              "search": NNDTW_CLASSIFY_PHASE_SEARCH}[phase])
     st = Stats()
     _check(load().nndtw_classify(_ptr(q), nq, _ptr(model.t), _ptr(model.U), _ptr(model.Lo),
                                  _ptr(model.kim), model.t.shape[0], model.index_base,
-                                 int(self_offset), L, model.w, model.v,
-                                 (NNDTW_CLASSIFY_EXACT if exact else 0) |
-                                 (NNDTW_CLASSIFY_BOUND_KEOGH if model.bound == "keogh" else 0) |
-                                 (NNDTW_CLASSIFY_BOUND_SYMMETRIC if model.symmetric else 0),
+                                 int(self_offset), L, model.w, model.v, flags,
                                  _ptr(ws), ws.numel(),
                                  _ptr(key), C.byref(st) if stats else None, _stream(stream)),
            "nndtw_classify")
     return key, ws, (st.as_dict() if stats else None)
+
+
+def merge_stats(a: dict | None, b: dict | None) -> dict | None:
+    """Sum two stats dicts (the seed and search phases of one sharded call)."""
+    if a is None or b is None:
+        return a or b
+    return {k: a[k] + b[k] for k in a}
 
 
 def classify_refine(model: Model, q, ws, gkey, stream=None) -> torch.Tensor:

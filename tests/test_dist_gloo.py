@@ -80,20 +80,42 @@ class OracleShardOps:
         return torch.tensor(out, dtype=torch.int64)
 
 
-def _worker(rank, world, port, T, Q, w, jitter, ret):
+class OracleTwoPhaseShardOps(OracleShardOps):
+    """The two-phase form (GpuShardOps.seed_keys / search_keys): the seed key of each query is
+    the shard's argmin-bound candidate (LB_Kim -> LB_Enhanced cascade, oracle); the search
+    starts from the MIN over ranks of the seed keys -- possibly another rank's candidate, which
+    this rank's refine/resolve never see -- and keeps the smaller of it and the local best."""
+
+    def seed_keys(self, Q):
+        U, Lo = self.o.envelopes(self.T[self.lo:self.hi], self.w)
+        keys = []
+        for q in Q.numpy():
+            lbs = [self.o.lb_cascade(q, self.T[n], U[n - self.lo], Lo[n - self.lo], self.w, 5)
+                   for n in range(self.lo, self.hi)]
+            n = self.lo + int(np.argmin(lbs))
+            d = np.float32(self._d64(q, n))
+            keys.append((int(d.view(np.uint32)) << 32) | n)
+        return torch.tensor(keys, dtype=torch.int64)
+
+    def search_keys(self, Q, gseed):
+        local = self.local_keys(Q)
+        return torch.minimum(local, gseed)
+
+
+def _worker(rank, world, port, T, Q, w, jitter, ret, two_phase=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1808_09617_b200.dist import combine, shard_range
     lo, hi = shard_range(T.shape[0], rank, world)
-    ops = OracleShardOps(T, lo, hi, w, jitter)
+    ops = (OracleTwoPhaseShardOps if two_phase else OracleShardOps)(T, lo, hi, w, jitter)
     out = combine(ops, torch.as_tensor(Q))
     ret[rank] = [int(x) >> 32 for x in out]
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_combine_matches_global_nn(oracle_lib, world):
+@pytest.mark.parametrize("world,two_phase", [(2, False), (3, False), (2, True), (3, True)])
+def test_sharded_combine_matches_global_nn(oracle_lib, world, two_phase):
     rng = np.random.default_rng(world)
     L, w = 10, 2
     T = datagen.random_series(rng, 23, L, "int")
@@ -106,7 +128,8 @@ def test_sharded_combine_matches_global_nn(oracle_lib, world):
     mgr = mp.Manager()
     ret = mgr.dict()
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, T, Q, w, jitter, ret), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, T, Q, w, jitter, ret, two_phase), nprocs=world,
+             join=True)
     ridx, _ = oracle_lib.nn(Q, T, w, mode="exhaustive")
     for r in range(world):
         assert list(ret[r]) == list(ridx), (r, ret[r], ridx)

@@ -280,28 +280,44 @@ def test_loocv_config3_full_sampled(dev, oracle_lib):
 
 # ---------------------------------------------------------------- S6 shard protocol (1 GPU)
 @pytest.mark.parametrize("nshards", [2, 3])
-def test_shard_protocol_through_abi(dev, oracle_lib, nshards):
+@pytest.mark.parametrize("two_phase", [False, True])
+@pytest.mark.parametrize("data", ["int", "config1"])
+def test_shard_protocol_through_abi(dev, oracle_lib, nshards, two_phase, data):
     """The sharded path of dist.py through the real C ABI, shards run one after another on one
     GPU and combined with torch.minimum (= the int64 MIN all-reduce): refine and resolve must
-    give the exact global 1-NN, including exact ties split across shards."""
+    give the exact global 1-NN, including exact ties split across shards.  two_phase: the seed
+    keys are MIN-combined first and every shard searches from the global seed."""
     import torch
     from paper_1808_09617_b200 import nndtw
     from paper_1808_09617_b200.dist import shard_range
     rng = np.random.default_rng(nshards)
-    L, w, V = 64, 6, 5
-    Tr = datagen.random_series(rng, 300, L, "int")
-    Tr[250] = Tr[20]      # duplicates in different shards
-    Tr[299] = Tr[120]
-    Q = datagen.random_series(rng, 40, L, "int")
-    Q[0] = Tr[20]
-    Q[1] = Tr[120]
-    labels = rng.integers(0, 5, size=300).astype(np.int32)
+    if data == "int":
+        L, w, V, N = 64, 6, 5, 300
+        Tr = datagen.random_series(rng, N, L, "int")
+        Tr[250] = Tr[20]      # duplicates in different shards
+        Tr[299] = Tr[120]
+        Q = datagen.random_series(rng, 40, L, "int")
+        Q[0] = Tr[20]
+        Q[1] = Tr[120]
+        labels = rng.integers(0, 5, size=N).astype(np.int32)
+    else:  # config-1 shaped (pruning and abandoning at work)
+        ds = datagen.make_dataset(1, n_train=1000, n_test=60)
+        Tr, Q, labels = ds.train, ds.test, ds.train_labels
+        N, L, w, V = 1000, 256, 26, 5
     q = T(Q, dev)
     models = []
     for r in range(nshards):
-        lo, hi = shard_range(300, r, nshards)
+        lo, hi = shard_range(N, r, nshards)
         models.append(nndtw.Model(T(Tr[lo:hi], dev), T(labels[lo:hi], dev), w, V, index_base=lo))
-    outs = [nndtw.classify_keys(m, q, exact=False) for m in models]
+    if two_phase:
+        seeds = [nndtw.classify_keys(m, q, exact=False, phase="seed") for m in models]
+        gseed = seeds[0][0].clone()
+        for k, _, _ in seeds[1:]:
+            gseed = torch.minimum(gseed, k)
+        outs = [nndtw.classify_keys(m, q, exact=False, phase="search", key=gseed.clone(), ws=ws)
+                for m, (_, ws, _) in zip(models, seeds)]
+    else:
+        outs = [nndtw.classify_keys(m, q, exact=False) for m in models]
     gkey = outs[0][0].clone()
     for k, _, _ in outs[1:]:
         gkey = torch.minimum(gkey, k)
@@ -315,7 +331,7 @@ def test_shard_protocol_through_abi(dev, oracle_lib, nshards):
         g = torch.minimum(g, x)
     idx, lab, dist = nndtw.finalize(g, T(labels, dev), key_format=1)
     _check_nn(oracle_lib, Tr, labels, Q, w, idx.cpu().numpy(), lab.cpu().numpy(),
-              dist.cpu().numpy())
+              dist.cpu().numpy(), V=V)
 
 
 # ---------------------------------------------------------------- NEXT-1: LB_Keogh baseline
