@@ -191,9 +191,16 @@ def run_reference(args, cfg, ds, w, V):
 
 
 def config_json(cfg, w, V, gpus):
-    return {"workload": f"config{cfg.idx}_{cfg.name}", "n_train": cfg.n_train,
-            "n_test": cfg.n_test, "L": cfg.L, "w": w, "V": V, "classes": cfg.classes,
-            "l2": "inputs larger than L2 (4 GB LB matrix + 600 MB series/envelopes per step)",
+    n, q, L = cfg.n_train, cfg.n_test, cfg.L
+    lb_bytes = q * ((n + 3) // 4 * 4) * 4
+    ser_bytes = n * L * 4 * 3
+    big = lb_bytes + ser_bytes > 126 * 2 ** 20
+    return {"workload": f"config{cfg.idx}_{cfg.name}", "n_train": n, "n_test": q, "L": L,
+            "w": w, "V": V, "classes": cfg.classes,
+            "l2": (f"inputs larger than L2 ({lb_bytes / 1e9:.2f} GB bound matrix + "
+                   f"{ser_bytes / 1e6:.0f} MB series/envelopes per step)" if big else
+                   f"working set {(lb_bytes + ser_bytes) / 1e6:.0f} MB fits the 126 MB L2 "
+                   "(small config; not flushed)"),
             "parallelism": f"train-sharded x{gpus}, queries replicated, int64 MIN allreduce"}
 
 
@@ -372,10 +379,12 @@ def main():
     lb_peak = lb_pair_col_peak(num_sms, sm_mhz)
     dominant = "dtw" if acc_tot["ms_dtw"] >= acc_tot["ms_lb"] else "lb"
     traffic = ncu_traffic()
-    roof_dtw = {"kernel": "k_dtw_band (S4 survivor round)", "bound": "alu",
+    dtw_kernel = "k_dtw_band" if 2 * min(w, L - 1) + 2 <= 1024 else "k_dtw_strip"
+    roof_dtw = {"kernel": f"{dtw_kernel} (S4 survivor round)", "bound": "alu",
                 "achieved": dtw_gcups, "peak": peak_cells, "unit": "Gcells/s",
                 "frac": dtw_gcups / peak_cells if peak_cells else None,
-                "traffic": traffic.get("k_dtw_band", {}).get("bytes_per_launch"),
+                "traffic": traffic.get(dtw_kernel, {}).get("bytes_per_launch")
+                if args.config == 2 else None,
                 "peak_source": f"{num_sms} SMs x 64 cells/clk (FMNMX3 at 16 lanes/clk/SMSP, "
                                f"tools/pipebench.cu) x {sm_mhz:.0f} MHz ({src})",
                 "ms_per_step": acc_tot["ms_dtw"] / args.steps}
@@ -383,7 +392,8 @@ def main():
     roof_lb = {"kernel": "k_lb_tile (S2 cascade)", "bound": "alu", "achieved": lb_rate,
                "peak": lb_peak, "unit": "G pair-columns/s",
                "frac": lb_rate / lb_peak if lb_peak else None,
-               "traffic": traffic.get("k_lb_tile", {}).get("bytes_per_launch"),
+               "traffic": traffic.get("k_lb_tile", {}).get("bytes_per_launch")
+               if args.config == 2 else None,
                "hbm_gbs": (lb_bytes / (acc_tot["ms_lb"] / args.steps * 1e-3) / 1e9
                            if acc_tot["ms_lb"] > 0 else None),
                "peak_source": f"{num_sms} SMs x 42.7 pair-cols/clk (3 FMA-pipe ops each) x "
@@ -393,7 +403,8 @@ def main():
     env_gbs = env_bytes / (acc_env_ms / args.steps * 1e-3) / 1e9 if acc_env_ms > 0 else None
     roof_env = {"kernel": "k_envelopes (S1)", "bound": "hbm", "achieved": env_gbs, "peak": hbm,
                 "unit": "GB/s", "frac": env_gbs / hbm if env_gbs else None,
-                "traffic": traffic.get("k_envelopes", {}).get("bytes_per_launch"),
+                "traffic": traffic.get("k_envelopes", {}).get("bytes_per_launch")
+                if args.config == 2 else None,
                 "algorithmic_bytes": env_bytes,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
                 "ms_per_step": acc_env_ms / args.steps}

@@ -215,7 +215,8 @@ def test_loocv_reduced(dev, oracle_lib):
 
 # ---------------------------------------------------------------- S4 long windows (strip kernel)
 @pytest.mark.parametrize("L,ws", [(1024, (1023, 600, 515)), (2048, (2047, 1500)),
-                                  (700, (699, 520)), (1100, (1099,))])
+                                  (700, (699, 520)), (1100, (1099,)), (513, (512,)),
+                                  (3001, (3000, 2000))])
 def test_dtw_batch_long_windows(dev, oracle_lib, L, ws):
     from paper_1808_09617_b200 import nndtw
     rng = np.random.default_rng(L)
