@@ -98,6 +98,12 @@ __global__ void __launch_bounds__(352) k_dtw_band(BandParams p) {
 #pragma unroll
         for (int r = 0; r < R; ++r) sc[r] = pin_reg((g * R + r == skill) ? kInf : 1.0f);
     }
+    // general layout, packed: negated per-slot scales in pairs (2m, 2m+1) for the FFMA2 form
+    unsigned long long scn[(!ALIGNED && PACK) ? R / 2 : 1];
+    if (!ALIGNED && PACK) {
+#pragma unroll
+        for (int m = 0; m < R / 2; ++m) scn[m] = f2_pack(-sc[2 * m], -sc[2 * m + 1]);
+    }
     const float nbmask_lo = (g == 0) ? kInf : 0.0f;        // selects +inf at group edges
     const float nbmask_hi = (g == G - 1) ? kInf : 0.0f;
 
@@ -177,12 +183,14 @@ __global__ void __launch_bounds__(352) k_dtw_band(BandParams p) {
         float aw[R - 1];
 #pragma unroll
         for (int x = 0; x < R - 1; ++x) aw[x] = pa[x];
-        if (ALIGNED && PACK) {
+        if (PACK) {
             // Half-packed cells: on an even diagonal t, cell m reads (a[t/2-m+H-1], b[t/2+m]);
             // on t+1 the same slot index m reads the same a and b one further.  One FADD2 with
             // a broadcast operand gives both differences: (a, a) - (b[y], b[y+1]).  The b pairs
             // come in two register copies -- pairs starting at even y (be) and at odd y (bo) --
-            // loaded separately so that every pair is an aligned 64-bit register pair.
+            // loaded separately so that every pair is an aligned 64-bit register pair.  In the
+            // general layout (kill slot anywhere) the pair is one FFMA2 instead:
+            // (b[y], b[y+1]) - (a, a) * (sc[2m], sc[2m+1]) -- same square, kill scale folded in.
             unsigned long long be[H], bo[H > 1 ? H - 1 : 1];
 #pragma unroll
             for (int k = 0; k < H; ++k) be[k] = f2_pack(pb[2 * k], pb[2 * k + 1]);
@@ -196,7 +204,9 @@ __global__ void __launch_bounds__(352) k_dtw_band(BandParams p) {
                 for (int m = 0; m < H; ++m) {
                     const float a = aw[(t >> 1) - m + H - 1];
                     const int y = (t >> 1) + m;
-                    T[m] = f2_sub(f2_pack(a, a), (y & 1) ? bo[y >> 1] : be[y >> 1]);
+                    const unsigned long long bp = (y & 1) ? bo[y >> 1] : be[y >> 1];
+                    if (ALIGNED) T[m] = f2_sub(f2_pack(a, a), bp);
+                    else T[m] = f2_fma(f2_pack(a, a), scn[m], bp);
                 }
                 {  // diagonal t (even offsets r = 2m)
                     float nlo;
@@ -222,7 +232,7 @@ __global__ void __launch_bounds__(352) k_dtw_band(BandParams p) {
                         f2_unpack(T[m], t0, t1);
                         const float hi = (r == R - 1) ? nhi : D[r + 1];
                         const float v = fmaf(t1, t1, fminf(fminf(D[r], D[r - 1]), hi));
-                        D[r] = (r == R - 1) ? v * sc[0] : v;
+                        D[r] = (ALIGNED && r == R - 1) ? v * sc[0] : v;
                     }
                 }
             }
@@ -441,19 +451,20 @@ static int launch_band_t(BandParams &p, const BandChoice &c, cudaStream_t st, in
                                      : launch_band_t<RR, 2, false>(p, c, st, num_sms))  \
                : c.km == 1 ? (c.pack ? launch_band_t<RR, 1, true>(p, c, st, num_sms)    \
                                      : launch_band_t<RR, 1, false>(p, c, st, num_sms))  \
-                           : launch_band_t<RR, 0, false>(p, c, st, num_sms);
+                           : (c.pack ? launch_band_t<RR, 0, true>(p, c, st, num_sms)    \
+                                     : launch_band_t<RR, 0, false>(p, c, st, num_sms));
 
 int launch_dtw_band(BandParams p, cudaStream_t st, int num_sms) {
     BandChoice c = choose_band(p.w, p.L);
     if (c.R == 0) return -1;
     {
-        // Half-packed cells (measured, tools/band_sweep.sh): +7% at R=26, G=8 (config 2), but
-        // the packed kernel needs ~178 registers, so it loses wherever the unpacked one would
-        // run more than 8 warps per SM or the group is narrow.  Used for full-warp aligned
-        // layouts with wide slots whose shared memory already caps the SM at 8 warps.
+        // Half-packed cells (FADD2, or FFMA2 with the kill scale in the general layout): a
+        // measured choice per slot width (tools/pack_sweep.sh, profiles/pack_sweep_b200.txt):
+        // faster at R = 20, 22, 26 (config 2's R=26: 5.4 -> 7.1 Tcells/s), slower at
+        // R = 14, 18, 24, 28, 32 (instruction schedule; registers are alike), equal elsewhere.
         static const char *pk = getenv("NNDTW_PACK");
-        const bool rule = c.km == 2 && c.G >= 4 && c.R >= 24 && c.warps * c.ctas <= 8;
-        c.pack = c.km >= 1 && (pk ? pk[0] == '1' : rule);
+        const bool rule = c.R == 20 || c.R == 22 || c.R == 26;
+        c.pack = pk ? pk[0] == '1' : rule;
     }
     static const bool verbose = getenv("NNDTW_VERBOSE") != nullptr;
     if (verbose)
