@@ -579,7 +579,8 @@ int nndtw_loocv_window(const float *x, const int32_t *labels, int64_t n, int32_t
     if (nw < 0 || (nw > 0 && !windows)) return fail(NNDTW_E_ARG, "bad window list");
     if (q_begin < 0 || q_end < q_begin || q_end > n)
         return fail(NNDTW_E_ARG, "query range outside [0, n]");
-    if (n > 0 && (!x || !labels || !errors || !ws)) return fail(NNDTW_E_ARG, "null pointer");
+    if (n > 0 && nw > 0 && (!x || !labels || !errors || !ws))
+        return fail(NNDTW_E_ARG, "null pointer");
     for (int p = 0; p < nw; ++p)
         if (windows[p] < 0) return fail(NNDTW_E_WINDOW, "w must be >= 0");
     const int64_t nq = q_end - q_begin;

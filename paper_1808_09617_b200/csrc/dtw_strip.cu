@@ -223,9 +223,11 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
 template <int RR, bool MASK>
 static int launch_strip_t(StripParams &p, cudaStream_t st, int num_sms) {
     auto kern = k_dtw_strip<RR, MASK>;
-    const int warps = 4;
+    // up to 4 warps per CTA, fewer when the rows are long (L up to 8192: 66 KB per warp)
+    int warps = (int)((220 * 1024) / ((size_t)p.rowlen * sizeof(float)));
+    if (warps > 4) warps = 4;
+    if (warps < 1) return -2;
     size_t smem = (size_t)warps * p.rowlen * sizeof(float);
-    if (smem > 220 * 1024) return -2;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem);

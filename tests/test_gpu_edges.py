@@ -1,0 +1,99 @@
+"""Edge cases of the boundary on the GPU: empty inputs, the error codes of include/nndtw.h,
+and the maximum supported length (L = 8192) against the fp64 oracle."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import datagen
+
+from test_gpu_parity import T, _check_nn, assert_rel, dev  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+
+def test_empty_inputs(dev):
+    import torch
+    from paper_1808_09617_b200 import nndtw
+    L, w = 64, 6
+    e = torch.empty((0, L), dtype=torch.float32, device=dev)
+    x = T(datagen.random_series(np.random.default_rng(0), 5, L, "walk"), dev)
+    U, Lo, kim = nndtw.envelopes(e, w)
+    assert U.shape == (0, L) and kim.shape == (0, 4)
+    assert nndtw.lb_enhanced(e, x, *nndtw.envelopes(x, w)[:2], w, 5).shape == (0, 5)
+    Ux, Lx, kx = nndtw.envelopes(x, w)
+    assert nndtw.lb_enhanced(x, e, U, Lo, w, 5).shape == (5, 0)
+    assert nndtw.dtw_batch(e, e, w).shape == (0,)
+    lab = torch.zeros(5, dtype=torch.int32, device=dev)
+    pred = nndtw.classify(nndtw.Model(x, lab, w, 5), e)
+    assert pred.idx.shape == (0,)
+    # empty train set: no candidate -> index -1, label -1, distance +inf
+    pred = nndtw.classify(nndtw.Model(e, torch.zeros(0, dtype=torch.int32, device=dev), w, 5), x)
+    assert (pred.idx.cpu().numpy() == -1).all() and (pred.label.cpu().numpy() == -1).all()
+    assert np.isinf(pred.dist.cpu().numpy()).all()
+    err, nn, _ = nndtw.loocv_window(x, lab, [], v=5)
+    assert err.shape == (0,)
+
+
+def test_error_codes(dev):
+    import torch
+    from paper_1808_09617_b200 import nndtw
+    lib = nndtw.load()
+    st = nndtw._stream()
+    x = T(datagen.random_series(np.random.default_rng(1), 4, 32, "walk"), dev)
+    out = torch.empty(4, dtype=torch.float32, device=dev)
+    p = nndtw._ptr
+    # L < 2 (Algorithm 1 is not admissible at L = 1, reading C11), L > 8192
+    assert lib.nndtw_dtw_batch(p(x), p(x), None, None, 4, 1, 0, None, p(out), st) == 2
+    assert lib.nndtw_dtw_batch(p(x), p(x), None, None, 4, 9000, 0, None, p(out), st) == 2
+    # negative window, V < 1, null pointers, negative count
+    assert lib.nndtw_dtw_batch(p(x), p(x), None, None, 4, 32, -1, None, p(out), st) == 3
+    lb = torch.empty((4, 4), dtype=torch.float32, device=dev)
+    U, Lo, kim = nndtw.envelopes(x, 3)
+    assert lib.nndtw_lb_enhanced(p(x), 4, None, p(x), p(U), p(Lo), None, 4, 32, 3, 0, 0, p(lb),
+                                 4, st) == 4
+    assert lib.nndtw_lb_enhanced(p(x), 4, None, p(x), None, p(Lo), None, 4, 32, 3, 5, 0, p(lb),
+                                 4, st) == 1
+    assert lib.nndtw_dtw_batch(None, p(x), None, None, 4, 32, 3, None, p(out), st) == 1
+    assert lib.nndtw_dtw_batch(p(x), p(x), None, None, -1, 32, 3, None, p(out), st) == 1
+    # workspace too small
+    key = torch.empty(4, dtype=torch.int64, device=dev)
+    ws = torch.empty(16, dtype=torch.uint8, device=dev)
+    rc = lib.nndtw_classify(p(x), 4, p(x), p(U), p(Lo), p(kim), 4, 0, -1, 32, 3, 5, 1, p(ws),
+                            ws.numel(), p(key), None, st)
+    assert rc == 5
+    assert b"workspace" in lib.nndtw_last_error()
+    # the Python layer rejects non-finite input before any kernel (NaN is dropped by fminf)
+    bad = x.clone()
+    bad[1, 3] = float("nan")
+    with pytest.raises(nndtw.NNDTWError):
+        nndtw.Model(bad, torch.zeros(4, dtype=torch.int32, device=dev), 3, 5)
+
+
+@pytest.mark.parametrize("w", [0, 13, 1000, 8191])
+def test_max_length_dtw(dev, oracle_lib, w):
+    from paper_1808_09617_b200 import nndtw
+    L = 8192
+    rng = np.random.default_rng(w)
+    A = datagen.random_series(rng, 2, L, "walk")
+    B = datagen.random_series(rng, 2, L, "walk")
+    A = (A - A.mean(1, keepdims=True)) / A.std(1, keepdims=True)
+    B = (B - B.mean(1, keepdims=True)) / B.std(1, keepdims=True)
+    A, B = A.astype(np.float32), B.astype(np.float32)
+    out = nndtw.dtw_batch(T(A, dev), T(B, dev), w).cpu().numpy()
+    ref = np.array([oracle_lib.dtw(A[i], B[i], w) for i in range(2)])
+    assert_rel(out, ref, what=f"L=8192 w={w}")
+
+
+def test_max_length_classify(dev, oracle_lib):
+    from paper_1808_09617_b200 import nndtw
+    L, w = 8192, 8191
+    rng = np.random.default_rng(8)
+    Tr = datagen.random_series(rng, 6, L, "walk")
+    Tr[5] = Tr[1]
+    Q = np.concatenate([Tr[1:2], datagen.random_series(rng, 1, L, "walk")])
+    lab = np.arange(6, dtype=np.int32)
+    model = nndtw.Model(T(Tr, dev), T(lab, dev), w, 8)
+    pred = nndtw.classify(model, T(Q, dev))
+    _check_nn(oracle_lib, Tr, lab, Q, w, pred.idx.cpu().numpy(), pred.label.cpu().numpy(),
+              pred.dist.cpu().numpy(), V=8)
