@@ -379,5 +379,73 @@ def loocv_window(x: torch.Tensor, labels: torch.Tensor, windows, v: int = 5, q_b
     return errors, nn, (st.as_dict() if stats else None)
 
 
+class GraphedClassifier:
+    """classify() for a fixed (model, nq), captured once into a CUDA graph and replayed: the
+    ~25 launches of a call (bound, seeds, compaction, DTW, fp64 near-tie re-rank, decode)
+    become one graph launch.  For launch-bound small problems (BJ:configs[0], [1]).
+
+    `__call__(q)` copies q into the graph's static input and replays; the returned Prediction
+    tensors are the graph's static outputs (overwritten by the next call -- clone to keep).
+    Inputs are not NaN-checked inside the graph (check once with check_finite)."""
+
+    def __init__(self, model: Model, nq: int):
+        dev = model.t.device
+        self.model = model
+        self.q = torch.zeros((nq, model.L), dtype=torch.float32, device=dev)
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # warm-up: workspace, kernel attributes
+            classify(model, self.q, check=False)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.pred = classify(model, self.q, check=False)
+
+    def __call__(self, q: torch.Tensor) -> Prediction:
+        self.q.copy_(q, non_blocking=True)
+        self.graph.replay()
+        return self.pred
+
+
+class GraphedLoocv:
+    """loocv_window() over a fixed window list captured into one CUDA graph (101 windows x
+    ~25 launches -> one graph launch).  `__call__()` replays and returns the device errors
+    [nw] (static tensor, recomputed from zero on every replay)."""
+
+    def __init__(self, x: torch.Tensor, labels: torch.Tensor, windows, v: int = 5):
+        _series(x, "x")
+        n, L = x.shape
+        self.x = x
+        self.labels = labels.to(device=x.device, dtype=torch.int32).contiguous()
+        self.win = (C.c_int32 * len(windows))(*[int(w) for w in windows])
+        self.nw = len(windows)
+        self.v = int(v)
+        need = load().nndtw_loocv_workspace_bytes(n, L, 0, n)
+        self.ws = torch.empty(need, dtype=torch.uint8, device=x.device)
+        self.errors = torch.zeros(self.nw, dtype=torch.int64, device=x.device)
+        side = torch.cuda.Stream(device=x.device)
+        side.wait_stream(torch.cuda.current_stream(x.device))
+        with torch.cuda.stream(side):
+            self._run()
+        torch.cuda.current_stream(x.device).wait_stream(side)
+        torch.cuda.synchronize(x.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._run()
+
+    def _run(self):
+        n, L = self.x.shape
+        self.errors.zero_()
+        _check(load().nndtw_loocv_window(_ptr(self.x), _ptr(self.labels), n, L,
+                                         C.cast(self.win, C.c_void_p), self.nw, self.v, 0, n,
+                                         _ptr(self.ws), self.ws.numel(), _ptr(self.errors),
+                                         None, None, _stream()), "nndtw_loocv_window")
+
+    def __call__(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.errors
+
+
 def launch_count() -> int:
     return int(load().nndtw_launch_count())

@@ -97,3 +97,28 @@ def test_max_length_classify(dev, oracle_lib):
     pred = nndtw.classify(model, T(Q, dev))
     _check_nn(oracle_lib, Tr, lab, Q, w, pred.idx.cpu().numpy(), pred.label.cpu().numpy(),
               pred.dist.cpu().numpy(), V=8)
+
+
+def test_graphed_classify_and_loocv(dev, oracle_lib):
+    """CUDA-graph replay of classify / LOOCV gives the eager (and the oracle's) answers, replay
+    after replay, with new inputs copied into the static buffers."""
+    import torch
+    from paper_1808_09617_b200 import nndtw
+    ds = datagen.make_dataset(0)
+    w = ds.cfg.windows()[0]
+    model = nndtw.Model(T(ds.train, dev), T(ds.train_labels, dev), w, 5)
+    g = nndtw.GraphedClassifier(model, 50)
+    for part in (ds.test[:50], ds.test[50:100], ds.test[:50]):
+        pred = g(T(part, dev))
+        torch.cuda.synchronize()
+        _check_nn(oracle_lib, ds.train, ds.train_labels, part, w, pred.idx.cpu().numpy(),
+                  pred.label.cpu().numpy(), pred.dist.cpu().numpy())
+    x = T(ds.train[:80], dev)
+    lab = T(ds.train_labels[:80], dev)
+    wins = [0, 3, 13, 40, 127]
+    gl = nndtw.GraphedLoocv(x, lab, wins)
+    eager, _, _ = nndtw.loocv_window(x, lab, wins)
+    for _ in range(2):
+        assert np.array_equal(gl().cpu().numpy(), eager.cpu().numpy())
+    ref, _ = oracle_lib.loocv(ds.train[:80], ds.train_labels[:80], wins)
+    assert np.array_equal(eager.cpu().numpy(), ref)

@@ -51,7 +51,14 @@ def classify_cfg(ds, w, V, reps):
     st = pred.stats
     acc = float((pred.label.cpu().numpy() == ds.test_labels).mean())
     Q, N, L = ds.test.shape[0], ds.train.shape[0], ds.train.shape[1]
+    # S2-S7 only (envelopes precomputed), eager and as one CUDA-graph replay
+    model = nndtw.Model(tr, lab, w, V, check=False)
+    ms_s2, _ = timed(lambda: nndtw.classify(model, te, check=False), reps)
+    g = nndtw.GraphedClassifier(model, Q)
+    ms_graph, _ = timed(lambda: g(te), max(reps, 5))
     return {"Q": Q, "N": N, "L": L, "w": w, "V": V, "ms": ms, "queries_s": Q / (ms / 1e3),
+            "ms_s2s7": ms_s2, "ms_s2s7_graph": ms_graph,
+            "queries_s_graph": Q / (ms_graph / 1e3),
             "dtw_gcups": st["cells"] / (st["ms_dtw"] * 1e-3) / 1e9 if st["ms_dtw"] else 0,
             "ms_lb": st["ms_lb"], "ms_dtw": st["ms_dtw"], "ms_other": st["ms_other"],
             "survivor_frac": st["survivors"] / max(1, st["lb_pairs"]),
@@ -76,8 +83,11 @@ def main():
             ms, (err, _, st) = timed(lambda: nndtw.loocv_window(x, lab, wins, v=5, stats=True),
                                      max(1, args.reps - 1))
             e = err.cpu().numpy()
+            gl = nndtw.GraphedLoocv(x, lab, wins, v=5)
+            ms_g, _ = timed(gl, max(1, args.reps - 1))
             rows.append({"config": 3, "N": cfg.n_train, "L": cfg.L, "windows": len(wins),
-                         "ms": ms, "windows_s": len(wins) / (ms / 1e3),
+                         "ms": ms, "windows_s": len(wins) / (ms / 1e3), "ms_graph": ms_g,
+                         "windows_s_graph": len(wins) / (ms_g / 1e3),
                          "heldout_queries_s": len(wins) * cfg.n_train / (ms / 1e3),
                          "best_w": int(wins[int(np.argmin(e))]), "min_errors": int(e.min()),
                          "errors_first": e[:8].tolist(), "dtw_calls": st["dtw_calls"],
