@@ -610,7 +610,18 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
     p.dbg_na = na;
     p.dbg_nb = nb;
     if (w == 0) return launch_dtw_w0(p, st, num_sms);
-    if (band_supported(w, L)) {
+    // Full window (w = L-1): the band sweeps (w+1)(2L-1) slot-cells for L^2 cells (50% useful)
+    // while the row-strip kernel computes L^2 unmasked cells, so it wins when its strips are
+    // nearly full (measured: L=256, w=255: 1.9 -> 4.4 Tcells/s; L=300: 3.6 -> 4.4; L=384: 2.8 -> 5.1;
+    // L=128 (one half-empty strip): 2.6 -> 1.9, so the band stays there).
+    static const char *fs = getenv("NNDTW_FORCE_STRIP");  // experiments: 1 = strip, 0 = band
+    bool strip = false;
+    if (w >= L - 1) {
+        const int H = 32 * strip_rows_per_lane(L);
+        strip = (long long)((L + H - 1) / H) * H * 100 <= (long long)L * 112;  // <= 12% idle rows
+    }
+    if (fs) strip = fs[0] == '1';
+    if (band_supported(w, L) && !strip) {
         int rc = launch_dtw_band(p, st, num_sms);
         if (rc == 0) return 0;
     }

@@ -220,6 +220,22 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
     }
 }
 
+// Rows per lane: the strips cover ceil(L / 32RR) * 32RR rows; take the RR in {16, 12, 10, 8}
+// that wastes the fewest rows (ties: the larger RR, fewer strips).
+int strip_rows_per_lane(int L) {
+    int best = 8;
+    long long best_rows = -1;
+    for (int RR : {16, 12, 10, 8}) {
+        const long long H = 32LL * RR;
+        const long long rows = (L + H - 1) / H * H;
+        if (best_rows < 0 || rows < best_rows) {
+            best_rows = rows;
+            best = RR;
+        }
+    }
+    return best;
+}
+
 template <int RR, bool MASK>
 static int launch_strip_t(StripParams &p, cudaStream_t st, int num_sms) {
     auto kern = k_dtw_strip<RR, MASK>;
@@ -271,12 +287,21 @@ int launch_dtw_strip(const float *A, const float *B, const Item *items,
     p.rowlen = (L + 2 * STRIP_PAD) + (L + 33);
     p.rowlen = (p.rowlen + 3) / 4 * 4;
     const bool mask = w < L - 1;
-    if (L >= 1024) {
-        return mask ? launch_strip_t<16, true>(p, st, num_sms)
-                    : launch_strip_t<16, false>(p, st, num_sms);
+    const int RR = strip_rows_per_lane(L);
+    switch (RR) {
+        case 16:
+            return mask ? launch_strip_t<16, true>(p, st, num_sms)
+                        : launch_strip_t<16, false>(p, st, num_sms);
+        case 12:
+            return mask ? launch_strip_t<12, true>(p, st, num_sms)
+                        : launch_strip_t<12, false>(p, st, num_sms);
+        case 10:
+            return mask ? launch_strip_t<10, true>(p, st, num_sms)
+                        : launch_strip_t<10, false>(p, st, num_sms);
+        default:
+            return mask ? launch_strip_t<8, true>(p, st, num_sms)
+                        : launch_strip_t<8, false>(p, st, num_sms);
     }
-    return mask ? launch_strip_t<8, true>(p, st, num_sms)
-                : launch_strip_t<8, false>(p, st, num_sms);
 }
 
 }  // namespace nndtw

@@ -66,6 +66,7 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
                  unsigned long long *counters, const long long *cells_prefix,
                  const float *cutoff, float *out, cudaStream_t st, int num_sms);
 
+int strip_rows_per_lane(int L);
 int launch_dtw_strip(const float *A, const float *B, const Item *items,
                      const unsigned long long *nitems_dev, unsigned long long item_cap,
                      const int32_t *ia, const int32_t *ib, int64_t nitems_host, int L, int w,
