@@ -216,6 +216,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-queries", type=int, default=0)
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the sharded path (NCCL process group, seed exchange, 3-step MIN "
+                         "combine) even at N=1 -- exercises the N>1 code on one GPU")
     args = ap.parse_args()
 
     cfg = datagen.CONFIGS[args.config]
@@ -236,8 +239,12 @@ def main():
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    sharded = world > 1 or args.sharded
+    if sharded:
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29513")
+            dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     if rank == 0:
         nbuild.build()
     if world > 1:
@@ -270,7 +277,7 @@ def main():
         if stats:
             ev[1].record(stream)
             env_ev.append(ev)
-        if world == 1:
+        if not sharded:
             pred = nndtw.classify(model, test_d, stats=stats, check=False)
         else:
             pred = classify_sharded(model, test_d, labels_d, stats=stats)
@@ -333,7 +340,7 @@ def main():
             te = test_h.to(dev, non_blocking=True)
             lb_ = labels_h.to(dev, non_blocking=True)
             model = nndtw.Model(tr, lb_[lo:hi], w, V, index_base=lo)
-            if world == 1:
+            if not sharded:
                 pred = nndtw.classify(model, te)
             else:
                 pred = classify_sharded(model, te, lb_)
@@ -361,7 +368,7 @@ def main():
                "d2h_bytes_per_step": d2h}
 
     if rank != 0:
-        if world > 1:
+        if sharded:
             dist.barrier()
             dist.destroy_process_group()
         return
@@ -425,7 +432,7 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_oracle(ds, w, V)
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.barrier()
         dist.destroy_process_group()
 
