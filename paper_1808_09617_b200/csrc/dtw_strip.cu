@@ -36,7 +36,8 @@ struct StripParams {
     const long long *cells_prefix;
     const float *cutoff;
     float *out;
-    int rowlen;  // floats per warp region: (L + 2*PAD) for B, then L + 1 for the row buffer
+    int rowlen;  // floats per warp region: (L + 2*PAD) for B, L + 33 for the row buffer,
+                 // then ceil(L/32) block suffix minima of the row buffer
 };
 
 template <int RR, bool MASK>
@@ -46,6 +47,7 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
     const int warp = threadIdx.x >> 5;
     const int L = p.L, w = p.w;
     float *sB = smem_s + (size_t)warp * p.rowlen;           // B[j] at sB[PAD + j]
+    float *bsuf = sB + (L + 2 * STRIP_PAD) + (L + 33);       // [ceil(L/32)]
     float *rb = sB + (L + 2 * STRIP_PAD);                    // rb[1 + j] = row above, column j
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -88,6 +90,7 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
         float res = kInf;
         bool abandoned = false;
         int strips_done = 0;
+        long long partial_cells = 0;  // cells of a strip left at a mid-strip checkpoint
         for (int st = 0; st < nstrips; ++st) {
             const int i0 = st * H + lane * RR;  // first row of this lane
             float a[RR], Dl[RR];
@@ -97,7 +100,29 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
                 a[r] = i < L ? __ldg(ga + i) : 0x1p64f * 3.0f;  // rows past the end: +inf cells
                 Dl[r] = kInf;                                    // D(i, -1) = +inf
             }
-            // the live best-so-far, used for the abandon test at the end of this strip
+            // Block suffix minima of the row above (the previous strip's bottom row):
+            // bsuf[m] = min over columns >= 32m.  With the lanes' frontier they form a cut of
+            // every warping path at any step of the strip (see the checkpoint below).
+            {
+                const int nblk = (L + 31) >> 5;
+                float carry = kInf;
+                for (int k0 = ((nblk - 1) >> 5) << 5; k0 >= 0; k0 -= 32) {
+                    const int m = k0 + lane;
+                    float bm = kInf;
+                    if (m < nblk)
+                        for (int j = 32 * m; j < 32 * m + 32 && j < L; ++j) bm = fminf(bm, rb[1 + j]);
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const float o = __shfl_down_sync(0xffffffffu, bm, off);
+                        if (lane + off < 32) bm = fminf(bm, o);
+                    }
+                    bm = fminf(bm, carry);
+                    if (m < nblk) bsuf[m] = bm;
+                    carry = __shfl_sync(0xffffffffu, bm, 0);
+                }
+                __syncwarp();
+            }
+            // the live best-so-far, used for the abandon tests of this strip
             float thr = thr_batch;
             if (p.mode == 0) thr = key_dist(ld_relaxed_u64(p.key + a_idx)) * (1.0f + p.eps_t);
             float up_prev = (lane == 0) ? rb[0] : kInf;  // diagonal input of the top row
@@ -147,9 +172,55 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
             const int s_lo = has_steady ? 31 : nsteps, s_hi = has_steady ? L - 1 : nsteps;
             for (int s = 0; s < s_lo; ++s) step(s, std::true_type{});
             int s = s_lo;
+            bool cut_abandon = false;
             for (; s + 1 < s_hi; s += 2) {
+                if ((s & 31) == 31 && s > 31) {
+                    // Checkpoint: lane l has computed columns <= s-1-l.  Every warping path
+                    // crosses the set {each lane's current column cells, the previous-column
+                    // bottom cell of the lane above (up_prev), lane 31's bottom row so far,
+                    // the previous strip's bottom row from column s-1 on}; D is non-decreasing
+                    // along paths, so its minimum is a lower bound of the distance (reading
+                    // C14).  bsuf[s/32] covers columns >= s-31 (a superset: still a bound).
+                    float mv = up_prev;
+#pragma unroll
+                    for (int r = 0; r < RR; ++r) mv = fminf(mv, Dl[r]);
+                    if (lane == 31) mv = fminf(mv, rowmin);
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1)
+                        mv = fminf(mv, __shfl_xor_sync(0xffffffffu, mv, off));
+                    mv = fminf(mv, bsuf[s >> 5]);
+                    float th = thr_batch;
+                    if (p.mode == 0) th = key_dist(ld_relaxed_u64(p.key + a_idx)) * (1.0f + p.eps_t);
+                    th = __shfl_sync(0xffffffffu, th, 0);  // one view of the live best per warp
+                    if (!(mv <= th)) {
+                        cut_abandon = true;
+                        break;
+                    }
+                }
                 step(s, std::false_type{});
                 step(s + 1, std::false_type{});
+            }
+            if (cut_abandon) {
+                // in-band cells of the complete strips plus this strip's computed columns
+                if (p.counters) {
+                    long long c = 0;
+#pragma unroll
+                    for (int r = 0; r < RR; ++r) {
+                        const int i = i0 + r;
+                        const int jmax = s - 1 - lane;  // last column computed by this lane
+                        if (i < L && jmax >= 0) {
+                            const int lo = i - w > 0 ? i - w : 0;
+                            int hi = i + w < L - 1 ? i + w : L - 1;
+                            hi = hi < jmax ? hi : jmax;
+                            c += hi >= lo ? hi - lo + 1 : 0;
+                        }
+                    }
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+                    partial_cells = c;
+                }
+                abandoned = true;
+                break;
             }
             for (; s < s_hi; ++s) step(s, std::false_type{});
             for (s = s_hi; s < nsteps; ++s) step(s, std::true_type{});
@@ -207,7 +278,7 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
                     long long s1 = t * (t - 1) / 2 + t * (long long)w + (R - t) * (L - 1);
                     long long m = R - 1 - w;
                     long long s2 = m > 0 ? m * (m + 1) / 2 : 0;
-                    c = s1 - s2 + R;
+                    c = s1 - s2 + R + partial_cells;
                 }
                 my_cells += c;
             }
@@ -284,7 +355,7 @@ int launch_dtw_strip(const float *A, const float *B, const Item *items,
     p.cells_prefix = cells_prefix;
     p.cutoff = cutoff;
     p.out = out;
-    p.rowlen = (L + 2 * STRIP_PAD) + (L + 33);
+    p.rowlen = (L + 2 * STRIP_PAD) + (L + 33) + (L + 31) / 32;
     p.rowlen = (p.rowlen + 3) / 4 * 4;
     const bool mask = w < L - 1;
     const int RR = strip_rows_per_lane(L);
