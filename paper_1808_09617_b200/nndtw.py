@@ -346,12 +346,35 @@ def finalize(key, labels, key_format: int = 0, stream=None):
     return idx, lab, dist
 
 
+WORKSPACE_BUDGET = 48 << 30  # bytes of classify workspace per call before queries are blocked
+
+
 def classify(model: Model, q: torch.Tensor, stats: bool = False, check: bool = True,
-             stream=None) -> Prediction:
-    """Exact 1-NN of every query (single GPU / single shard, fp64-exact tie resolution)."""
+             stream=None, workspace_budget: int | None = None) -> Prediction:
+    """Exact 1-NN of every query (single GPU / single shard, fp64-exact tie resolution).
+
+    The workspace holds the bound matrix and a worst-case survivor list (12 bytes per
+    (query, train) pair); when that exceeds `workspace_budget` (default 48 GB of the B200's
+    180 GB) the queries are processed in blocks -- queries are independent, the answer is
+    the same."""
     if check and not check_finite(q, stream):
         raise NNDTWError("queries contain NaN or infinity")
-    key, _, st = classify_keys(model, q, exact=True, stats=stats, stream=stream)
+    budget = WORKSPACE_BUDGET if workspace_budget is None else int(workspace_budget)
+    nq = q.shape[0]
+    nt = model.t.shape[0]
+    blk = nq
+    lib = load()
+    while blk > 1 and lib.nndtw_classify_workspace_bytes(blk, nt, model.L, model.w) > budget:
+        blk = (blk + 1) // 2
+    if blk >= nq:
+        key, _, st = classify_keys(model, q, exact=True, stats=stats, stream=stream)
+    else:
+        keys, st = [], None
+        for i in range(0, nq, blk):
+            k, _, s = classify_keys(model, q[i:i + blk], exact=True, stats=stats, stream=stream)
+            keys.append(k)
+            st = merge_stats(st, s) if stats else None
+        key = torch.cat(keys)
     idx, lab, dist = finalize(key, model.labels, 0, stream)
     return Prediction(idx, lab, dist, st)
 

@@ -122,3 +122,15 @@ def test_graphed_classify_and_loocv(dev, oracle_lib):
         assert np.array_equal(gl().cpu().numpy(), eager.cpu().numpy())
     ref, _ = oracle_lib.loocv(ds.train[:80], ds.train_labels[:80], wins)
     assert np.array_equal(eager.cpu().numpy(), ref)
+
+
+def test_classify_query_blocking(dev, oracle_lib):
+    """A small workspace budget forces query blocks; the answer is unchanged."""
+    from paper_1808_09617_b200 import nndtw
+    ds = datagen.make_dataset(0)
+    w = ds.cfg.windows()[0]
+    model = nndtw.Model(T(ds.train, dev), T(ds.train_labels, dev), w, 5)
+    pred = nndtw.classify(model, T(ds.test, dev), stats=True, workspace_budget=400_000)
+    assert pred.stats["lb_pairs"] == 100 * 100
+    _check_nn(oracle_lib, ds.train, ds.train_labels, ds.test, w, pred.idx.cpu().numpy(),
+              pred.label.cpu().numpy(), pred.dist.cpu().numpy())
