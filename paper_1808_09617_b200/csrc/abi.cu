@@ -98,6 +98,7 @@ struct ClassifyWs {
     unsigned *tiecnt;
     float *lb;
     int64_t ldlb;
+    unsigned long long *buckets;  // survivor-order buckets: count | base | fill
     Item *seed_items;
     Item *items;
     unsigned long long item_cap;
@@ -130,6 +131,7 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
     W.tiecnt = (unsigned *)take(4 * q1);
     W.ldlb = (nt + 3) / 4 * 4;
     W.lb = (float *)take(sizeof(float) * (size_t)nq * (size_t)W.ldlb);
+    W.buckets = (unsigned long long *)take(sizeof(unsigned long long) * 3 * NBUCKET);
     W.seed_items = (Item *)take(sizeof(Item) * (2 * q1 + 1));
     W.item_cap = (unsigned long long)nq * (unsigned long long)nt + 1;
     W.items = (Item *)take(sizeof(Item) * (size_t)W.item_cap);
@@ -274,7 +276,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     if (nt > 0 && do_search) {
         // S3: prune + compact the survivors against the seeded best-so-far
         launch_compact(W.lb, W.ldlb, nq, nt, key, W.minkey, seed2, eps_p, W.items,
-                       W.main_count, W.item_cap, sms, st);
+                       W.main_count, W.buckets, W.item_cap, sms, st);
     }
     tm.mark();  // 3
     if (nt > 0 && do_search) {

@@ -130,10 +130,16 @@ __device__ __forceinline__ void cp_async_wait_group1() {
 }
 
 // ---- work items ---------------------------------------------------------------------------
-// A DTW work item: query (row of A) and train (row of B), local indices.
+// A DTW work item: query (row of A), train (row of B), local indices, and the pair's cascade
+// bound (survivor items are skipped at fetch time when it exceeds the live best-so-far).
 struct Item {
     unsigned q, n;
+    float lb;
 };
+
+// Survivor order (S3/S4): LB / bsf_seed buckets, visited in ascending order so that every query's
+// most promising candidates run first and later ones meet a tightened best-so-far.
+constexpr int NBUCKET = 16;
 
 // near-tie log entry (S7): completed candidate within the band of the live best at the time
 struct TieEntry {
@@ -152,6 +158,6 @@ struct TieLog {
 
 // Per-call device counters (stats); index meaning below.
 enum { CNT_ITEMS = 0, CNT_ABANDONED = 1, CNT_CELLS = 2, CNT_SURVIVORS = 3, CNT_TIES = 4,
-       CNT_N = 8 };
+       CNT_SKIPPED = 5, CNT_N = 8 };
 
 }  // namespace nndtw

@@ -36,6 +36,7 @@ struct BandParams {
     unsigned long long *key;
     int64_t index_base;
     float eps_t;
+    float eps_p;                          // search mode: skip items with lb > bsf*(1+eps_p)
     TieLog log;
     unsigned long long *counters;         // nullable
     const long long *cells_prefix;        // [2L-1], nullable iff counters null
@@ -123,12 +124,23 @@ __global__ void __launch_bounds__(352) k_dtw_band(BandParams p) {
     float thr_batch = kInf;
     long long my_items = 0, my_aband = 0, my_cells = 0;
 
+    // Search mode: an item whose bound exceeds its query's live best-so-far (prune margin as
+    // in S3) is skipped -- survivors arrive in LB-bucket order, so later ones often meet a
+    // best-so-far already tightened by the earlier (lower-bound) candidates of their query.
+    // The best-so-far load overlaps the row copies; a skipped item starts with an all-+inf
+    // state, so the period's cut test retires it after one period (no extra control flow in
+    // the hot loop).
+    bool skipping = false;
+    long long my_skipped = 0;
+    unsigned long long kstart = 0;
     auto setup = [&]() {
         unsigned a_idx, b_idx;
+        float ilb = 0.0f;
         if (p.mode == 0) {
             Item itm = p.items[it];
             a_idx = itm.q;
             b_idx = itm.n;
+            ilb = itm.lb;
         } else {
             a_idx = p.ia ? (unsigned)p.ia[it] : (unsigned)it;
             b_idx = p.ib ? (unsigned)p.ib[it] : (unsigned)it;
@@ -163,9 +175,15 @@ __global__ void __launch_bounds__(352) k_dtw_band(BandParams p) {
                 bulk_prefetch_l2(p.B + (int64_t)nb * L, (unsigned)L * 4u);
             }
         }
+        if (p.mode == 0) kstart = ld_relaxed_u64(p.key + a_idx);
         cp_async_wait_all();
+        skipping = false;
+        if (p.mode == 0) {
+            // (all lanes of the group read the same address in one instruction)
+            skipping = ilb > key_dist(kstart) * (1.0f + p.eps_p);
+        }
 #pragma unroll
-        for (int r = 0; r < R; ++r) D[r] = (g == g0 && r == r0) ? 0.0f : kInf;
+        for (int r = 0; r < R; ++r) D[r] = (!skipping && g == g0 && r == r0) ? 0.0f : kInf;
         per = 0;
     };
 
@@ -174,7 +192,7 @@ __global__ void __launch_bounds__(352) k_dtw_band(BandParams p) {
 
     // live best-so-far of the group's query, read one period ahead (the abandon test uses the
     // value loaded during the previous period: never tighter than the true live value)
-    unsigned long long kprev = (p.mode == 0 && active) ? ld_relaxed_u64(p.key + qcur) : 0ull;
+    unsigned long long kprev = kstart;
     while (__any_sync(0xffffffffu, active)) {
         unsigned long long knext = 0;
         if (p.mode == 0 && active) knext = ld_relaxed_u64(p.key + qcur);
@@ -319,17 +337,21 @@ __global__ void __launch_bounds__(352) k_dtw_band(BandParams p) {
             if (abandon && p.mode == 1 && g == 0) p.out[it] = kInf;
             if (done || abandon) {
                 if (g == 0 && p.counters != nullptr) {
-                    int klast = p.k0 + per * R - 1;
-                    if (klast > 2 * L - 2) klast = 2 * L - 2;
-                    my_items += 1;
-                    my_aband += abandon ? 1 : 0;
-                    my_cells += klast >= 0 ? p.cells_prefix[klast] : 0;
+                    if (skipping) {
+                        my_skipped += 1;
+                    } else {
+                        int klast = p.k0 + per * R - 1;
+                        if (klast > 2 * L - 2) klast = 2 * L - 2;
+                        my_items += 1;
+                        my_aband += abandon ? 1 : 0;
+                        my_cells += klast >= 0 ? p.cells_prefix[klast] : 0;
+                    }
                 }
                 it += ngroups;
                 active = it < nitems;
                 if (active) {
                     setup();
-                    if (p.mode == 0) kprev = ld_relaxed_u64(p.key + qcur);
+                    kprev = kstart;
                 } else {
                     per = 0;  // idle groups replay period 0 (stay in bounds)
                 }
@@ -337,6 +359,8 @@ __global__ void __launch_bounds__(352) k_dtw_band(BandParams p) {
         }
         __syncwarp();
     }
+    if (p.counters != nullptr && valid_lane && g == 0 && my_skipped > 0)
+        atomicAdd(p.counters + CNT_SKIPPED, (unsigned long long)my_skipped);
     if (p.counters != nullptr && valid_lane && g == 0 && my_items > 0) {
         atomicAdd(p.counters + CNT_ITEMS, (unsigned long long)my_items);
         atomicAdd(p.counters + CNT_ABANDONED, (unsigned long long)my_aband);
@@ -526,6 +550,12 @@ __global__ void __launch_bounds__(256) k_dtw_w0(BandParams p) {
             Item itm = p.items[it];
             a_idx = itm.q;
             b_idx = itm.n;
+            float live = key_dist(ld_relaxed_u64(p.key + a_idx));
+            live = __shfl_sync(0xffffffffu, live, 0);
+            if (itm.lb > live * (1.0f + p.eps_p)) {  // pruned by the live best-so-far
+                if (lane == 0 && p.counters) atomicAdd(p.counters + CNT_SKIPPED, 1ull);
+                continue;
+            }
         } else {
             a_idx = p.ia ? (unsigned)p.ia[it] : (unsigned)it;
             b_idx = p.ib ? (unsigned)p.ib[it] : (unsigned)it;
@@ -602,6 +632,11 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
     p.key = key;
     p.index_base = index_base;
     p.eps_t = eps_t;
+    p.eps_p = eps_prune(L);
+    {
+        static const char *ns = getenv("NNDTW_NO_SKIP");  // experiments: no live-bsf skip
+        if (ns && ns[0] == '1') p.eps_p = kInf;
+    }
     p.log = log;
     p.counters = counters;
     p.cells_prefix = cells_prefix;

@@ -31,6 +31,7 @@ struct StripParams {
     unsigned long long *key;
     int64_t index_base;
     float eps_t;
+    float eps_p;  // search mode: skip items with lb > bsf*(1+eps_p)
     TieLog log;
     unsigned long long *counters;
     const long long *cells_prefix;
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
     const int H = 32 * RR;
     const int nstrips = (L + H - 1) / H;
     const int nsteps = L + 31;
-    long long my_items = 0, my_aband = 0, my_cells = 0;
+    long long my_items = 0, my_aband = 0, my_cells = 0, my_skipped = 0;
 
     for (int64_t it = gw; it < nitems; it += nwarps) {
         unsigned a_idx, b_idx;
@@ -73,6 +74,12 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
             Item itm = p.items[it];
             a_idx = itm.q;
             b_idx = itm.n;
+            float live = key_dist(ld_relaxed_u64(p.key + a_idx));
+            live = __shfl_sync(0xffffffffu, live, 0);
+            if (itm.lb > live * (1.0f + p.eps_p)) {  // pruned by the live best-so-far
+                ++my_skipped;
+                continue;
+            }
         } else {
             a_idx = p.ia ? (unsigned)p.ia[it] : (unsigned)it;
             b_idx = p.ib ? (unsigned)p.ib[it] : (unsigned)it;
@@ -284,6 +291,8 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
             }
         }
     }
+    if (p.counters && lane == 0 && my_skipped > 0)
+        atomicAdd(p.counters + CNT_SKIPPED, (unsigned long long)my_skipped);
     if (p.counters && lane == 0 && my_items > 0) {
         atomicAdd(p.counters + CNT_ITEMS, (unsigned long long)my_items);
         atomicAdd(p.counters + CNT_ABANDONED, (unsigned long long)my_aband);
@@ -350,6 +359,7 @@ int launch_dtw_strip(const float *A, const float *B, const Item *items,
     p.key = key;
     p.index_base = index_base;
     p.eps_t = eps_t;
+    p.eps_p = eps_prune(L);
     p.log = log;
     p.counters = counters;
     p.cells_prefix = cells_prefix;

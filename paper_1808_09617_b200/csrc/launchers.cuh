@@ -27,7 +27,8 @@ int launch_seed_items(const unsigned long long *minkey, const int32_t *seed2, in
 int launch_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
                    const unsigned long long *key, const unsigned long long *minkey,
                    const int32_t *seed2, float eps_p, Item *items, unsigned long long *count,
-                   unsigned long long capacity, int num_sms, cudaStream_t st);
+                   unsigned long long *buckets, unsigned long long capacity, int num_sms,
+                   cudaStream_t st);
 int launch_cells_prefix(int L, int w, long long *prefix, cudaStream_t st);
 int launch_refine(TieEntry *e, const unsigned long long *count, unsigned long long cap,
                   const float *A, const float *B, int L, int w, const unsigned long long *gkey,

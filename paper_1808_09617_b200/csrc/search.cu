@@ -1,5 +1,7 @@
 // search.cu -- S3 (seed, prune, compaction), S5 (per-query argmin decode), S7 (fp64 near-tie
 // re-rank) and S8 bookkeeping kernels.
+#include <cstdlib>
+
 #include "launchers.cuh"
 
 namespace nndtw {
@@ -29,13 +31,13 @@ __global__ void k_seed_items(const unsigned long long *minkey, const int32_t *se
     unsigned n1 = (unsigned)(k & 0xffffffffull);
     if (k != kNone && n1 < (unsigned)nt) {
         unsigned long long pos = atomicAdd(count, 1ull);
-        items[pos] = Item{(unsigned)q, n1};
+        items[pos] = Item{(unsigned)q, n1, 0.0f};
     }
     if (seed2 != nullptr) {
         int n2 = seed2[q];
         if (n2 >= 0 && n2 < nt && (unsigned)n2 != n1) {
             unsigned long long pos = atomicAdd(count, 1ull);
-            items[pos] = Item{(unsigned)q, (unsigned)n2};
+            items[pos] = Item{(unsigned)q, (unsigned)n2, 0.0f};
         }
     }
 }
@@ -49,94 +51,131 @@ int launch_seed_items(const unsigned long long *minkey, const int32_t *seed2, in
     return 0;
 }
 
-// ---- S3 compaction: surviving pairs LB <= bsf*(1+eps_p), compacted with ballot/popc ----------
+// ---- S3 compaction: surviving pairs LB <= bsf*(1+eps_p), in LB-bucket order -------------------
 // One CTA-tile = (query q, CT_N consecutive train indices), 16 consecutive ones per thread (4
-// float4 loads), so the items leave in train-index order within the tile.  Survivor counts are scanned within the warp (shuffles) and across the
-// CTA's warps (shared memory), so there is one atomicAdd on the global item counter per tile --
-// a per-warp atomic on that single address serialised the kernel at ~8M atomics per step.
+// float4 loads).  A survivor's bucket is floor(NBUCKET * LB / thr) (thr = the query's seeded
+// best-so-far with the prune margin).  PASS 0 counts survivors per bucket (a shared-memory
+// histogram per tile, one global atomic per bucket and tile); k_bucket_scan turns the counts
+// into bucket offsets; PASS 1 reserves a contiguous run per bucket and tile and scatters the
+// items, so the item list is bucket-major (and query-major inside a bucket): every query's
+// lowest-bound candidates are processed first, across all queries at once.
 constexpr int CT_N = 4096;
 
+template <int PASS>
 __global__ void __launch_bounds__(256) k_compact(const float *__restrict__ lb, int64_t ldlb,
                                                  int64_t nq, int64_t nt,
                                                  const unsigned long long *__restrict__ key,
                                                  const unsigned long long *__restrict__ minkey,
                                                  const int32_t *__restrict__ seed2, float eps_p,
                                                  Item *__restrict__ items,
-                                                 unsigned long long *count,
-                                                 unsigned long long capacity) {
-    __shared__ int wsum[8];
-    __shared__ unsigned long long sbase;
+                                                 unsigned long long *bucket_count,
+                                                 const unsigned long long *bucket_base,
+                                                 unsigned long long *bucket_fill,
+                                                 unsigned long long capacity, int one_bucket) {
+    __shared__ unsigned hist[NBUCKET];
+    __shared__ unsigned long long base[NBUCKET];
     const int64_t tiles_per_row = (nt + CT_N - 1) / CT_N;
     const int64_t ntiles = tiles_per_row * nq;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool vec = (ldlb & 3) == 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (threadIdx.x < NBUCKET) hist[threadIdx.x] = 0u;
+        __syncthreads();
         const int64_t q = tile / tiles_per_row;
         const int64_t nbase = (tile % tiles_per_row) * CT_N;
         const float thr = key_dist(key[q]) * (1.0f + eps_p);
+        const float scale = (thr > 0.0f && !one_bucket) ? (float)NBUCKET / thr : 0.0f;
         const unsigned s1 = (unsigned)(minkey[q] & 0xffffffffull);
         const unsigned s2 = seed2 ? (unsigned)seed2[q] : 0xffffffffu;
         const float *row = lb + q * ldlb;
-        unsigned flags = 0;  // bit 4k+e: element nbase + 16*tid + 4k + e survives
+        float v[16];
+        unsigned flags = 0;  // bit e: element nbase + 16*tid + e survives
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int64_t n0 = nbase + 16 * threadIdx.x + 4 * k;
-            float v[4];
             if (vec && n0 + 3 < nt) {
                 const float4 f = *reinterpret_cast<const float4 *>(row + n0);
-                v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+                v[4 * k] = f.x; v[4 * k + 1] = f.y; v[4 * k + 2] = f.z; v[4 * k + 3] = f.w;
             } else {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) v[e] = (n0 + e < nt) ? row[n0 + e] : kInf;
+                for (int e = 0; e < 4; ++e) v[4 * k + e] = (n0 + e < nt) ? row[n0 + e] : kInf;
             }
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const unsigned n = (unsigned)(n0 + e);
-                const bool ok = (n0 + e < nt) && v[e] <= thr && n != s1 && n != s2;
+                const bool ok = (n0 + e < nt) && v[4 * k + e] <= thr && n != s1 && n != s2;
                 flags |= (ok ? 1u : 0u) << (4 * k + e);
             }
         }
-        const int c = __popc(flags);
-        int incl = c;
+        auto bucket_of = [&](float x) {
+            const int b = (int)(x * scale);
+            return b < 0 ? 0 : (b >= NBUCKET ? NBUCKET - 1 : b);
+        };
+        if (PASS == 0) {
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int o = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl += o;
-        }
-        if (lane == 31) wsum[warp] = incl;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int run = 0;
-            for (int i = 0; i < 8; ++i) {
-                const int t = wsum[i];
-                wsum[i] = run;
-                run += t;
+            for (int e = 0; e < 16; ++e)
+                if ((flags >> e) & 1u) atomicAdd(&hist[bucket_of(v[e])], 1u);
+            __syncthreads();
+            if (threadIdx.x < NBUCKET && hist[threadIdx.x])
+                atomicAdd(bucket_count + threadIdx.x, (unsigned long long)hist[threadIdx.x]);
+        } else {
+            unsigned slot[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+                slot[e] = ((flags >> e) & 1u) ? atomicAdd(&hist[bucket_of(v[e])], 1u) : 0u;
+            __syncthreads();
+            if (threadIdx.x < NBUCKET) {
+                const unsigned c = hist[threadIdx.x];
+                base[threadIdx.x] = c ? bucket_base[threadIdx.x] +
+                                            atomicAdd(bucket_fill + threadIdx.x, (unsigned long long)c)
+                                      : 0ull;
             }
-            sbase = run > 0 ? atomicAdd(count, (unsigned long long)run) : 0ull;
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                if ((flags >> e) & 1u) {
+                    const unsigned long long pos = base[bucket_of(v[e])] + slot[e];
+                    if (pos < capacity)
+                        items[pos] = Item{(unsigned)q, (unsigned)(nbase + 16 * threadIdx.x + e), v[e]};
+                }
+            }
         }
-        __syncthreads();
-        unsigned long long pos = sbase + (unsigned long long)(wsum[warp] + incl - c);
-        while (flags) {
-            const int bit = __ffs(flags) - 1;
-            flags &= flags - 1;
-            if (pos < capacity)
-                items[pos] = Item{(unsigned)q, (unsigned)(nbase + 16 * threadIdx.x + bit)};
-            ++pos;
+        __syncthreads();  // hist / base are reused by the next tile
+    }
+}
+
+// bucket counts -> offsets; the total is the survivor count the DTW kernel reads
+__global__ void k_bucket_scan(const unsigned long long *count, unsigned long long *base,
+                              unsigned long long *fill, unsigned long long *total) {
+    if (threadIdx.x == 0) {
+        unsigned long long run = 0;
+        for (int b = 0; b < NBUCKET; ++b) {
+            base[b] = run;
+            fill[b] = 0ull;
+            run += count[b];
         }
-        __syncthreads();  // wsum / sbase are reused by the next tile
+        *total = run;
     }
 }
 
 int launch_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
                    const unsigned long long *key, const unsigned long long *minkey,
                    const int32_t *seed2, float eps_p, Item *items, unsigned long long *count,
-                   unsigned long long capacity, int num_sms, cudaStream_t st) {
+                   unsigned long long *buckets, unsigned long long capacity, int num_sms,
+                   cudaStream_t st) {
     if (nq == 0 || nt == 0) return 0;
+    // buckets: [count | base | fill] x NBUCKET, zeroed here
+    unsigned long long *bcount = buckets, *bbase = buckets + NBUCKET, *bfill = buckets + 2 * NBUCKET;
+    cudaMemsetAsync(bcount, 0, sizeof(unsigned long long) * NBUCKET, st);
     int64_t ntiles = ((nt + CT_N - 1) / CT_N) * nq;
     int64_t grid = ntiles < (int64_t)num_sms * 8 ? ntiles : (int64_t)num_sms * 8;
-    k_compact<<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, minkey, seed2, eps_p,
-                                               items, count, capacity);
-    count_launch(1, __func__);
+    static const char *ob = getenv("NNDTW_ONE_BUCKET");  // experiments: q-major order
+    const int one = ob && ob[0] == '1';
+    k_compact<0><<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, minkey, seed2, eps_p,
+                                                  items, bcount, bbase, bfill, capacity, one);
+    k_bucket_scan<<<1, 32, 0, st>>>(bcount, bbase, bfill, count);
+    k_compact<1><<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, minkey, seed2, eps_p,
+                                                  items, bcount, bbase, bfill, capacity, one);
+    count_launch(3, __func__);
     return 0;
 }
 
