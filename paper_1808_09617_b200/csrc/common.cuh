@@ -139,7 +139,7 @@ struct Item {
 
 // Survivor order (S3/S4): LB / bsf_seed buckets, visited in ascending order so that every query's
 // most promising candidates run first and later ones meet a tightened best-so-far.
-constexpr int NBUCKET = 16;
+constexpr int NBUCKET = 64;
 
 // near-tie log entry (S7): completed candidate within the band of the live best at the time
 struct TieEntry {
