@@ -58,6 +58,40 @@ def test_envelopes_bit_exact(dev, oracle_lib, L):
     assert np.array_equal(k[:, 0].view(np.float32), X.min(axis=1))
 
 
+@pytest.mark.parametrize("L", [257, 300, 512, 513, 1000, 2048])
+def test_envelopes_direct_residues(dev, oracle_lib, L):
+    """The direct (w >= 16) envelope kernel is instantiated per R = w mod 16: every residue, the
+    smallest q, windows near L, and the Kim features of every call."""
+    from paper_1808_09617_b200 import nndtw
+    rng = np.random.default_rng(L + 1)
+    X = np.concatenate([datagen.random_series(rng, 7, L, k) for k in ("walk", "int")])
+    ws = list(range(16, 48)) + [103, L // 3, L // 2 + 5, L - 17, L - 2]
+    for w in sorted(set(ws)):
+        U, Lo, kim = nndtw.envelopes(T(X, dev), w)
+        eu, el = oracle_lib.envelopes(X, w)
+        assert np.array_equal(U.cpu().numpy(), eu), (L, w)
+        assert np.array_equal(Lo.cpu().numpy(), el), (L, w)
+        k = kim.cpu().numpy()
+        assert np.array_equal(k[:, 2], np.argmin(X, axis=1)), (L, w)
+        assert np.array_equal(k[:, 3], np.argmax(X, axis=1)), (L, w)
+        assert np.array_equal(k[:, 0].view(np.float32), X.min(axis=1)), (L, w)
+        assert np.array_equal(k[:, 1].view(np.float32), X.max(axis=1)), (L, w)
+
+
+def test_envelopes_many_sets(dev, oracle_lib):
+    """More series than resident blocks: the persistent kernels loop over series sets."""
+    from paper_1808_09617_b200 import nndtw
+    rng = np.random.default_rng(5)
+    L = 512
+    X = datagen.random_series(rng, 6001, L, "walk")
+    for w in (5, 51, 103):
+        U, Lo, kim = nndtw.envelopes(T(X, dev), w)
+        eu, el = oracle_lib.envelopes(X, w)
+        assert np.array_equal(U.cpu().numpy(), eu), w
+        assert np.array_equal(Lo.cpu().numpy(), el), w
+        assert np.array_equal(kim.cpu().numpy()[:, 3], np.argmax(X, axis=1)), w
+
+
 # ---------------------------------------------------------------- S2 bounds
 @pytest.mark.parametrize("L,w,V", [(2, 0, 1), (3, 1, 2), (16, 3, 5), (64, 0, 5), (100, 7, 3),
                                    (128, 13, 5), (256, 255, 8), (300, 30, 40), (512, 103, 5),
