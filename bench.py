@@ -34,6 +34,24 @@ import datagen  # noqa: E402
 METRIC = "NN-DTW queries/s (LB_Enhanced^V cascade) at 1/2/4/8 B200; DTW GCUPS"
 
 
+def envelope_kernel(L: int, w: int) -> str:
+    """Which S1 kernel launch_envelopes (envelopes.cu) picks: the direct form for w >= 16 when
+    its padded shared-memory arrays fit, van Herk otherwise (same rule as the launcher)."""
+    w = min(w, L - 1)
+    if L <= 256 or w < 16:
+        return "k_envelopes"
+    tps = 32 * ((L + 511) // 512)
+    if tps > 256:
+        return "k_envelopes"
+    groups = max(64, tps) // tps
+    q = w >> 4
+    plen = (17 * (2 * (q + 1) + tps) + 1) & ~1
+    zlen = tps + 2 * (q + 1)
+    zall = (3 * zlen + 1) & ~1
+    smem = groups * ((2 * plen + zall) * 8 + 16 * 16 + 2 * 16 * tps * 4)
+    return "k_env_direct" if smem <= 112 * 1024 else "k_envelopes"
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -408,9 +426,10 @@ def main():
                "ms_per_step": acc_tot["ms_lb"] / args.steps}
     hbm = float(pk.get("hbm_gbs", 6650.0))
     env_gbs = env_bytes / (acc_env_ms / args.steps * 1e-3) / 1e9 if acc_env_ms > 0 else None
-    roof_env = {"kernel": "k_envelopes (S1)", "bound": "hbm", "achieved": env_gbs, "peak": hbm,
+    env_kernel = envelope_kernel(L, w)
+    roof_env = {"kernel": f"{env_kernel} (S1)", "bound": "hbm", "achieved": env_gbs, "peak": hbm,
                 "unit": "GB/s", "frac": env_gbs / hbm if env_gbs else None,
-                "traffic": traffic.get("k_envelopes", {}).get("bytes_per_launch")
+                "traffic": traffic.get(env_kernel, {}).get("bytes_per_launch")
                 if args.config == 2 else None,
                 "algorithmic_bytes": env_bytes,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
