@@ -20,6 +20,11 @@ int64 MIN is the unsigned MIN.  Messages are Q x 8 bytes per step.
 The per-shard operations are injected (`ShardOps`) so that the combine protocol itself is
 tested on CPU with the gloo backend (tests/test_dist_gloo.py); `GpuShardOps` is the product
 path through the C ABI.
+
+S8 (LOOCV window search) shards the other way: every rank holds all n series
+(each is a candidate for every held-out query), the held-out queries are split into contiguous
+ranges, and the per-window error counts are summed with one int64 SUM all-reduce of nw
+entries; the best window is then the same on every rank.
 """
 from __future__ import annotations
 
@@ -112,3 +117,29 @@ def classify_sharded(model: nndtw.Model, q: torch.Tensor, labels_global: torch.T
     out = combine(ops, q, group)
     idx, lab, d = nndtw.finalize(out, labels_global, key_format=1, stream=stream)
     return nndtw.Prediction(idx, lab, d, ops.last_stats)
+
+
+def best_window(errors, windows) -> int:
+    """argmin of the error counts, ties to the smallest w (reading C17)."""
+    e = [int(x) for x in errors]
+    return min(range(len(e)), key=lambda p: (e[p], int(windows[p]))) if e else -1
+
+
+def loocv_sharded(x: torch.Tensor, labels: torch.Tensor, windows, v: int = 5, group=None,
+                  stream=None, shard_fn=None):
+    """S8 over ranks: LOOCV error counts for every window in `windows` (absolute w), the
+    held-out queries split by shard_range over the ranks of `group`, all n series replicated
+    (self excluded by the kernel).  Returns (errors int64 [nw] on every rank, best window index).
+
+    shard_fn(q_begin, q_end) -> int64 [nw] computes one shard's counts; the default is the C-ABI
+    path (nndtw.loocv_window); the gloo tests inject the oracle."""
+    n = x.shape[0]
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    lo, hi = shard_range(n, rank, world)
+    if shard_fn is None:
+        def shard_fn(a, b):
+            return nndtw.loocv_window(x, labels, windows, v=v, q_begin=a, q_end=b,
+                                      stream=stream)[0]
+    errors = shard_fn(lo, hi).to(torch.int64)
+    dist.all_reduce(errors, op=dist.ReduceOp.SUM, group=group)
+    return errors, best_window(errors.cpu().tolist(), windows)

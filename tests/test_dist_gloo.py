@@ -142,3 +142,45 @@ def test_shard_range_partition():
             parts = [shard_range(n, r, world) for r in range(world)]
             assert parts[0][0] == 0 and parts[-1][1] == n
             assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+
+
+def _loocv_worker(rank, world, port, X, lab, windows, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_1808_09617_b200.dist import loocv_sharded
+
+    def shard_fn(a, b):  # one rank's held-out range, emulated with the oracle
+        return torch.as_tensor(oracle.loocv(X, lab, windows, V=2, q_begin=a, q_end=b,
+                                            threads=1)[0])
+    errors, best = loocv_sharded(torch.as_tensor(X), torch.as_tensor(lab), windows,
+                                 shard_fn=shard_fn)
+    ret[rank] = (errors.tolist(), best)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_loocv_sharded_sums_to_global(oracle_lib, world):
+    """S8 sharded over held-out queries: the SUM all-reduce of per-shard counts equals the
+    unsharded LOOCV, and every rank agrees on the best window (ties to the smallest w)."""
+    from paper_1808_09617_b200.dist import best_window
+    rng = np.random.default_rng(40 + world)
+    X = datagen.random_series(rng, 17, 12, "walk")
+    lab = (np.arange(17) % 3).astype(np.int32)
+    windows = [0, 1, 2, 4, 11]
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_loocv_worker, args=(world, _free_port(), X, lab, windows, ret), nprocs=world,
+             join=True)
+    ref, _ = oracle_lib.loocv(X, lab, windows, V=2, mode="exhaustive")
+    for r in range(world):
+        assert ret[r][0] == list(ref), (r, ret[r], ref)
+        assert ret[r][1] == best_window(ref, windows)
+
+
+def test_best_window_ties_to_smallest_w():
+    from paper_1808_09617_b200.dist import best_window
+    assert best_window([3, 1, 1, 2], [0, 5, 9, 12]) == 1
+    assert best_window([2, 2], [7, 3]) == 1
+    assert best_window([], []) == -1

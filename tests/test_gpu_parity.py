@@ -411,3 +411,30 @@ def test_classify_tie_log_overflow(dev, oracle_lib, monkeypatch):
         pred = nndtw.classify(model, T(Q, dev))
         _check_nn(oracle_lib, Tr, lab, Q, w, pred.idx.cpu().numpy(), pred.label.cpu().numpy(),
                   pred.dist.cpu().numpy(), V=3)
+
+
+def test_loocv_sharded_world1_nccl(dev, oracle_lib):
+    """dist.loocv_sharded through the C ABI and a real one-rank NCCL group (the N>1 launch path of
+    S8 at N=1): counts and best window equal the oracle's."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_1808_09617_b200.dist import best_window, loocv_sharded
+    rng = np.random.default_rng(11)
+    X = datagen.random_series(rng, 90, 40, "walk")
+    lab = (np.arange(90) % 4).astype(np.int32)
+    wins = [0, 2, 4, 8, 20, 39]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    store = dist.TCPStore("127.0.0.1", port, 1, True)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=dev)
+    try:
+        errors, best = loocv_sharded(T(X, dev), T(lab, dev), wins, v=5)
+    finally:
+        dist.destroy_process_group()
+    ref, _ = oracle_lib.loocv(X, lab, wins, V=5)
+    assert errors.cpu().tolist() == list(ref)
+    assert best == best_window(ref, wins)
