@@ -102,24 +102,27 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
     const int ch_end = (L - nbb + LB_CC - 1) / LB_CC;  // exclusive
     float ra[4];
     float2 re[8];
+    // load slot k of this thread: tile row (tid >> 4) + 16k, column c0 + (tid & 15) -- the same
+    // column for every k, so the column test is one per chunk; row pointers are hoisted and
+    // full tiles skip the row tests
+    const int lr = tid >> 4, lc = tid & 15;
+    const bool qfull = q0 + LB_TQ <= p.nq, nfull = n0 + LB_TN <= p.nt;
+    const int64_t rs16 = 16 * (int64_t)L;
+    const float *qrow = p.q + (q0 + lr < p.nq ? q0 + lr : 0) * (int64_t)L + lc;
+    const int64_t erow = (n0 + lr < p.nt ? n0 + lr : 0) * (int64_t)L + lc;
+    const float *urow = p.U + erow, *lrow = p.Lo + erow;
     auto load_chunk = [&](int ch) {
         const int c0 = ch * LB_CC;
+        const bool cok = c0 + lc >= nbb && c0 + lc < L - nbb;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            int e = tid + 256 * k;
-            int r = e >> 4, c = c0 + (e & 15);
-            int64_t qq = q0 + r;
-            bool ok = qq < p.nq && c >= nbb && c < L - nbb;
-            ra[k] = ok ? __ldg(p.q + qq * (int64_t)L + c) : 0.0f;
+            const bool ok = cok && (qfull || q0 + lr + 16 * k < p.nq);
+            ra[k] = ok ? __ldg(qrow + k * rs16 + c0) : 0.0f;
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            int e = tid + 256 * k;
-            int r = e >> 4, c = c0 + (e & 15);
-            int64_t nn = n0 + r;
-            bool ok = nn < p.nt && c >= nbb && c < L - nbb;
-            int64_t off = nn * (int64_t)L + c;
-            re[k] = ok ? make_float2(__ldg(p.U + off), __ldg(p.Lo + off))
+            const bool ok = cok && (nfull || n0 + lr + 16 * k < p.nt);
+            re[k] = ok ? make_float2(__ldg(urow + k * rs16 + c0), __ldg(lrow + k * rs16 + c0))
                        : make_float2(kInf, -kInf);
         }
     };
