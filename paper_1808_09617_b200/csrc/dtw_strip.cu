@@ -2,10 +2,14 @@
 // BJ:configs[4], L = 2048, w = L-1): windowed DTW (Eq. 1) by row strips.
 //
 // B200 design.  One warp per (query, train) pair.  The matrix is
-// cut into strips of H = 32*RR rows; lane l owns rows i0 + l*RR .. i0 + l*RR + RR-1 and sweeps
-// the columns with a one-lane skew (lane l is at column j = s - l on step s), so the value from
-// the row above (lane l-1's bottom row, one step earlier) arrives by one warp shuffle.  Inside a
-// lane the RR rows are evaluated top-down, keeping the previous column in registers:
+// cut into strips of H = 32*RR rows; lane l owns rows i0 + l*RR .. i0 + l*RR + RR-1, split into
+// KS sub-blocks of RB = RR/KS rows, and sweeps the columns with a staggered skew: on step s,
+// sub-block k of lane l is at column j = s - l*KS - k.  Then every cell's inputs were produced
+// on an earlier step -- the row above a sub-block is the previous sub-block's bottom row one
+// step earlier (one register; across lanes one warp shuffle), the diagonal two steps earlier --
+// so the KS sub-blocks of a step are independent dependency chains (a lane evaluating its RR
+// rows top-down at one column is one serial chain of RR fused cells, which left the SM issue
+// mostly waiting on the previous cell: KS = 4 cuts that chain 4x).  Inside a sub-block:
 //     D(i,j) = (A_i - B_j)^2 + min(D(i,j-1), D(i-1,j-1), D(i-1,j))
 // The bottom row of a strip is written to shared memory (the next strip's "row above") and its
 // minimum -- a complete row, hence a cut of every warping path (reading C14) -- decides early
@@ -18,7 +22,7 @@
 
 namespace nndtw {
 
-constexpr int STRIP_PAD = 40;  // B pads on each side (>= 32 skew steps)
+constexpr int STRIP_PAD = 136;  // B pads on each side (>= 32*KS skew steps, KS <= 4)
 
 struct StripParams {
     const float *A, *B;
@@ -37,18 +41,21 @@ struct StripParams {
     const long long *cells_prefix;
     const float *cutoff;
     float *out;
-    int rowlen;  // floats per warp region: (L + 2*PAD) for B, L + 33 for the row buffer,
-                 // then ceil(L/32) block suffix minima of the row buffer
+    int rowlen;  // floats per warp region: (L + 2*PAD) for B, L + 32*KS + 1 for the row
+                 // buffer, then ceil(L/32) block suffix minima of the row buffer
+    int ks;      // sub-blocks per lane (the template KS; sizes rowlen)
 };
 
-template <int RR, bool MASK>
+template <int RR, int KS, bool MASK>
 __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
+    static_assert(RR % KS == 0, "sub-blocks split the lane's rows evenly");
+    constexpr int RB = RR / KS;
     extern __shared__ __align__(16) float smem_s[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int L = p.L, w = p.w;
     float *sB = smem_s + (size_t)warp * p.rowlen;           // B[j] at sB[PAD + j]
-    float *bsuf = sB + (L + 2 * STRIP_PAD) + (L + 33);       // [ceil(L/32)]
+    float *bsuf = sB + (L + 2 * STRIP_PAD) + (L + 32 * KS + 1);  // [ceil(L/32)]
     float *rb = sB + (L + 2 * STRIP_PAD);                    // rb[1 + j] = row above, column j
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -64,7 +71,7 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
     }
     const int H = 32 * RR;
     const int nstrips = (L + H - 1) / H;
-    const int nsteps = L + 31;
+    const int nsteps = L + 32 * KS - 1;
     long long my_items = 0, my_aband = 0, my_cells = 0, my_skipped = 0;
 
     for (int64_t it = gw; it < nitems; it += nwarps) {
@@ -89,7 +96,7 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
         const float *gb = p.B + (int64_t)b_idx * L;
         __syncwarp();
         for (int x = lane; x < L; x += 32) cp_async4(sB + STRIP_PAD + x, gb + x);
-        for (int x = lane; x < L + 32; x += 32) rb[1 + x] = kInf;  // D(-1, j) = +inf; pads
+        for (int x = lane; x < L + 32 * KS; x += 32) rb[1 + x] = kInf;  // D(-1, j) = +inf; pads
         if (lane == 0) rb[0] = 0.0f;                          // D(-1,-1) = 0
         cp_async_wait_all();
         __syncwarp();
@@ -133,64 +140,82 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
             float thr = thr_batch;
             if (p.mode == 0) thr = key_dist(ld_relaxed_u64(p.key + a_idx)) * (1.0f + p.eps_t);
             float up_prev = (lane == 0) ? rb[0] : kInf;  // diagonal input of the top row
-            float bot = kInf;
+            float pb2[KS];  // bottom of sub-block k two steps ago (diagonal input of k+1)
+#pragma unroll
+            for (int k = 0; k < KS; ++k) pb2[k] = kInf;
             float rowmin = kInf;
             const bool last = (st == nstrips - 1);
             const int rstar = (L - 1) - (st * H + lane * RR);  // row L-1 in this lane?
-            // One column step of this lane's RR rows.  CHECK: ramp-up / ramp-down steps where
-            // some lane's column is outside [0, L) (range-checked); steady steps need no checks.
+            // One step: sub-block k of this lane at column s - lane*KS - k.  CHECK: ramp-up /
+            // ramp-down steps where some column is outside [0, L) (range-checked); steady steps
+            // need no checks.
             auto step = [&](int s, auto check_tag) {
                 constexpr bool CHECK = decltype(check_tag)::value;
-                const int j = s - lane;
-                const float b = sB[STRIP_PAD + j];  // pads make out-of-range columns +inf
-                const float from_up = __shfl_up_sync(0xffffffffu, bot, 1);
+                // the lane above's last sub-block bottom, one step ago, at this lane's column
+                const float from_up = __shfl_up_sync(0xffffffffu, Dl[RR - 1], 1);
                 const float rbv = rb[1 + s];        // lane 0's column; rb padded with +inf
                 const float up = (lane == 0) ? rbv : from_up;
-                float dgv = up_prev, upv = up;
+                float nb2[KS];
 #pragma unroll
-                for (int r = 0; r < RR; ++r) {
-                    const float t = a[r] - b;
-                    const float old = Dl[r];
-                    float nv = fmaf(t, t, fminf(fminf(old, dgv), upv));
-                    if (MASK) {
-                        const int i = i0 + r;
-                        if (j - i > w || i - j > w) nv = kInf;
+                for (int k = KS - 1; k >= 0; --k) {  // descending: k reads k-1's old bottom
+                    const int j = s - lane * KS - k;
+                    const float b = sB[STRIP_PAD + j];  // pads make out-of-range columns +inf
+                    float dgv = (k == 0) ? up_prev : pb2[k - 1];
+                    float upv = (k == 0) ? up : Dl[k * RB - 1];
+                    nb2[k] = Dl[k * RB + RB - 1];
+#pragma unroll
+                    for (int r = 0; r < RB; ++r) {
+                        const int R = k * RB + r;
+                        const float t = a[R] - b;
+                        const float old = Dl[R];
+                        float nv = fmaf(t, t, fminf(fminf(old, dgv), upv));
+                        if (MASK) {
+                            const int i = i0 + R;
+                            if (j - i > w || i - j > w) nv = kInf;
+                        }
+                        Dl[R] = nv;
+                        dgv = old;
+                        upv = nv;
                     }
-                    Dl[r] = nv;
-                    dgv = old;
-                    upv = nv;
-                }
-                up_prev = up;
-                bot = Dl[RR - 1];
-                const bool jin = !CHECK || (j >= 0 && j < L);
-                if (lane == 31 && jin) {
-                    rb[1 + j] = bot;
-                    rowmin = fminf(rowmin, bot);
-                }
-                if (CHECK && last && j == L - 1 && rstar >= 0 && rstar < RR) {
+                    if (CHECK && last && j == L - 1 && rstar >= k * RB && rstar < k * RB + RB) {
 #pragma unroll
-                    for (int r = 0; r < RR; ++r)
-                        if (r == rstar) res = Dl[r];
+                        for (int r = 0; r < RB; ++r)
+                            if (k * RB + r == rstar) res = Dl[k * RB + r];
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < KS; ++k) pb2[k] = nb2[k];
+                up_prev = up;
+                const int jb = s - lane * KS - (KS - 1);  // the bottom row's column
+                const bool jin = !CHECK || (jb >= 0 && jb < L);
+                if (lane == 31 && jin) {
+                    rb[1 + jb] = Dl[RR - 1];
+                    rowmin = fminf(rowmin, Dl[RR - 1]);
                 }
             };
-            // steady phase: every lane's column in [0, L-1) <=> 31 <= s < L-1 (no lane reaches
+            // steady phase: every column in [0, L-1) <=> 32KS-1 <= s < L-1 (no sub-block reaches
             // the last column, where the result is captured); the rest is range-checked
-            const bool has_steady = L >= 33;
-            const int s_lo = has_steady ? 31 : nsteps, s_hi = has_steady ? L - 1 : nsteps;
+            const bool has_steady = L >= 32 * KS + 1;
+            const int s_lo = has_steady ? 32 * KS - 1 : nsteps, s_hi = has_steady ? L - 1 : nsteps;
             for (int s = 0; s < s_lo; ++s) step(s, std::true_type{});
             int s = s_lo;
             bool cut_abandon = false;
             for (; s + 1 < s_hi; s += 2) {
-                if ((s & 31) == 31 && s > 31) {
-                    // Checkpoint: lane l has computed columns <= s-1-l.  Every warping path
-                    // crosses the set {each lane's current column cells, the previous-column
-                    // bottom cell of the lane above (up_prev), lane 31's bottom row so far,
-                    // the previous strip's bottom row from column s-1 on}; D is non-decreasing
-                    // along paths, so its minimum is a lower bound of the distance (reading
-                    // C14).  bsuf[s/32] covers columns >= s-31 (a superset: still a bound).
+                if ((s & 31) == 31 && s > 32 * KS) {
+                    // Checkpoint: the computed cells of this strip form a staircase (row by row
+                    // the last column is non-increasing, by one between consecutive sub-blocks
+                    // and lanes).  Every warping path leaves it through a frontier cell: the
+                    // last cell of each row (Dl), the cell left of it in the bottom row of each
+                    // sub-block or lane above (pb2, up_prev: their diagonal successor is not
+                    // computed), the bottom row of the strip so far (lane 31's rowmin), or the
+                    // previous strip's bottom row from column s-1 on (bsuf[s/32] covers columns
+                    // >= s-31, a superset).  D is non-decreasing along paths, so the minimum is a
+                    // lower bound of the distance (reading C14).
                     float mv = up_prev;
 #pragma unroll
                     for (int r = 0; r < RR; ++r) mv = fminf(mv, Dl[r]);
+#pragma unroll
+                    for (int k = 0; k < KS; ++k) mv = fminf(mv, pb2[k]);
                     if (lane == 31) mv = fminf(mv, rowmin);
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1)
@@ -214,7 +239,7 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
 #pragma unroll
                     for (int r = 0; r < RR; ++r) {
                         const int i = i0 + r;
-                        const int jmax = s - 1 - lane;  // last column computed by this lane
+                        const int jmax = s - 1 - lane * KS - r / RB;  // last column computed
                         if (i < L && jmax >= 0) {
                             const int lo = i - w > 0 ? i - w : 0;
                             int hi = i + w < L - 1 ? i + w : L - 1;
@@ -316,9 +341,9 @@ int strip_rows_per_lane(int L) {
     return best;
 }
 
-template <int RR, bool MASK>
+template <int RR, int KS, bool MASK>
 static int launch_strip_t(StripParams &p, cudaStream_t st, int num_sms) {
-    auto kern = k_dtw_strip<RR, MASK>;
+    auto kern = k_dtw_strip<RR, KS, MASK>;
     // up to 4 warps per CTA, fewer when the rows are long (L up to 8192: 66 KB per warp)
     int warps = (int)((220 * 1024) / ((size_t)p.rowlen * sizeof(float)));
     if (warps > 4) warps = 4;
@@ -365,23 +390,24 @@ int launch_dtw_strip(const float *A, const float *B, const Item *items,
     p.cells_prefix = cells_prefix;
     p.cutoff = cutoff;
     p.out = out;
-    p.rowlen = (L + 2 * STRIP_PAD) + (L + 33) + (L + 31) / 32;
-    p.rowlen = (p.rowlen + 3) / 4 * 4;
     const bool mask = w < L - 1;
     const int RR = strip_rows_per_lane(L);
+    p.ks = (RR == 10) ? 2 : 4;  // sub-blocks per lane (KS divides RR)
+    p.rowlen = (L + 2 * STRIP_PAD) + (L + 32 * p.ks + 1) + (L + 31) / 32;
+    p.rowlen = (p.rowlen + 3) / 4 * 4;
     switch (RR) {
         case 16:
-            return mask ? launch_strip_t<16, true>(p, st, num_sms)
-                        : launch_strip_t<16, false>(p, st, num_sms);
+            return mask ? launch_strip_t<16, 4, true>(p, st, num_sms)
+                        : launch_strip_t<16, 4, false>(p, st, num_sms);
         case 12:
-            return mask ? launch_strip_t<12, true>(p, st, num_sms)
-                        : launch_strip_t<12, false>(p, st, num_sms);
+            return mask ? launch_strip_t<12, 4, true>(p, st, num_sms)
+                        : launch_strip_t<12, 4, false>(p, st, num_sms);
         case 10:
-            return mask ? launch_strip_t<10, true>(p, st, num_sms)
-                        : launch_strip_t<10, false>(p, st, num_sms);
+            return mask ? launch_strip_t<10, 2, true>(p, st, num_sms)
+                        : launch_strip_t<10, 2, false>(p, st, num_sms);
         default:
-            return mask ? launch_strip_t<8, true>(p, st, num_sms)
-                        : launch_strip_t<8, false>(p, st, num_sms);
+            return mask ? launch_strip_t<8, 4, true>(p, st, num_sms)
+                        : launch_strip_t<8, 4, false>(p, st, num_sms);
     }
 }
 
