@@ -145,11 +145,12 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
             for (int k = 0; k < KS; ++k) pb2[k] = kInf;
             float rowmin = kInf;
             const bool last = (st == nstrips - 1);
-            const int rstar = (L - 1) - (st * H + lane * RR);  // row L-1 in this lane?
             // One step: sub-block k of this lane at column s - lane*KS - k.  CHECK: ramp-up /
             // ramp-down steps where some column is outside [0, L) (range-checked); steady steps
             // need no checks.
-            auto step = [&](int s, auto check_tag) {
+            // bw: nullptr -> each sub-block loads its B value; else bw[-k] is sub-block k's value
+            // (the 4-step groups below fetch them as two aligned float4 per group)
+            auto step = [&](int s, auto check_tag, const float *bw) {
                 constexpr bool CHECK = decltype(check_tag)::value;
                 // the lane above's last sub-block bottom, one step ago, at this lane's column
                 const float from_up = __shfl_up_sync(0xffffffffu, Dl[RR - 1], 1);
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
 #pragma unroll
                 for (int k = KS - 1; k >= 0; --k) {  // descending: k reads k-1's old bottom
                     const int j = s - lane * KS - k;
-                    const float b = sB[STRIP_PAD + j];  // pads make out-of-range columns +inf
+                    const float b = bw ? bw[-k] : sB[STRIP_PAD + j];  // pads: +inf cells
                     float dgv = (k == 0) ? up_prev : pb2[k - 1];
                     float upv = (k == 0) ? up : Dl[k * RB - 1];
                     nb2[k] = Dl[k * RB + RB - 1];
@@ -177,11 +178,6 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
                         dgv = old;
                         upv = nv;
                     }
-                    if (CHECK && last && j == L - 1 && rstar >= k * RB && rstar < k * RB + RB) {
-#pragma unroll
-                        for (int r = 0; r < RB; ++r)
-                            if (k * RB + r == rstar) res = Dl[k * RB + r];
-                    }
                 }
 #pragma unroll
                 for (int k = 0; k < KS; ++k) pb2[k] = nb2[k];
@@ -197,10 +193,10 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
             // the last column, where the result is captured); the rest is range-checked
             const bool has_steady = L >= 32 * KS + 1;
             const int s_lo = has_steady ? 32 * KS - 1 : nsteps, s_hi = has_steady ? L - 1 : nsteps;
-            for (int s = 0; s < s_lo; ++s) step(s, std::true_type{});
+            for (int s = 0; s < s_lo; ++s) step(s, std::true_type{}, nullptr);
             int s = s_lo;
             bool cut_abandon = false;
-            for (; s + 1 < s_hi; s += 2) {
+            for (; s + 3 < s_hi; s += 4) {
                 if ((s & 31) == 31 && s > 32 * KS) {
                     // Checkpoint: the computed cells of this strip form a staircase (row by row
                     // the last column is non-increasing, by one between consecutive sub-blocks
@@ -229,8 +225,27 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
                         break;
                     }
                 }
-                step(s, std::false_type{});
-                step(s + 1, std::false_type{});
+                if constexpr (KS == 4) {
+                    // the group's B values: columns x0-3 .. x0+3 of this lane, x0 = s - 4*lane;
+                    // PAD + s = 3 (mod 4) at every group start (s_lo = 127, PAD = 136), so they
+                    // are two aligned float4 -- 2 loads per 4 steps, and the 32 lanes' float4
+                    // are contiguous (no bank conflicts), instead of 4 stride-4 loads per step
+                    static_assert((STRIP_PAD + 32 * KS - 1) % 4 == 3, "group alignment");
+                    const float *bp = sB + STRIP_PAD + s - 4 * lane - 3;
+                    const float4 lo = *reinterpret_cast<const float4 *>(bp);
+                    const float4 hi = *reinterpret_cast<const float4 *>(bp + 4);
+                    const float bw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+                    // step s+m, sub-block k: column x0 + m - k = bw[3 + m - k]
+                    step(s, std::false_type{}, bw + 3);
+                    step(s + 1, std::false_type{}, bw + 4);
+                    step(s + 2, std::false_type{}, bw + 5);
+                    step(s + 3, std::false_type{}, bw + 6);
+                } else {
+                    step(s, std::false_type{}, nullptr);
+                    step(s + 1, std::false_type{}, nullptr);
+                    step(s + 2, std::false_type{}, nullptr);
+                    step(s + 3, std::false_type{}, nullptr);
+                }
             }
             if (cut_abandon) {
                 // in-band cells of the complete strips plus this strip's computed columns
@@ -254,8 +269,18 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
                 abandoned = true;
                 break;
             }
-            for (; s < s_hi; ++s) step(s, std::false_type{});
-            for (s = s_hi; s < nsteps; ++s) step(s, std::true_type{});
+            for (; s < s_hi; ++s) step(s, std::false_type{}, nullptr);
+            // ramp-down; row L-1 (last strip) reaches column L-1 on step s_star, uniform
+            const int own_l = ((L - 1) % H) / RR, own_r = (L - 1) - (st * H + own_l * RR);
+            const int s_star = (L - 1) + own_l * KS + own_r / RB;
+            for (s = s_hi; s < nsteps; ++s) {
+                step(s, std::true_type{}, nullptr);
+                if (last && s == s_star && lane == own_l) {
+#pragma unroll
+                    for (int r = 0; r < RR; ++r)
+                        if (r == own_r) res = Dl[r];
+                }
+            }
             __syncwarp();
             // column -1 of the next strip's row above is +inf (only row -1 has the 0 corner)
             if (lane == 0) rb[0] = kInf;
