@@ -183,10 +183,13 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
             for (int qi = 0; qi < LB_QPT; ++qi) ai[qi] = side ? qtv(qi, i) : qhv(qi, i);
 #pragma unroll
             for (int j = 0; j < LB_NPT; ++j) bi[j] = side ? ttv(j, i) : thv(j, i);
+            // min over the band of (x-y)^2 = (min |x-y|)^2 exactly (rounding is monotone in
+            // |x-y|): the band minimum runs on |differences| (FMNMX3 with |.| operands, ALU pipe)
+            // and squares once -- one FMA-pipe op per band cell instead of two
 #pragma unroll
             for (int qi = 0; qi < LB_QPT; ++qi)
 #pragma unroll
-                for (int j = 0; j < LB_NPT; ++j) m[qi][j] = sq(ai[qi] - bi[j]);
+                for (int j = 0; j < LB_NPT; ++j) m[qi][j] = fabsf(ai[qi] - bi[j]);
             for (int jj = jlo; jj < i; ++jj) {
                 float aj[LB_QPT], bj[LB_NPT];
 #pragma unroll
@@ -198,12 +201,13 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
 #pragma unroll
                     for (int j = 0; j < LB_NPT; ++j)
                         m[qi][j] = fminf(m[qi][j],
-                                         fminf(sq(ai[qi] - bj[j]), sq(aj[qi] - bi[j])));
+                                         fminf(fabsf(ai[qi] - bj[j]), fabsf(aj[qi] - bi[j])));
             }
 #pragma unroll
             for (int qi = 0; qi < LB_QPT; ++qi)
 #pragma unroll
-                for (int j = 0; j < LB_NPT; ++j) acc[qi][j] = acc[qi][j] + m[qi][j];
+                for (int j = 0; j < LB_NPT; ++j)  // rounded square, then add (no FFMA contraction)
+                    acc[qi][j] = __fadd_rn(acc[qi][j], __fmul_rn(m[qi][j], m[qi][j]));
         }
     }
 
