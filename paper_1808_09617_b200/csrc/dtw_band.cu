@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(352) k_dtw_band(BandParams p) {
         // all copies in flight at once (cp.async), one wait: the rows arrive in about one
         // memory round trip instead of L/G dependent load->store steps
         if (p.vec4) {
+#pragma unroll 4
             for (int x = 4 * g; x < L; x += 4 * G) {
                 cp_async16(sA + p.padl + x, ga + x);
                 cp_async16(sB + p.padl + x, gb + x);
