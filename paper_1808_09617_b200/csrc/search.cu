@@ -52,8 +52,8 @@ int launch_seed_items(const unsigned long long *minkey, const int32_t *seed2, in
 }
 
 // ---- S3 compaction: surviving pairs LB <= bsf*(1+eps_p), in LB-bucket order -------------------
-// One CTA-tile = (query q, CT_N consecutive train indices), 16 per thread as 4 warp-contiguous
-// float4 loads.  A survivor's bucket is floor(NBUCKET * LB / thr) (thr = the query's seeded
+// One CTA-tile = (query q, CT_N consecutive train indices), 16 consecutive ones per thread (4
+// float4 loads).  A survivor's bucket is floor(NBUCKET * LB / thr) (thr = the query's seeded
 // best-so-far with the prune margin).  PASS 0 counts survivors per bucket (a shared-memory
 // histogram per tile, one global atomic per bucket and tile); k_bucket_scan turns the counts
 // into bucket offsets; PASS 1 reserves a contiguous run per bucket and tile and scatters the
@@ -88,13 +88,10 @@ __global__ void __launch_bounds__(256) k_compact(const float *__restrict__ lb, i
         const unsigned s2 = seed2 ? (unsigned)seed2[q] : 0xffffffffu;
         const float *row = lb + q * ldlb;
         float v[16];
-        // element 4k+e of this thread is train index nbase + 4*(tid + 256k) + e: each float4
-        // load is warp-contiguous (16 contiguous floats per thread would be 64-byte strided
-        // accesses, which cap the stream well below HBM bandwidth, tools/rw_roof.cu)
-        unsigned flags = 0;  // bit 4k+e: that element survives
+        unsigned flags = 0;  // bit e: element nbase + 16*tid + e survives
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const int64_t n0 = nbase + 4 * (threadIdx.x + 256 * k);
+            const int64_t n0 = nbase + 16 * threadIdx.x + 4 * k;
             if (vec && n0 + 3 < nt) {
                 const float4 f = *reinterpret_cast<const float4 *>(row + n0);
                 v[4 * k] = f.x; v[4 * k + 1] = f.y; v[4 * k + 2] = f.z; v[4 * k + 3] = f.w;
@@ -138,10 +135,7 @@ __global__ void __launch_bounds__(256) k_compact(const float *__restrict__ lb, i
                 if ((flags >> e) & 1u) {
                     const unsigned long long pos = base[bucket_of(v[e])] + slot[e];
                     if (pos < capacity)
-                        items[pos] = Item{(unsigned)q,
-                                          (unsigned)(nbase + 4 * (threadIdx.x + 256 * (e >> 2)) +
-                                                     (e & 3)),
-                                          v[e]};
+                        items[pos] = Item{(unsigned)q, (unsigned)(nbase + 16 * threadIdx.x + e), v[e]};
                 }
             }
         }
