@@ -16,6 +16,7 @@
 // abandoning against the live best-so-far.  B and the strip rows live in shared memory; padded
 // B values (+/-2^64) make out-of-range columns +inf.  When w < L-1, cells with |i-j| > w are
 // masked to +inf (MASK variant).
+#include <cstdlib>
 #include <type_traits>
 
 #include "launchers.cuh"
@@ -417,23 +418,32 @@ int launch_dtw_strip(const float *A, const float *B, const Item *items,
     p.out = out;
     const bool mask = w < L - 1;
     const int RR = strip_rows_per_lane(L);
-    p.ks = (RR == 10) ? 2 : 4;  // sub-blocks per lane (KS divides RR)
+    // sub-blocks per lane: the stagger costs 32*KS-1 ramp steps per strip of L + 32*KS - 1, so
+    // short rows keep fewer sub-blocks (L = 256: KS = 4 would add 50 % steps); KS divides RR
+    int ks = L >= 1024 ? 4 : (L >= 512 ? 2 : 1);
+    if (RR % ks != 0) ks = 2;
+    static const char *kse = getenv("NNDTW_STRIP_KS");  // experiments: force 1, 2 or 4
+    if (kse && RR % atoi(kse) == 0) ks = atoi(kse);
+    p.ks = ks;
     p.rowlen = (L + 2 * STRIP_PAD) + (L + 32 * p.ks + 1) + (L + 31) / 32;
     p.rowlen = (p.rowlen + 3) / 4 * 4;
-    switch (RR) {
-        case 16:
-            return mask ? launch_strip_t<16, 4, true>(p, st, num_sms)
-                        : launch_strip_t<16, 4, false>(p, st, num_sms);
-        case 12:
-            return mask ? launch_strip_t<12, 4, true>(p, st, num_sms)
-                        : launch_strip_t<12, 4, false>(p, st, num_sms);
-        case 10:
-            return mask ? launch_strip_t<10, 2, true>(p, st, num_sms)
-                        : launch_strip_t<10, 2, false>(p, st, num_sms);
-        default:
-            return mask ? launch_strip_t<8, 4, true>(p, st, num_sms)
-                        : launch_strip_t<8, 4, false>(p, st, num_sms);
+#define STRIP_KS(RRv)                                                                             \
+    if (RR == RRv) {                                                                              \
+        if (ks == 4)                                                                              \
+            return mask ? launch_strip_t<RRv, (RRv % 4 == 0 ? 4 : 2), true>(p, st, num_sms)      \
+                        : launch_strip_t<RRv, (RRv % 4 == 0 ? 4 : 2), false>(p, st, num_sms);    \
+        if (ks == 2)                                                                              \
+            return mask ? launch_strip_t<RRv, 2, true>(p, st, num_sms)                            \
+                        : launch_strip_t<RRv, 2, false>(p, st, num_sms);                          \
+        return mask ? launch_strip_t<RRv, 1, true>(p, st, num_sms)                                \
+                    : launch_strip_t<RRv, 1, false>(p, st, num_sms);                              \
     }
+    STRIP_KS(16)
+    STRIP_KS(12)
+    STRIP_KS(10)
+    STRIP_KS(8)
+#undef STRIP_KS
+    return -1;
 }
 
 }  // namespace nndtw
