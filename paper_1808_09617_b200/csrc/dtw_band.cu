@@ -57,8 +57,15 @@ __device__ __forceinline__ float pin_reg(float v) {
 // 1 = aligned, G*R = 2w+2 (kill slot is the top lane's last register: one scale register,
 // edge masks); 2 = aligned and gpw*G = 32 (every lane used: rotating shuffles deliver the
 // neighbouring group's kill slot, so no edge masks are needed at all).
+// Two resident CTAs of 8 warps per SM need <= 128 registers: kept where that costs no spills
+// (R <= 24, or R = 26 in the aligned layouts); measured on config 2: 206.6 -> 198.7 ms.
+template <int R, int KM>
+constexpr int band_min_blocks() {
+    return (R <= 24 || (R == 26 && KM >= 1)) ? 2 : 1;
+}
+
 template <int R, int KM, bool PACK>
-__global__ void __launch_bounds__(352) k_dtw_band(BandParams p) {
+__global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(BandParams p) {
     constexpr bool ALIGNED = KM >= 1;
     constexpr bool NOMASK = KM == 2;
     extern __shared__ __align__(16) float smem_f[];
@@ -308,11 +315,11 @@ __global__ void __launch_bounds__(352) k_dtw_band(BandParams p) {
                    (int)abandon);
 #endif
         if (__any_sync(0xffffffffu, done || abandon)) {  // rare: once per item per group
-            float res = D[0];
+            if (done && g == g0) {  // (most items end abandoned: the result slot only here)
+                float res = D[0];
 #pragma unroll
-            for (int r = 1; r < R; ++r)
-                if (r == r0) res = D[r];
-            if (done && g == g0) {
+                for (int r = 1; r < R; ++r)
+                    if (r == r0) res = D[r];
                 if (p.mode == 0) {
                     unsigned gidx = (unsigned)(p.index_base + ncur);
                     unsigned long long old = atomicMin(p.key + qcur, make_key(res, gidx));
@@ -429,7 +436,8 @@ static BandChoice choose_band(int w, int L) {
         band_geometry(R, G, L, w, c);
         const double warp_smem = (double)c.gpw * 2 * c.seglen * sizeof(float);
         static const char *wcap_env = getenv("NNDTW_BAND_WARPS");  // experiments
-        const int wcap = wcap_env ? atoi(wcap_env) : 8;
+        int wcap = wcap_env ? atoi(wcap_env) : 8;
+        if (wcap > 8) wcap = 8;  // __launch_bounds__(256, ...)
         int warps = (int)((226.0 * 1024) / warp_smem);
         if (warps < 1) continue;
         if (warps > wcap) warps = wcap;
