@@ -501,11 +501,12 @@ int launch_dtw_band(BandParams p, cudaStream_t st, int num_sms) {
     if (c.R == 0) return -1;
     {
         // Half-packed cells (FADD2, or FFMA2 with the kill scale in the general layout): a
-        // measured choice per slot width (tools/pack_sweep.sh, profiles/pack_sweep_b200.txt):
-        // faster at R = 20, 22, 26 (config 2's R=26: 5.4 -> 7.1 Tcells/s), slower at
-        // R = 14, 18, 24, 28, 32 (instruction schedule; registers are alike), equal elsewhere.
+        // measured choice (tools/pack_sweep.sh, tools/band_sweep.sh; profiles/pack_sweep_b200.txt,
+        // profiles/band_sweep_r1i.txt): in the aligned layouts faster at R = 20, 22, 26 (config
+        // 2's R=26: 6.6 -> 7.3 Tcells/s), slower at R = 16; in the general layout (per-slot
+        // kill scales, FFMA2 form) 3-15 % slower at every R with two CTAs per SM.
         static const char *pk = getenv("NNDTW_PACK");
-        const bool rule = c.R == 20 || c.R == 22 || c.R == 26;
+        const bool rule = c.km >= 1 && (c.R == 20 || c.R == 22 || c.R == 26);
         c.pack = pk ? pk[0] == '1' : rule;
     }
     static const bool verbose = getenv("NNDTW_VERBOSE") != nullptr;
