@@ -57,8 +57,10 @@ __device__ __forceinline__ float pin_reg(float v) {
 // 1 = aligned, G*R = 2w+2 (kill slot is the top lane's last register: one scale register,
 // edge masks); 2 = aligned and gpw*G = 32 (every lane used: rotating shuffles deliver the
 // neighbouring group's kill slot, so no edge masks are needed at all).
-// Two resident CTAs of 8 warps per SM need <= 128 registers: kept where that costs no spills
-// (R <= 24, or R = 26 in the aligned layouts); measured on config 2: 206.6 -> 198.7 ms.
+// A 128-register cap (launch bounds asking for two CTAs of 8 warps) where it costs no spills
+// (R <= 24, or R = 26 in the aligned layouts).  Shared memory still holds the SM to one CTA on
+// config 2 (8 groups x 2 padded rows = 164 KB), but the capped allocation schedules better:
+// 130 -> 126 registers, DTW 206.6 -> 198.2 ms (profiles/round1k_full.md).
 template <int R, int KM>
 constexpr int band_min_blocks() {
     return (R <= 24 || (R == 26 && KM >= 1)) ? 2 : 1;
