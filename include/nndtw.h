@@ -84,7 +84,9 @@ NNDTW_API int nndtw_check_finite(const float *x, int64_t n, int32_t *bad, void *
 /*
  * S1 -- envelopes, Eq. 3-4:
  *   upper[i][k] = max_{max(0,k-w) <= j <= min(L-1,k+w)} x[i][j],  lower = min over the same.
- * x: [n][L]; upper, lower: [n][L] outputs (bit-exact: min/max of floats are exact).
+ * x: [n][L]; upper, lower: [n][L] outputs (bit-exact: min/max of floats are exact); the
+ * outputs must not overlap x (series are staged through shared memory by persistent CTAs, so
+ * one series' output can be written before another's input is read).
  * kim: [n] output, nullable: the LB_Kim features of each series (nndtw_kim).
  * Precomputed "at training time".  Errors: E_ARG, E_LENGTH (L < 1), E_WINDOW.
  */
