@@ -1,7 +1,10 @@
 // envelopes.cu -- S1: upper/lower warping envelopes (Eq. 3-4) and LB_Kim features.
 //
-// Design: O(1) work per element independent of w, so the kernel is HBM-bound
-// (12 B per element: read x, write U and L).  Van Herk / Gil-Werman: in padded coordinates the
+// Design: O(1) work per element independent of w, so the kernels are HBM-bound
+// (12 B per element: read x, write U and L).  Two kernels: k_env_direct (w >= 16; chunk
+// prefix/suffix + a sparse table over chunk extremes, further below) and the van Herk kernel
+// k_envelopes (w < 16, L <= 256, or padded rows too large for shared memory), described here.
+// Van Herk / Gil-Werman: in padded coordinates the
 // clipped window [i-w, i+w] has length k = 2w+1; cutting the axis into segments of length k
 // aligned at padded position 0 (position p starts a segment iff (p+w) mod k == 0), every
 // window is a suffix of one segment plus a prefix of the next, so
