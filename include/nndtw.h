@@ -206,6 +206,14 @@ NNDTW_API int nndtw_dtw_batch(const float *a, const float *b, const int32_t *ia,
  * and S4/S5.  Neither flag: both phases in one call.  The answer does not change. */
 #define NNDTW_CLASSIFY_PHASE_SEED 8u
 #define NNDTW_CLASSIFY_PHASE_SEARCH 16u
+/* PHASE_SEARCH in two halves, so that shards can exchange their best-so-far in between:
+ * SEARCH_A runs S3 compaction and S4 on the survivors of the lowest-bound buckets (LB below a
+ * fixed fraction of the seeded best-so-far); the caller MIN-reduces key over the
+ * shards; SEARCH_B (same ws) takes that key and runs S4/S5 on the remaining survivors.  The
+ * union is PHASE_SEARCH's work; the answer does not change.  SEARCH_B synchronises the stream
+ * once (it reads the split point). */
+#define NNDTW_CLASSIFY_PHASE_SEARCH_A 32u
+#define NNDTW_CLASSIFY_PHASE_SEARCH_B 64u
 NNDTW_API size_t nndtw_classify_workspace_bytes(int64_t nq, int64_t nt, int32_t L, int32_t w);
 NNDTW_API int nndtw_classify(const float *q, int64_t nq, const float *t, const float *upper,
                    const float *lower, const nndtw_kim *tkim, int64_t nt, int64_t index_base,

@@ -99,6 +99,7 @@ struct ClassifyWs {
     float *lb;
     int64_t ldlb;
     unsigned long long *buckets;  // survivor-order buckets: count | base | fill
+    unsigned long long *split_count;  // SEARCH_B: survivors in the buckets after the split
     Item *seed_items;
     Item *items;
     unsigned long long item_cap;
@@ -132,6 +133,7 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
     W.ldlb = (nt + 3) / 4 * 4;
     W.lb = (float *)take(sizeof(float) * (size_t)nq * (size_t)W.ldlb);
     W.buckets = (unsigned long long *)take(sizeof(unsigned long long) * 3 * NBUCKET);
+    W.split_count = (unsigned long long *)take(sizeof(unsigned long long));
     W.seed_items = (Item *)take(sizeof(Item) * (2 * q1 + 1));
     W.item_cap = (unsigned long long)nq * (unsigned long long)nt + 1;
     W.items = (Item *)take(sizeof(Item) * (size_t)W.item_cap);
@@ -229,10 +231,24 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
 
     // Phases (sharded search, dist.py): SEED = init + S2 bound + S3 seed round, leaving the state
     // in ws; SEARCH = S3 compaction + S4/S5 survivors against the key passed in (the MIN over
-    // shards of the seed keys).  Neither flag: both, in one call.
-    const bool only_seed = (flags & NNDTW_CLASSIFY_PHASE_SEED) && !(flags & NNDTW_CLASSIFY_PHASE_SEARCH);
-    const bool only_search = (flags & NNDTW_CLASSIFY_PHASE_SEARCH) && !(flags & NNDTW_CLASSIFY_PHASE_SEED);
-    const bool do_seed = !only_search, do_search = !only_seed;
+    // shards of the seed keys), or the same in two halves SEARCH_A (compaction + the survivors
+    // of buckets < split) and SEARCH_B (the rest), with another MIN over shards in between.
+    // No phase flag: everything, in one call.
+    const unsigned phases = flags & (NNDTW_CLASSIFY_PHASE_SEED | NNDTW_CLASSIFY_PHASE_SEARCH |
+                                     NNDTW_CLASSIFY_PHASE_SEARCH_A | NNDTW_CLASSIFY_PHASE_SEARCH_B);
+    const bool all = phases == 0;
+    const bool do_seed = all || (flags & NNDTW_CLASSIFY_PHASE_SEED);
+    const bool whole = all || (flags & NNDTW_CLASSIFY_PHASE_SEARCH) ||
+                       ((flags & NNDTW_CLASSIFY_PHASE_SEARCH_A) && (flags & NNDTW_CLASSIFY_PHASE_SEARCH_B));
+    const bool do_compact = whole || (flags & NNDTW_CLASSIFY_PHASE_SEARCH_A);
+    const bool dtw_a = !whole && (flags & NNDTW_CLASSIFY_PHASE_SEARCH_A);
+    const bool dtw_b = !whole && (flags & NNDTW_CLASSIFY_PHASE_SEARCH_B);
+    const bool do_finish = whole || dtw_b;              // S5/S7 after the last survivors
+    static const int split_b = [] {
+        const char *e = getenv("NNDTW_SPLIT_BUCKET");  // experiments: the SEARCH_A/B split
+        const int b = e ? atoi(e) : NBUCKET / 4;
+        return b < 0 ? 0 : (b > NBUCKET ? NBUCKET : b);
+    }();
     const int keogh = (flags & NNDTW_CLASSIFY_BOUND_KEOGH) ? 1 : 0;
     const bool sym = (flags & NNDTW_CLASSIFY_BOUND_SYMMETRIC) != 0;
     TieLog log{W.log, W.log_count, W.log_cap, W.overflow};
@@ -273,22 +289,48 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
                           W.cells_prefix, nullptr, nullptr, st, sms);
         if ((rc = dtw_fail(rc, L, w))) return rc;
     }
-    if (nt > 0 && do_search) {
+    if (nt > 0 && do_compact) {
         // S3: prune + compact the survivors against the seeded best-so-far
         launch_compact(W.lb, W.ldlb, nq, nt, key, W.minkey, seed2, eps_p, W.items,
                        W.main_count, W.buckets, W.item_cap, sms, st);
     }
     tm.mark();  // 3
-    if (nt > 0 && do_search) {
+    if (nt > 0 && whole) {
         // S4/S5: DTW with early abandoning on the survivors
         rc = dispatch_dtw(q, t, nq, nt, W.items, W.main_count, W.item_cap, nullptr, nullptr, 0, L, w, 0,
                           key, index_base, eps_t, log, cnt, W.cells_prefix, nullptr, nullptr,
                           st, sms);
         if ((rc = dtw_fail(rc, L, w))) return rc;
+    } else if (nt > 0 && dtw_a) {
+        // the survivors of buckets < split_b: items [0, base[split_b]) (the bucket-major list)
+        const unsigned long long *na = split_b < NBUCKET ? W.buckets + NBUCKET + split_b
+                                                         : W.main_count;
+        rc = dispatch_dtw(q, t, nq, nt, W.items, na, W.item_cap, nullptr, nullptr, 0, L, w, 0,
+                          key, index_base, eps_t, log, cnt, W.cells_prefix, nullptr, nullptr,
+                          st, sms);
+        if ((rc = dtw_fail(rc, L, w))) return rc;
+    } else if (nt > 0 && dtw_b) {
+        // the rest: items [base[split_b], total) -- the offset is read on the host
+        unsigned long long h[2] = {0ull, 0ull};
+        if (split_b < NBUCKET)
+            cudaMemcpyAsync(&h[0], W.buckets + NBUCKET + split_b, 8, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(&h[1], W.main_count, 8, cudaMemcpyDeviceToHost, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_fail("classify split sync");
+        unsigned long long total = h[1] < W.item_cap ? h[1] : W.item_cap;
+        const unsigned long long a = split_b < NBUCKET ? (h[0] < total ? h[0] : total) : total;
+        const unsigned long long nbrest = total - a;
+        cudaMemcpyAsync(W.split_count, &nbrest, 8, cudaMemcpyHostToDevice, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_fail("classify split sync");
+        if (nbrest > 0) {
+            rc = dispatch_dtw(q, t, nq, nt, W.items + a, W.split_count, W.item_cap - a, nullptr,
+                              nullptr, 0, L, w, 0, key, index_base, eps_t, log, cnt,
+                              W.cells_prefix, nullptr, nullptr, st, sms);
+            if ((rc = dtw_fail(rc, L, w))) return rc;
+        }
     }
     tm.mark();  // 4
     if ((rc = cuda_fail("dtw"))) return rc;
-    if ((flags & NNDTW_CLASSIFY_EXACT) && nt > 0 && do_search)
+    if ((flags & NNDTW_CLASSIFY_EXACT) && nt > 0 && do_finish)
         exact_local(W, q, nq, t, nt, L, w, index_base, key, cnt, sms, st);
     tm.mark();  // 5
     if ((rc = cuda_fail("classify"))) return rc;
@@ -300,8 +342,10 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
             stats->lb_pairs += nq * nt;
             stats->rounds += 1;
         }
-        if (do_search) {
-            stats->survivors += (int64_t)h[CNT_N + 1];
+        // (the counters accumulate from the seed phase on: the call that finishes the survivor
+        // round reports them once)
+        if (do_compact) stats->survivors += (int64_t)h[CNT_N + 1];
+        if (do_finish) {
             stats->dtw_calls += (int64_t)h[CNT_ITEMS] + (int64_t)h[CNT_N];  // main + seed items
             stats->dtw_abandoned += (int64_t)h[CNT_ABANDONED];
             stats->cells += (int64_t)h[CNT_CELLS];

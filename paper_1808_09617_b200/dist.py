@@ -15,7 +15,12 @@ exact answer:
            -> lowest index among exact fp64 ties.
 
 All keys are < 2^63 (non-negative floats, indices < 2^31, "none" = INT64_MAX), so a signed
-int64 MIN is the unsigned MIN.  Messages are Q x 8 bytes per step.
+int64 MIN is the unsigned MIN.  Messages are Q x 8 bytes per step.  Optionally (split=True)
+the search runs in two halves (the survivors of the lowest-bound buckets first, then the rest)
+with one more key MIN between them, so that every shard's second half prunes and abandons
+against the best distances all shards found in their first half: at 8 shards 4 % fewer DTW
+cells, but the extra synchronisation point leaves the projected step time within 1 %
+(profiles/round1l_shard_sim.md), so it is off by default.
 
 The per-shard operations are injected (`ShardOps`) so that the combine protocol itself is
 tested on CPU with the gloo backend (tests/test_dist_gloo.py); `GpuShardOps` is the product
@@ -48,6 +53,9 @@ class ShardOps:
     # optional two-phase form of local_keys (seed keys, MIN over ranks, then the search)
     seed_keys = None
     search_keys = None
+    # optional split search (the lowest-bound survivors, MIN over ranks, then the rest)
+    search_a_keys = None
+    search_b_keys = None
 
     def refine(self, q, gkey):
         raise NotImplementedError
@@ -57,12 +65,15 @@ class ShardOps:
 
 
 class GpuShardOps(ShardOps):
-    def __init__(self, model: nndtw.Model, stats: bool = False, stream=None):
+    def __init__(self, model: nndtw.Model, stats: bool = False, stream=None, split: bool = False):
         self.model = model
         self.stats = stats
         self.stream = stream
         self.ws = None
         self.last_stats = None
+        if not split:  # one search phase (no mid-search exchange)
+            self.search_a_keys = None
+            self.search_b_keys = None
 
     def local_keys(self, q):
         key, ws, st = nndtw.classify_keys(self.model, q, exact=False, stats=self.stats,
@@ -85,6 +96,20 @@ class GpuShardOps(ShardOps):
         self.last_stats = nndtw.merge_stats(self.last_stats, st)
         return key
 
+    def search_a_keys(self, q, gseed):
+        key, _, st = nndtw.classify_keys(self.model, q, exact=False, stats=self.stats,
+                                         stream=self.stream, phase="search_a", key=gseed,
+                                         ws=self.ws)
+        self.last_stats = nndtw.merge_stats(self.last_stats, st)
+        return key
+
+    def search_b_keys(self, q, gkey):
+        key, _, st = nndtw.classify_keys(self.model, q, exact=False, stats=self.stats,
+                                         stream=self.stream, phase="search_b", key=gkey,
+                                         ws=self.ws)
+        self.last_stats = nndtw.merge_stats(self.last_stats, st)
+        return key
+
     def refine(self, q, gkey):
         return nndtw.classify_refine(self.model, q, self.ws, gkey, self.stream)
 
@@ -98,7 +123,12 @@ def combine(ops: ShardOps, q, group=None):
     if getattr(ops, "seed_keys", None) is not None:
         key = ops.seed_keys(q)
         dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)  # global seed best-so-far
-        key = ops.search_keys(q, key)
+        if getattr(ops, "search_a_keys", None) is not None:
+            key = ops.search_a_keys(q, key)  # the lowest-bound survivors
+            dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)  # global best so far
+            key = ops.search_b_keys(q, key)  # the rest, pruned by all shards' best
+        else:
+            key = ops.search_keys(q, key)
     else:
         key = ops.local_keys(q)
     dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
@@ -110,10 +140,12 @@ def combine(ops: ShardOps, q, group=None):
 
 
 def classify_sharded(model: nndtw.Model, q: torch.Tensor, labels_global: torch.Tensor,
-                     group=None, stats: bool = False, stream=None) -> nndtw.Prediction:
+                     group=None, stats: bool = False, stream=None,
+                     split: bool = False) -> nndtw.Prediction:
     """Exact 1-NN of every query against the union of all ranks' shards.  `model` holds this
-    rank's shard with index_base = its first global index; labels_global is replicated."""
-    ops = GpuShardOps(model, stats=stats, stream=stream)
+    rank's shard with index_base = its first global index; labels_global is replicated.
+    split: exchange the best-so-far once more in the middle of the survivor round."""
+    ops = GpuShardOps(model, stats=stats, stream=stream, split=split)
     out = combine(ops, q, group)
     idx, lab, d = nndtw.finalize(out, labels_global, key_format=1, stream=stream)
     return nndtw.Prediction(idx, lab, d, ops.last_stats)

@@ -26,6 +26,8 @@ NNDTW_CLASSIFY_BOUND_KEOGH = 2
 NNDTW_CLASSIFY_BOUND_SYMMETRIC = 4
 NNDTW_CLASSIFY_PHASE_SEED = 8
 NNDTW_CLASSIFY_PHASE_SEARCH = 16
+NNDTW_CLASSIFY_PHASE_SEARCH_A = 32
+NNDTW_CLASSIFY_PHASE_SEARCH_B = 64
 KEY_INIT = 0x7F800000FFFFFFFF
 
 
@@ -282,15 +284,16 @@ def classify_keys(model: Model, q: torch.Tensor, exact: bool = True, self_offset
 
     phase None runs everything; "seed" stops after the S3 seed round (keys = seed keys);
     "search" continues from a "seed" call's workspace `ws` with `key` = the MIN over shards
-    of the seed keys (updated in place and returned)."""
+    of the seed keys (updated in place and returned); "search_a" / "search_b" split "search"
+    in two (the lowest-bound survivors first), with another MIN over shards of `key` between."""
     _series(q, "q")
     nq, L = q.shape
     if L != model.L:
         raise NNDTWError("query length differs from train length (unequal lengths are out of "
                          "scope, reading C15)")
-    if phase == "search":
+    if phase in ("search", "search_a", "search_b"):
         if ws is None or key is None:
-            raise NNDTWError("phase 'search' needs the seed call's ws and the combined key")
+            raise NNDTWError(f"phase {phase!r} needs the seed call's ws and the combined key")
     else:
         ws = model.workspace(nq)
         key = torch.empty(nq, dtype=torch.int64, device=q.device)
@@ -298,7 +301,9 @@ def classify_keys(model: Model, q: torch.Tensor, exact: bool = True, self_offset
              (NNDTW_CLASSIFY_BOUND_KEOGH if model.bound == "keogh" else 0) |
              (NNDTW_CLASSIFY_BOUND_SYMMETRIC if model.symmetric else 0) |
              {None: 0, "seed": NNDTW_CLASSIFY_PHASE_SEED,
-              "search": NNDTW_CLASSIFY_PHASE_SEARCH}[phase])
+              "search": NNDTW_CLASSIFY_PHASE_SEARCH,
+              "search_a": NNDTW_CLASSIFY_PHASE_SEARCH_A,
+              "search_b": NNDTW_CLASSIFY_PHASE_SEARCH_B}[phase])
     st = Stats()
     _check(load().nndtw_classify(_ptr(q), nq, _ptr(model.t), _ptr(model.U), _ptr(model.Lo),
                                  _ptr(model.kim), model.t.shape[0], model.index_base,

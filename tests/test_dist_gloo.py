@@ -102,19 +102,35 @@ class OracleTwoPhaseShardOps(OracleShardOps):
         return torch.minimum(local, gseed)
 
 
+class OracleSplitShardOps(OracleTwoPhaseShardOps):
+    """The split search (GpuShardOps.search_a_keys / search_b_keys): the first half searches the
+    shard's candidates with the lowest bounds (here: the first half of its index range) from the
+    global seed, the keys are MIN-combined again, and the second half continues from that."""
+
+    def search_a_keys(self, Q, gseed):
+        local = self.local_keys(Q)  # (emulation: the full local search; the halves only order it)
+        return torch.minimum(local, gseed)
+
+    def search_b_keys(self, Q, gkey):
+        return torch.minimum(self.local_keys(Q), gkey)
+
+
 def _worker(rank, world, port, T, Q, w, jitter, ret, two_phase=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1808_09617_b200.dist import combine, shard_range
     lo, hi = shard_range(T.shape[0], rank, world)
-    ops = (OracleTwoPhaseShardOps if two_phase else OracleShardOps)(T, lo, hi, w, jitter)
+    cls = {False: OracleShardOps, True: OracleTwoPhaseShardOps,
+           "split": OracleSplitShardOps}[two_phase]
+    ops = cls(T, lo, hi, w, jitter)
     out = combine(ops, torch.as_tensor(Q))
     ret[rank] = [int(x) >> 32 for x in out]
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,two_phase", [(2, False), (3, False), (2, True), (3, True)])
+@pytest.mark.parametrize("world,two_phase", [(2, False), (3, False), (2, True), (3, True),
+                                              (2, "split"), (3, "split")])
 def test_sharded_combine_matches_global_nn(oracle_lib, world, two_phase):
     rng = np.random.default_rng(world)
     L, w = 10, 2

@@ -318,13 +318,14 @@ def test_loocv_config3_full_sampled(dev, oracle_lib):
 
 # ---------------------------------------------------------------- S6 shard protocol (1 GPU)
 @pytest.mark.parametrize("nshards", [2, 3])
-@pytest.mark.parametrize("two_phase", [False, True])
+@pytest.mark.parametrize("two_phase", [False, True, "split"])
 @pytest.mark.parametrize("data", ["int", "config1"])
 def test_shard_protocol_through_abi(dev, oracle_lib, nshards, two_phase, data):
     """The sharded path of dist.py through the real C ABI, shards run one after another on one
     GPU and combined with torch.minimum (= the int64 MIN all-reduce): refine and resolve must
     give the exact global 1-NN, including exact ties split across shards.  two_phase: the seed
-    keys are MIN-combined first and every shard searches from the global seed."""
+    keys are MIN-combined first and every shard searches from the global seed; "split": the
+    search in two halves (PHASE_SEARCH_A / _B) with another MIN between them."""
     import torch
     from paper_1808_09617_b200 import nndtw
     from paper_1808_09617_b200.dist import shard_range
@@ -352,8 +353,17 @@ def test_shard_protocol_through_abi(dev, oracle_lib, nshards, two_phase, data):
         gseed = seeds[0][0].clone()
         for k, _, _ in seeds[1:]:
             gseed = torch.minimum(gseed, k)
-        outs = [nndtw.classify_keys(m, q, exact=False, phase="search", key=gseed.clone(), ws=ws)
-                for m, (_, ws, _) in zip(models, seeds)]
+        if two_phase == "split":
+            mids = [nndtw.classify_keys(m, q, exact=False, phase="search_a", key=gseed.clone(),
+                                        ws=ws) for m, (_, ws, _) in zip(models, seeds)]
+            gmid = mids[0][0].clone()
+            for k, _, _ in mids[1:]:
+                gmid = torch.minimum(gmid, k)
+            outs = [nndtw.classify_keys(m, q, exact=False, phase="search_b", key=gmid.clone(),
+                                        ws=ws) for m, (_, ws, _) in zip(models, seeds)]
+        else:
+            outs = [nndtw.classify_keys(m, q, exact=False, phase="search", key=gseed.clone(),
+                                        ws=ws) for m, (_, ws, _) in zip(models, seeds)]
     else:
         outs = [nndtw.classify_keys(m, q, exact=False) for m in models]
     gkey = outs[0][0].clone()

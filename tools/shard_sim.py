@@ -38,8 +38,8 @@ def main():
     N = tr.shape[0]
     rows = []
     for G in [int(x) for x in args.gpus.split(",")]:
-        for glob in (False, True):
-            if G == 1 and glob:
+        for mode in ("own", "seed", "split"):
+            if G == 1 and mode != "own":
                 continue
             models = []
             for r in range(G):
@@ -50,50 +50,83 @@ def main():
             for m in models:
                 nndtw.classify_keys(m, q, exact=False)
             torch.cuda.synchronize()
-            t_seed, t_search, st_all = [], [], []
-            seeds = []
+
+            def timed(fn):
+                e0 = ev()
+                out = fn()
+                e1 = ev()
+                torch.cuda.synchronize()
+                return out, e0.elapsed_time(e1)
+
+            def gmin(keys):
+                g = keys[0].clone()
+                for k in keys[1:]:
+                    g = torch.minimum(g, k)
+                return g
+
+            seeds, t_seed = [], []
             for m in models:
-                e0 = ev()
-                k, ws, st = nndtw.classify_keys(m, q, exact=False, stats=True, phase="seed")
-                e1 = ev()
-                torch.cuda.synchronize()
-                t_seed.append(e0.elapsed_time(e1))
-                seeds.append((k, ws, st))
-            gseed = seeds[0][0].clone()
-            for k, _, _ in seeds[1:]:
-                gseed = torch.minimum(gseed, k)
-            for m, (k, ws, st) in zip(models, seeds):
-                start = gseed.clone() if glob else k
-                e0 = ev()
-                _, _, st2 = nndtw.classify_keys(m, q, exact=False, stats=True, phase="search",
-                                                key=start, ws=ws)
-                e1 = ev()
-                torch.cuda.synchronize()
-                t_search.append(e0.elapsed_time(e1))
-                st_all.append(nndtw.merge_stats(st, st2))
-            per = [a + b for a, b in zip(t_seed, t_search)]
-            row = {"gpus": G, "global_seed": glob, "max_shard_ms": max(per),
-                   "sum_shard_ms": sum(per), "cells": sum(s["cells"] for s in st_all),
+                out, t = timed(lambda: nndtw.classify_keys(m, q, exact=False, stats=True,
+                                                           phase="seed"))
+                seeds.append(out)
+                t_seed.append(t)
+            gseed = gmin([k for k, _, _ in seeds])
+            phase_ms = [max(t_seed)]
+            st_all = [st for _, _, st in seeds]
+            if mode == "split":
+                mids, t_a = [], []
+                for m, (k, ws, st) in zip(models, seeds):
+                    out, t = timed(lambda: nndtw.classify_keys(
+                        m, q, exact=False, stats=True, phase="search_a", key=gseed.clone(),
+                        ws=ws))
+                    mids.append(out)
+                    t_a.append(t)
+                gmid = gmin([k for k, _, _ in mids])
+                t_b = []
+                for i, (m, (k, ws, st)) in enumerate(zip(models, seeds)):
+                    (_, _, st2), t = timed(lambda: nndtw.classify_keys(
+                        m, q, exact=False, stats=True, phase="search_b", key=gmid.clone(),
+                        ws=ws))
+                    t_b.append(t)
+                    st_all[i] = nndtw.merge_stats(nndtw.merge_stats(st_all[i], mids[i][2]), st2)
+                phase_ms += [max(t_a), max(t_b)]
+            else:
+                t_s = []
+                for i, (m, (k, ws, st)) in enumerate(zip(models, seeds)):
+                    start = gseed.clone() if mode == "seed" else k
+                    (_, _, st2), t = timed(lambda: nndtw.classify_keys(
+                        m, q, exact=False, stats=True, phase="search", key=start, ws=ws))
+                    t_s.append(t)
+                    st_all[i] = nndtw.merge_stats(st_all[i], st2)
+                phase_ms += [max(t_s)]
+            step = sum(phase_ms)  # the all-reduces between phases synchronise the shards
+            row = {"gpus": G, "exchange": mode, "step_ms": step,
+                   "phase_ms": [round(x, 2) for x in phase_ms],
+                   "cells": sum(s["cells"] for s in st_all),
                    "dtw_calls": sum(s["dtw_calls"] for s in st_all),
-                   "queries_s_projected": q.shape[0] / (max(per) / 1e3)}
+                   "queries_s_projected": q.shape[0] / (step / 1e3)}
             rows.append(row)
             print(json.dumps(row), flush=True)
     if args.out:
-        base = rows[0]["max_shard_ms"]
+        base = rows[0]["step_ms"]
         lines = ["# Projected multi-GPU scaling of config 2 (one B200, shards run in turn)\n",
-                 "Each shard runs its S2-S5 work on its contiguous train slice (dist.py); the "
-                 "projected G-GPU step time is the slowest shard (the three Q x 8-byte MIN "
-                 "all-reduces, tens of microseconds on NVLink, are not included).  'global "
-                 "seed': shards prune against the MIN over shards of the seed keys "
-                 "(NNDTW_CLASSIFY_PHASE_SEED / _SEARCH); otherwise each against its own seed.\n",
-                 "| GPUs | global seed | slowest shard ms | projected queries/s | "
+                 "Each shard runs its S2-S5 work on its contiguous train slice (dist.py), phase by "
+                 "phase; a G-GPU step is the sum over phases of the slowest shard (the Q x 8-byte "
+                 "MIN all-reduces between phases synchronise the ranks; their tens of "
+                 "microseconds on NVLink are not included).  Exchange 'own': every shard prunes "
+                 "against its own seed; 'seed': against the MIN over shards of the seed keys "
+                 "(NNDTW_CLASSIFY_PHASE_SEED / _SEARCH); 'split': in addition the survivor round "
+                 "runs in two halves with another MIN between them (PHASE_SEARCH_A / _B, the "
+                 "default of dist.py).\n",
+                 "| GPUs | exchange | step ms (phases) | projected queries/s | "
                  "projected efficiency | DTW cells (all shards) | DTW calls |",
                  "|---|---|---|---|---|---|---|"]
         for r in rows:
-            eff = base / (r["max_shard_ms"] * r["gpus"])
-            lines.append(f"| {r['gpus']} | {'yes' if r['global_seed'] else 'no'} | "
-                         f"{r['max_shard_ms']:.1f} | {r['queries_s_projected']:.0f} | "
-                         f"{eff:.2f} | {r['cells']:.3e} | {r['dtw_calls']:.3e} |")
+            eff = base / (r["step_ms"] * r["gpus"])
+            ph = " + ".join(f"{x:.1f}" for x in r["phase_ms"])
+            lines.append(f"| {r['gpus']} | {r['exchange']} | {r['step_ms']:.1f} ({ph}) | "
+                         f"{r['queries_s_projected']:.0f} | {eff:.2f} | {r['cells']:.3e} | "
+                         f"{r['dtw_calls']:.3e} |")
         with open(args.out, "w") as f:
             f.write("\n".join(lines) + "\n")
 
