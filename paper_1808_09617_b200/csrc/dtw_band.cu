@@ -429,7 +429,18 @@ static BandChoice choose_band(int w, int L) {
         int G = (2 * w + 2 + R - 1) / R;
         if (G > 32) continue;
         bool aligned = (G * R == 2 * w + 2);
-        if (!aligned && R > 24) continue;  // register budget of the general variant
+        // Measured pruning of the candidate list (profiles/round1l_band_layout_check_L300.txt,
+        // band_sweep_r1i.txt): R = 16 and R = 32 are the slowest widths in every sweep; general
+        // (unaligned) layouts wider than R = 24 pay for their per-slot scale registers and win
+        // only where no R <= 24 layout fits two groups in a warp (2w+2 > 16*24): w = 192..234
+        // at L = 300 go from one group per warp (2.2-3.9 Tcells/s) to two (4.3-4.5).
+        static const int gmax = [] {  // experiments: widest general (unaligned) layout
+            const char *e = getenv("NNDTW_BAND_GENERAL_MAX");
+            return e ? atoi(e) : 30;
+        }();
+        if (!rforce && (R == 16 || R == 32)) continue;
+        if (!aligned && R > gmax) continue;  // register budget of the general variant
+        if (!aligned && R > 24 && !rforce && (2 * w + 2 + 23) / 24 <= 16) continue;
         BandChoice c{};
         c.R = R;
         c.G = G;

@@ -253,7 +253,11 @@ def test_loocv_reduced(dev, oracle_lib):
 @pytest.mark.parametrize("L,ws", [(1024, (1023, 600, 515)), (2048, (2047, 1500)),
                                   (700, (699, 520)), (1100, (1099,)), (513, (512,)),
                                   (600, (599, 520)), (1792, (1791, 600)), (256, (255,)),
-                                  (3001, (3000, 2000))])
+                                  (3001, (3000, 2000)),
+                                  # band kernel, general layouts wider than R = 24 (two groups
+                                  # per warp from 2w+2 > 384, one group up to 2w+2 = 960)
+                                  (300, (192, 210, 225, 255)), (1024, (200, 400)),
+                                  (2048, (409,))])
 def test_dtw_batch_long_windows(dev, oracle_lib, L, ws):
     from paper_1808_09617_b200 import nndtw
     rng = np.random.default_rng(L)
