@@ -374,6 +374,15 @@ def main():
     acc_tot["ms_lb"] = acc_tot["ms_lb"] / world
     value = Q * args.steps / (ms / 1e3)
 
+    # ---- per-level prune counters (one untimed call; the level pass is not in the step) ----
+    levels = None
+    if not sharded:
+        model_l = nndtw.Model(train_d, labels_d[lo:hi], w, V, index_base=lo, check=False)
+        st_l = nndtw.classify(model_l, test_d, stats=True, check=False, level_stats=True).stats
+        levels = {k: st_l[k] for k in ("pruned_kim", "pruned_bands", "pruned_keogh",
+                                       "survivors")}
+        del model_l
+
     # ---- e2e through the public API with host buffers ---------------------------------
     e2e = None
     if not args.no_e2e:
@@ -428,7 +437,7 @@ def main():
     lb_peak = lb_pair_col_peak(num_sms, sm_mhz)
     dominant = "dtw" if acc_tot["ms_dtw"] >= acc_tot["ms_lb"] else "lb"
     traffic = ncu_traffic()
-    dtw_kernel = "k_dtw_band" if 2 * min(w, L - 1) + 2 <= 1024 else "k_dtw_strip"
+    dtw_kernel = lib.nndtw_dtw_kernel_name(L, w).decode()  # the kernel dispatch_dtw runs
     roof_dtw = {"kernel": f"{dtw_kernel} (S4 survivor round)", "bound": "alu",
                 "achieved": dtw_gcups, "peak": peak_cells, "unit": "Gcells/s",
                 "frac": dtw_gcups / peak_cells if peak_cells else None,
@@ -472,8 +481,8 @@ def main():
             "dtw_gcups": dtw_gcups,
             "effective_gcups": Q * N * (L * (2 * w + 1) - w * (w + 1)) /
             (ms / args.steps * 1e-3) / 1e9,
-            "counters_per_step": {k: acc_tot[k] / args.steps for k in
-                                  ("lb_pairs", "dtw_calls", "cells")},
+            "counters_per_step": {**{k: acc_tot[k] / args.steps for k in
+                                     ("lb_pairs", "dtw_calls", "cells")}, **(levels or {})},
             "gpu_launches": launches, "clocks": clocks, "e2e": e2e}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_oracle(ds, w, V)

@@ -18,8 +18,9 @@
  *  - The window w is absolute (reading C4 resolves fractions); w >= L-1 is clamped to L-1,
  *    which is unconstrained DTW (reading C3).  w = 0 is the squared Euclidean distance.
  *  - Return value: NNDTW_OK or an NNDTW_E_* code; nndtw_last_error() gives a thread-local
- *    message.  No C++ exception crosses the ABI.  Inputs must be finite (the Python layer
- *    checks; NaN would silently be dropped by fminf).
+ *    message.  No C++ exception crosses the ABI.  Inputs must be finite with |x| < 2^36
+ *    (nndtw_check_finite; the Python layer checks: NaN would silently be dropped by fminf and
+ *    larger magnitudes break the DTW kernels' +inf pads).
  */
 #ifndef NNDTW_H
 #define NNDTW_H
@@ -45,7 +46,7 @@ extern "C" {
 #define NNDTW_E_WORKSPACE 5  /* ws too small */
 #define NNDTW_E_CUDA 6       /* a CUDA runtime error (message has the name) */
 #define NNDTW_E_ARCH 7       /* the current device is not sm_100 */
-#define NNDTW_E_INDEX 8      /* a global train index does not fit in 32 bits */
+#define NNDTW_E_INDEX 8      /* a global train index is >= 2^31 (index_base + nt > 2^31 - 1) */
 
 /* Per-series LB_Kim features (sum variant P:619-621, reading C7):
  * min / max value and their lowest indices (ties -> lowest index).  First and last values are
@@ -60,13 +61,23 @@ typedef struct {
 typedef struct {
     int64_t lb_pairs;       /* (query, train) pairs whose cascade bound was computed */
     int64_t survivors;      /* pairs with LB <= bsf*(1+eps_p) after the seed round */
+    /* Pairs pruned by each level of the cascade against the seeded best-so-far
+     * bsf*(1+eps_p): LB_Kim already exceeds it; else the boundary terms + bands of
+     * Algorithm 1 exceed it (its line-12 abort); else the full bound with
+     * the LB_Keogh bridge does.  Seed pairs and the leave-one-out self pair are not counted, so
+     * lb_pairs = pruned_kim + pruned_bands + pruned_keogh + survivors + seeds (+ self pairs).
+     * Filled only under NNDTW_CLASSIFY_LEVEL_STATS (an extra bands-only pass over the pairs,
+     * timed in ms_other); -1 otherwise. */
+    int64_t pruned_kim, pruned_bands, pruned_keogh;
     int64_t dtw_calls;      /* DTW work items started (seeds + survivors) */
     int64_t dtw_abandoned;  /* survivor items stopped by early abandoning */
     int64_t cells;          /* in-band DP cells on the diagonals the survivor round processed */
     int64_t near_tie_pairs; /* pairs re-ranked in fp64 (reading C16) */
     int32_t rounds;         /* DTW rounds run (seed round included) */
     int32_t launches;       /* kernel launches issued by the call */
-    /* CUDA-event stage times on the call's stream: ms_lb = the LB cascade kernel, ms_dtw = the
+    /* CUDA-event stage times on the call's stream: ms_envelopes = the query-side S1 work (Kim
+     * features, and the queries' envelopes for the symmetric bound; the train envelopes are
+     * built before the call), ms_lb = the LB cascade kernel(s), ms_dtw = the
      * survivor-round DTW kernel, ms_other = everything else (seed round, compaction, S7). */
     float ms_envelopes, ms_lb, ms_dtw, ms_other;
 } nndtw_stats;
@@ -76,9 +87,15 @@ NNDTW_API const char *nndtw_last_error(void);
 NNDTW_API int nndtw_version(void);
 /* Number of kernels this library has launched in the process so far (bench bookkeeping). */
 NNDTW_API int64_t nndtw_launch_count(void);
+/* Name of the S4 kernel nndtw_dtw_batch / nndtw_classify run for (L, w): "k_dtw_w0" (w = 0,
+ * squared ED), "k_dtw_band" (anti-diagonal band wavefront) or "k_dtw_strip" (row strips, long
+ * windows); "" for invalid arguments.  Host-only (bench / profiling bookkeeping). */
+NNDTW_API const char *nndtw_dtw_kernel_name(int32_t L, int32_t w);
 /* NNDTW_OK if the current device is sm_100 (B200); NNDTW_E_ARCH otherwise. */
 NNDTW_API int nndtw_check_device(void);
-/* *bad (device int32, caller-zeroed) is set to 1 if x [n] holds a NaN or infinity. */
+/* *bad (device int32, caller-zeroed) is set to 1 if x [n] holds a NaN, an infinity or a value
+ * with |x| >= 2^36.  Input precondition of every DTW entry point: the kernels' out-of-matrix
+ * shared-memory pads (+-2^64*k) rely on (pad - x)^2 overflowing to +inf. */
 NNDTW_API int nndtw_check_finite(const float *x, int64_t n, int32_t *bad, void *stream);
 
 /*
@@ -175,7 +192,8 @@ NNDTW_API int nndtw_dtw_batch(const float *a, const float *b, const int32_t *ia,
 /*
  * S2-S7 -- 1-NN search of every query against one train shard.
  * Key format: key[i] = (float bits of the squared distance << 32) | global train index;
- * global index = index_base + local index (< 2^32).  Non-negative floats order like their
+ * global index = index_base + local index (< 2^31, else NNDTW_E_INDEX: format-1 keys put the
+ * index in the high half and must stay non-negative as int64).  Non-negative floats order like their
  * bits, so an unsigned (or signed int64: bit 63 is 0) MIN over keys gives the smallest
  * distance with ties to the lowest index (reading C13) -- the shard combine of S6.
  * Stages: LB cascade for all pairs (S2); seed = DTW to the argmin-LB candidate (S3); prune
@@ -214,6 +232,9 @@ NNDTW_API int nndtw_dtw_batch(const float *a, const float *b, const int32_t *ia,
  * once (it reads the split point). */
 #define NNDTW_CLASSIFY_PHASE_SEARCH_A 32u
 #define NNDTW_CLASSIFY_PHASE_SEARCH_B 64u
+/* flags & NNDTW_CLASSIFY_LEVEL_STATS (with non-NULL stats): fill the per-level prune counters
+ * pruned_kim / pruned_bands / pruned_keogh (one extra bands-only pass, no bridge). */
+#define NNDTW_CLASSIFY_LEVEL_STATS 128u
 NNDTW_API size_t nndtw_classify_workspace_bytes(int64_t nq, int64_t nt, int32_t L, int32_t w);
 NNDTW_API int nndtw_classify(const float *q, int64_t nq, const float *t, const float *upper,
                    const float *lower, const nndtw_kim *tkim, int64_t nt, int64_t index_base,

@@ -420,7 +420,8 @@ void oracle_loocv(const float *X, const int32_t *labels, int64_t n, int L,
         run_pool(&J, threads);
         int64_t e = 0;
         for (int64_t q = 0; q < nq; ++q) {
-            if (labels[idx[q]] != labels[q_begin + q]) ++e;
+            /* no other series (n = 1): no neighbour, counted as an error (C17) */
+            if (idx[q] < 0 || labels[idx[q]] != labels[q_begin + q]) ++e;
             if (nn_out) nn_out[(int64_t)p * nq + q] = idx[q];
         }
         errors[p] = e;

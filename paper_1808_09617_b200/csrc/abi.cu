@@ -31,11 +31,13 @@ void count_launch(int n, const char *who) {
 int64_t launches_total() { return g_launches.load(std::memory_order_relaxed); }
 
 // ---- finite check (input validation for the Python layer) -----------------------------------
+// Flags NaN, +-inf and |x| >= 2^36: the DTW kernels' out-of-matrix pads (+-2^64*k, see
+// dtw_band.cu) must square to +inf against every real value, which holds for |x| < 2^36.
 __global__ void k_check_finite(const float *x, int64_t n, int32_t *bad) {
     int found = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        if (!isfinite(x[i])) found = 1;
+        if (!(fabsf(x[i]) < 0x1p36f)) found = 1;
     if (__any_sync(0xffffffffu, found) && (threadIdx.x & 31) == 0) *bad = 1;
 }
 
@@ -220,8 +222,9 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     if (w > L - 1) w = L - 1;
     if (nq > 0 && (!q || !key || !ws)) return fail(NNDTW_E_ARG, "null pointer argument");
     if (nt > 0 && (!t || !U || !Lo || !tkim)) return fail(NNDTW_E_ARG, "null pointer argument");
-    if (index_base < 0 || index_base + nt > 0xffffffffll)
-        return fail(NNDTW_E_INDEX, "global train indices must fit in 32 bits");
+    if (index_base < 0 || index_base + nt > 0x7fffffffll)
+        return fail(NNDTW_E_INDEX, "global train indices must be < 2^31 (signed int64 shard "
+                                   "combine of (index << 32) keys)");
     ClassifyWs W = classify_layout(ws, nq, nt, L);
     if (ws_bytes < W.bytes) return fail(NNDTW_E_WORKSPACE, "workspace too small");
     if (nq == 0) return NNDTW_OK;
@@ -263,23 +266,26 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         launch_fill_u64(W.resolve_out, nq, kNone64, st);
         cudaMemsetAsync(W.overflow, 0, 4 * (size_t)nq, st);
         launch_cells_prefix(L, w, W.cells_prefix, st);
-        launch_series_stats(q, nq, L, W.qkim, st);
     }
     tm.mark();  // 1
+    if (do_seed) {  // query-side S1: Kim features (+ envelopes for the symmetric bound)
+        launch_series_stats(q, nq, L, W.qkim, st);
+        if (nt > 0 && sym) launch_envelopes(q, nq, L, w, W.qU, W.qL, nullptr, st);
+    }
+    tm.mark();  // 2
     if (do_seed) {
         // S2: cascade bound for all pairs + per-query argmin-LB candidate
         if (nt > 0 && launch_lb(q, nq, W.qkim, t, U, Lo, tkim, nt, L, w, v, 1, self_offset,
                                 W.lb, W.ldlb, sym ? nullptr : W.minkey, st, keogh))
             return fail(NNDTW_E_ARG, "too many train series for one launch");
         if (nt > 0 && sym) {  // second direction of the symmetric bound, then the seed argmin
-            launch_envelopes(q, nq, L, w, W.qU, W.qL, nullptr, st);
             if (launch_lb(t, nt, nullptr, q, W.qU, W.qL, nullptr, nq, L, w, v, 0, -1, W.lb,
                           W.ldlb, nullptr, st, keogh, 1))
                 return fail(NNDTW_E_ARG, "too many queries for one launch");
             launch_row_argmin(W.lb, W.ldlb, nq, nt, W.minkey, st);
         }
     }
-    tm.mark();  // 2
+    tm.mark();  // 3
     if ((rc = cuda_fail("lb"))) return rc;
     if (nt > 0 && do_seed) {
         // S3: seed round (argmin-LB candidate, plus seed2 if given)
@@ -289,12 +295,19 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
                           W.cells_prefix, nullptr, nullptr, st, sms);
         if ((rc = dtw_fail(rc, L, w))) return rc;
     }
+    const bool level_stats = stats != nullptr && (flags & NNDTW_CLASSIFY_LEVEL_STATS) != 0;
+    if (nt > 0 && do_compact && level_stats) {
+        // stats: pairs pruned per cascade level against the same threshold as the compaction
+        launch_lb_level_counts(q, nq, W.qkim, t, tkim, nt, L, w, v, 1, keogh, self_offset, W.lb,
+                               W.ldlb, key, W.minkey, seed2, eps_p,
+                               W.counters + CNT_PRUNED_KIM, st);
+    }
     if (nt > 0 && do_compact) {
         // S3: prune + compact the survivors against the seeded best-so-far
         launch_compact(W.lb, W.ldlb, nq, nt, key, W.minkey, seed2, eps_p, W.items,
                        W.main_count, W.buckets, W.item_cap, sms, st);
     }
-    tm.mark();  // 3
+    tm.mark();  // 4
     if (nt > 0 && whole) {
         // S4/S5: DTW with early abandoning on the survivors
         rc = dispatch_dtw(q, t, nq, nt, W.items, W.main_count, W.item_cap, nullptr, nullptr, 0, L, w, 0,
@@ -328,11 +341,11 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
             if ((rc = dtw_fail(rc, L, w))) return rc;
         }
     }
-    tm.mark();  // 4
+    tm.mark();  // 5
     if ((rc = cuda_fail("dtw"))) return rc;
     if ((flags & NNDTW_CLASSIFY_EXACT) && nt > 0 && do_finish)
         exact_local(W, q, nq, t, nt, L, w, index_base, key, cnt, sms, st);
-    tm.mark();  // 5
+    tm.mark();  // 6
     if ((rc = cuda_fail("classify"))) return rc;
     if (stats) {
         unsigned long long h[CNT_N + 3];
@@ -345,6 +358,11 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         // (the counters accumulate from the seed phase on: the call that finishes the survivor
         // round reports them once)
         if (do_compact) stats->survivors += (int64_t)h[CNT_N + 1];
+        if (do_compact && level_stats) {
+            stats->pruned_kim = (stats->pruned_kim < 0 ? 0 : stats->pruned_kim) + (int64_t)h[CNT_PRUNED_KIM];
+            stats->pruned_bands = (stats->pruned_bands < 0 ? 0 : stats->pruned_bands) + (int64_t)h[CNT_PRUNED_BANDS];
+            stats->pruned_keogh = (stats->pruned_keogh < 0 ? 0 : stats->pruned_keogh) + (int64_t)h[CNT_PRUNED_KEOGH];
+        }
         if (do_finish) {
             stats->dtw_calls += (int64_t)h[CNT_ITEMS] + (int64_t)h[CNT_N];  // main + seed items
             stats->dtw_abandoned += (int64_t)h[CNT_ABANDONED];
@@ -354,9 +372,10 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         }
         stats->launches += (int32_t)(launches_total() - launches0);
         if (outer_tm == nullptr) {
-            stats->ms_lb += tm.ms(1, 2);
-            stats->ms_dtw += tm.ms(3, 4);
-            stats->ms_other += tm.ms(0, 1) + tm.ms(2, 3) + tm.ms(4, 5);
+            stats->ms_envelopes += tm.ms(1, 2);
+            stats->ms_lb += tm.ms(2, 3);
+            stats->ms_dtw += tm.ms(4, 5);
+            stats->ms_other += tm.ms(0, 1) + tm.ms(3, 4) + tm.ms(5, 6);
         }
     }
     return NNDTW_OK;
@@ -397,7 +416,13 @@ static LoocvWs loocv_layout(void *base, int64_t n, int L, int64_t nq) {
 extern "C" {
 
 const char *nndtw_last_error(void) { return g_err.c_str(); }
-int nndtw_version(void) { return 1; }
+int nndtw_version(void) { return 2; }
+
+const char *nndtw_dtw_kernel_name(int32_t L, int32_t w) {
+    if (L < 2 || w < 0) return "";
+    static const char *names[3] = {"k_dtw_w0", "k_dtw_band", "k_dtw_strip"};
+    return names[dtw_kernel_kind(L, w)];
+}
 int64_t nndtw_launch_count(void) { return launches_total(); }
 
 int nndtw_check_device(void) {
@@ -545,7 +570,10 @@ int nndtw_classify(const float *q, int64_t nq, const float *t, const float *uppe
                    const float *lower, const nndtw_kim *tkim, int64_t nt, int64_t index_base,
                    int64_t self_offset, int32_t L, int32_t w, int32_t v, uint32_t flags,
                    void *ws, size_t ws_bytes, uint64_t *key, nndtw_stats *stats, void *stream) {
-    if (stats) std::memset(stats, 0, sizeof *stats);
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        stats->pruned_kim = stats->pruned_bands = stats->pruned_keogh = -1;
+    }
     return classify_impl(q, nq, t, upper, lower, tkim, nt, index_base, self_offset, L, w, v,
                          flags, nullptr, ws, ws_bytes, (unsigned long long *)key, stats,
                          (cudaStream_t)stream);
@@ -633,7 +661,10 @@ int nndtw_loocv_window(const float *x, const int32_t *labels, int64_t n, int32_t
     LoocvWs W = loocv_layout(ws, n, L, nq);
     if (ws_bytes < W.bytes) return fail(NNDTW_E_WORKSPACE, "workspace too small");
     cudaStream_t st = (cudaStream_t)stream;
-    if (stats) std::memset(stats, 0, sizeof *stats);
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        stats->pruned_kim = stats->pruned_bands = stats->pruned_keogh = -1;
+    }
     if (nq == 0 || nw == 0) return NNDTW_OK;
     const float *qx = x + q_begin * (int64_t)L;
     cudaEvent_t e0, e1, e2;

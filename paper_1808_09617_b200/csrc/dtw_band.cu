@@ -418,7 +418,17 @@ static void band_geometry(int R, int G, int L, int w, BandChoice &c) {
 // edge-cell chain (shuffle + min + fma, ~38 cycles) bounds a warp to >= 38R cycles per
 // period.  Useful cells per SMSP-cycle = wps*gpw*R*(w+1/2)*slot_util / max(wps*issue, 38R),
 // wps = resident warps per scheduler (shared memory / register limited).
+static BandChoice choose_band_pass(int w, int L, bool all_widths);
+
 static BandChoice choose_band(int w, int L) {
+    BandChoice c = choose_band_pass(w, L, false);
+    // R = 16 / 32 are excluded only while another width fits: at 2w+2 = 1024 (w = 511) the
+    // aligned R = 32, G = 32 layout is the only band layout
+    if (c.R == 0) c = choose_band_pass(w, L, true);
+    return c;
+}
+
+static BandChoice choose_band_pass(int w, int L, bool all_widths) {
     BandChoice best{};
     best.R = 0;
     double bt = 0;
@@ -438,7 +448,7 @@ static BandChoice choose_band(int w, int L) {
             const char *e = getenv("NNDTW_BAND_GENERAL_MAX");
             return e ? atoi(e) : 30;
         }();
-        if (!rforce && (R == 16 || R == 32)) continue;
+        if (!rforce && !all_widths && (R == 16 || R == 32)) continue;
         if (!aligned && R > gmax) continue;  // register budget of the general variant
         if (!aligned && R > 24 && !rforce && (2 * w + 2 + 23) / 24 <= 16) continue;
         BandChoice c{};
@@ -633,6 +643,24 @@ static int launch_dtw_w0(BandParams &p, cudaStream_t st, int num_sms) {
     return 0;
 }
 
+// Which S4 kernel runs for (L, w): 0 = k_dtw_w0, 1 = k_dtw_band, 2 = k_dtw_strip.
+int dtw_kernel_kind(int L, int w) {
+    if (w > L - 1) w = L - 1;
+    if (w == 0) return 0;
+    // Full window (w = L-1): the band sweeps (w+1)(2L-1) slot-cells for L^2 cells (50% useful)
+    // while the row-strip kernel computes L^2 unmasked cells, so it wins when its strips are
+    // nearly full (measured: L=256, w=255: 1.9 -> 4.4 Tcells/s; L=300: 3.6 -> 4.4; L=384: 2.8 -> 5.1;
+    // L=128 (one half-empty strip): 2.6 -> 1.9, so the band stays there).
+    static const char *fs = getenv("NNDTW_FORCE_STRIP");  // experiments: 1 = strip, 0 = band
+    bool strip = false;
+    if (w >= L - 1) {
+        const int H = 32 * strip_rows_per_lane(L);
+        strip = (long long)((L + H - 1) / H) * H * 100 <= (long long)L * 112;  // <= 12% idle rows
+    }
+    if (fs) strip = fs[0] == '1';
+    return (band_supported(w, L) && !strip) ? 1 : 2;
+}
+
 int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const Item *items,
                  const unsigned long long *nitems_dev, unsigned long long item_cap,
                  const int32_t *ia, const int32_t *ib, int64_t nitems_host, int L, int w,
@@ -667,19 +695,9 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
     p.out = out;
     p.dbg_na = na;
     p.dbg_nb = nb;
-    if (w == 0) return launch_dtw_w0(p, st, num_sms);
-    // Full window (w = L-1): the band sweeps (w+1)(2L-1) slot-cells for L^2 cells (50% useful)
-    // while the row-strip kernel computes L^2 unmasked cells, so it wins when its strips are
-    // nearly full (measured: L=256, w=255: 1.9 -> 4.4 Tcells/s; L=300: 3.6 -> 4.4; L=384: 2.8 -> 5.1;
-    // L=128 (one half-empty strip): 2.6 -> 1.9, so the band stays there).
-    static const char *fs = getenv("NNDTW_FORCE_STRIP");  // experiments: 1 = strip, 0 = band
-    bool strip = false;
-    if (w >= L - 1) {
-        const int H = 32 * strip_rows_per_lane(L);
-        strip = (long long)((L + H - 1) / H) * H * 100 <= (long long)L * 112;  // <= 12% idle rows
-    }
-    if (fs) strip = fs[0] == '1';
-    if (band_supported(w, L) && !strip) {
+    const int kind = dtw_kernel_kind(L, w);
+    if (kind == 0) return launch_dtw_w0(p, st, num_sms);
+    if (kind == 1) {
         int rc = launch_dtw_band(p, st, num_sms);
         if (rc == 0) return 0;
     }

@@ -12,6 +12,13 @@ int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
               const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L, int w,
               int v, int with_kim, int64_t self_offset, float *lb, int64_t ldlb,
               unsigned long long *minkey, cudaStream_t st, int keogh = 0, int transposed = 0);
+// S3 prune counters per cascade level (stats; lb.cu k_lb_tile in level-count mode)
+int launch_lb_level_counts(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
+                           const nndtw_kim *tkim, int64_t nt, int L, int w, int v, int with_kim,
+                           int keogh, int64_t self_offset, const float *lb, int64_t ldlb,
+                           const unsigned long long *key, const unsigned long long *minkey,
+                           const int32_t *seed2, float eps_p, unsigned long long *level_cnt,
+                           cudaStream_t st);
 // S2 extras (bounds_next.cu): kind 0 = LB_New, 1 = LB_Improved (all pairs, measurement kernels)
 int launch_lb_pairs(int kind, const float *q, int64_t nq, const float *t, const float *U,
                     const float *Lo, int64_t nt, int L, int w, float *lb, int64_t ldlb,
@@ -67,6 +74,7 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
                  unsigned long long *counters, const long long *cells_prefix,
                  const float *cutoff, float *out, cudaStream_t st, int num_sms);
 
+int dtw_kernel_kind(int L, int w);  // 0 = k_dtw_w0, 1 = k_dtw_band, 2 = k_dtw_strip
 int strip_rows_per_lane(int L);
 int launch_dtw_strip(const float *A, const float *B, const Item *items,
                      const unsigned long long *nitems_dev, unsigned long long item_cap,

@@ -45,6 +45,17 @@ struct LbParams {
     float *lb;
     int64_t ldlb;
     unsigned long long *minkey;
+    // Level-count mode (stats): no bridge, no output; lb holds
+    // the finished cascade values, count_key the seeded best-so-far keys.  Each pair outside
+    // the seeds / self pair with cascade value > bsf*(1+count_eps) is counted at the first level
+    // of the cascade that already exceeds the threshold: Kim, the
+    // boundary + band part of Algorithm 1 (its line-12 abort), or the full bound with the
+    // LB_Keogh bridge.  level_cnt[0..2] += those counts.
+    const unsigned long long *count_key;
+    const unsigned long long *seed_minkey;
+    const int32_t *seed2;
+    float count_eps;
+    unsigned long long *level_cnt;
 };
 
 struct LbSmem {
@@ -99,7 +110,7 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
 
     // ---- column-chunk loader (register prefetch) ------------------------------------------
     const int ch_begin = nbb / LB_CC;
-    const int ch_end = (L - nbb + LB_CC - 1) / LB_CC;  // exclusive
+    const int ch_end = p.count_key ? ch_begin : (L - nbb + LB_CC - 1) / LB_CC;  // exclusive
     float ra[4];
     float2 re[8];
     // load slot k of this thread: tile row (tid >> 4) + 16k, column c0 + (tid & 15) -- the same
@@ -257,6 +268,55 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
         __syncthreads();
     }
 
+    if (p.count_key) {  // level-count mode (see LbParams)
+        unsigned long long c0 = 0, c1 = 0, c2 = 0;
+#pragma unroll
+        for (int qi = 0; qi < LB_QPT; ++qi) {
+            const int rq = tq * LB_QPT + qi;
+            const int64_t qq = q0 + rq;
+            const bool qok = qq < p.nq;
+            const float thr = qok ? key_dist(p.count_key[qq]) * (1.0f + p.count_eps) : 0.0f;
+            const unsigned s1 = qok ? (unsigned)(p.seed_minkey[qq] & 0xffffffffull) : 0u;
+            const unsigned s2 = (qok && p.seed2) ? (unsigned)p.seed2[qq] : 0xffffffffu;
+#pragma unroll
+            for (int j = 0; j < LB_NPT; ++j) {
+                const int rn = lane + 32 * j;
+                const int64_t nn = n0 + rn;
+                if (!qok || nn >= p.nt || (p.self_offset >= 0 && nn == qq + p.self_offset) ||
+                    (unsigned)nn == s1 || (unsigned)nn == s2)
+                    continue;
+                const float full = p.lb[qq * p.ldlb + nn];
+                float kim = 0.0f;
+                if (p.with_kim) {
+                    nndtw_kim ka = S.qk[rq], kb = S.tk[rn];
+                    kim = sq(qhv(qi, 0) - thv(j, 0)) + sq(qtv(qi, 0) - ttv(j, 0));
+                    bool okmin = ka.imin != 0 && ka.imin != L - 1 && kb.imin != 0 && kb.imin != L - 1;
+                    if (okmin) kim = kim + sq(ka.vmin - kb.vmin);
+                    bool okmax = ka.imax != 0 && ka.imax != L - 1 && kb.imax != 0 &&
+                                 kb.imax != L - 1 && !(okmin && (ka.imax == ka.imin || kb.imax == kb.imin));
+                    if (okmax) kim = kim + sq(ka.vmax - kb.vmax);
+                }
+                if (kim > thr) c0 += 1;
+                else if (full > thr) {
+                    if (acc[qi][j] > thr) c1 += 1;
+                    else c2 += 1;
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            c0 += __shfl_xor_sync(0xffffffffu, c0, off);
+            c1 += __shfl_xor_sync(0xffffffffu, c1, off);
+            c2 += __shfl_xor_sync(0xffffffffu, c2, off);
+        }
+        if (lane == 0) {
+            if (c0) atomicAdd(p.level_cnt + 0, c0);
+            if (c1) atomicAdd(p.level_cnt + 1, c1);
+            if (c2) atomicAdd(p.level_cnt + 2, c2);
+        }
+        return;
+    }
+
     // ---- Kim cascade, self exclusion, output, per-query argmin key --------------------------
 #pragma unroll
     for (int qi = 0; qi < LB_QPT; ++qi) {
@@ -285,11 +345,14 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
                 }
                 continue;
             }
-            if (p.self_offset >= 0 && nn == qq + p.self_offset) v = kInf;
+            // the leave-one-out self pair: NaN (fails every "lb <= threshold" test, so it is never
+            // compacted nor re-ranked) and never the argmin seed
+            const bool self = p.self_offset >= 0 && nn == qq + p.self_offset;
+            if (self) v = __int_as_float(0x7fffffff);
             if (qq < p.nq && nn < p.nt) {
                 p.lb[qq * p.ldlb + nn] = v;
                 unsigned long long k = make_key(v, (unsigned)nn);
-                best = k < best ? k : best;
+                if (!self) best = k < best ? k : best;
             }
         }
         if (p.minkey != nullptr) {
@@ -302,6 +365,8 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
         }
     }
 }
+
+static int launch_lb_params(LbParams &p, cudaStream_t st);
 
 int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
               const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L, int w,
@@ -333,6 +398,51 @@ int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
     p.lb = lb;
     p.ldlb = ldlb;
     p.minkey = minkey;
+    p.count_key = nullptr;
+    p.seed_minkey = nullptr;
+    p.seed2 = nullptr;
+    p.count_eps = 0.0f;
+    p.level_cnt = nullptr;
+    return launch_lb_params(p, st);
+}
+
+int launch_lb_level_counts(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
+                           const nndtw_kim *tkim, int64_t nt, int L, int w, int v, int with_kim,
+                           int keogh, int64_t self_offset, const float *lb, int64_t ldlb,
+                           const unsigned long long *key, const unsigned long long *minkey,
+                           const int32_t *seed2, float eps_p, unsigned long long *level_cnt,
+                           cudaStream_t st) {
+    if (nq == 0 || nt == 0) return 0;
+    if (w > L - 1) w = L - 1;
+    LbParams p;
+    p.q = q;
+    p.nq = nq;
+    p.qkim = qkim;
+    p.t = t;
+    p.U = nullptr;
+    p.Lo = nullptr;
+    p.tkim = tkim;
+    p.nt = nt;
+    p.L = L;
+    p.w = w;
+    p.nb = (L / 2) < v ? (L / 2) : v;
+    p.with_kim = with_kim;
+    p.keogh = keogh;
+    p.transposed = 0;
+    p.self_offset = self_offset;
+    p.lb = const_cast<float *>(lb);
+    p.ldlb = ldlb;
+    p.minkey = nullptr;
+    p.count_key = key;
+    p.seed_minkey = minkey;
+    p.seed2 = seed2;
+    p.count_eps = eps_p;
+    p.level_cnt = level_cnt;
+    return launch_lb_params(p, st);
+}
+
+static int launch_lb_params(LbParams &p, cudaStream_t st) {
+    const int64_t nq = p.nq, nt = p.nt;
     dim3 grid((unsigned)((nq + LB_TQ - 1) / LB_TQ), (unsigned)((nt + LB_TN - 1) / LB_TN));
     if (grid.y > 65535u) return -1;
     size_t smem = sizeof(LbSmem);

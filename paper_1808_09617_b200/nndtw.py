@@ -28,6 +28,7 @@ NNDTW_CLASSIFY_PHASE_SEED = 8
 NNDTW_CLASSIFY_PHASE_SEARCH = 16
 NNDTW_CLASSIFY_PHASE_SEARCH_A = 32
 NNDTW_CLASSIFY_PHASE_SEARCH_B = 64
+NNDTW_CLASSIFY_LEVEL_STATS = 128
 KEY_INIT = 0x7F800000FFFFFFFF
 
 
@@ -36,7 +37,8 @@ class NNDTWError(RuntimeError):
 
 
 class Stats(C.Structure):
-    _fields_ = [("lb_pairs", C.c_int64), ("survivors", C.c_int64), ("dtw_calls", C.c_int64),
+    _fields_ = [("lb_pairs", C.c_int64), ("survivors", C.c_int64), ("pruned_kim", C.c_int64),
+                ("pruned_bands", C.c_int64), ("pruned_keogh", C.c_int64), ("dtw_calls", C.c_int64),
                 ("dtw_abandoned", C.c_int64), ("cells", C.c_int64),
                 ("near_tie_pairs", C.c_int64), ("rounds", C.c_int32), ("launches", C.c_int32),
                 ("ms_envelopes", C.c_float), ("ms_lb", C.c_float), ("ms_dtw", C.c_float),
@@ -44,6 +46,18 @@ class Stats(C.Structure):
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+def merge_stat_dicts(a: dict, b: dict) -> dict:
+    """Sum two stats dicts; the per-level prune counters stay -1 (not computed) unless one
+    side has them."""
+    out = {}
+    for k in a:
+        if k.startswith("pruned_"):
+            out[k] = -1 if a[k] < 0 and b[k] < 0 else max(a[k], 0) + max(b[k], 0)
+        else:
+            out[k] = a[k] + b[k]
+    return out
 
 
 _lib = None
@@ -56,6 +70,7 @@ _SIGS = {
     "nndtw_version": (C.c_int, []),
     "nndtw_launch_count": (_I64, []),
     "nndtw_check_device": (C.c_int, []),
+    "nndtw_dtw_kernel_name": (C.c_char_p, [_I32, _I32]),
     "nndtw_check_finite": (C.c_int, [_P, _I64, _P, _P]),
     "nndtw_envelopes": (C.c_int, [_P, _I64, _I32, _I32, _P, _P, _P, _P]),
     "nndtw_series_stats": (C.c_int, [_P, _I64, _I32, _P, _P]),
@@ -279,7 +294,8 @@ class Model:
 
 
 def classify_keys(model: Model, q: torch.Tensor, exact: bool = True, self_offset: int = -1,
-                  stats: bool = False, stream=None, phase: str | None = None, key=None, ws=None):
+                  stats: bool = False, stream=None, phase: str | None = None, key=None, ws=None,
+                  level_stats: bool = False):
     """S2-S7 on one shard: returns (key int64 [nq], workspace, stats dict | None).
 
     phase None runs everything; "seed" stops after the S3 seed round (keys = seed keys);
@@ -300,6 +316,7 @@ def classify_keys(model: Model, q: torch.Tensor, exact: bool = True, self_offset
     flags = ((NNDTW_CLASSIFY_EXACT if exact else 0) |
              (NNDTW_CLASSIFY_BOUND_KEOGH if model.bound == "keogh" else 0) |
              (NNDTW_CLASSIFY_BOUND_SYMMETRIC if model.symmetric else 0) |
+             (NNDTW_CLASSIFY_LEVEL_STATS if (stats and level_stats) else 0) |
              {None: 0, "seed": NNDTW_CLASSIFY_PHASE_SEED,
               "search": NNDTW_CLASSIFY_PHASE_SEARCH,
               "search_a": NNDTW_CLASSIFY_PHASE_SEARCH_A,
@@ -318,7 +335,7 @@ def merge_stats(a: dict | None, b: dict | None) -> dict | None:
     """Sum two stats dicts (the seed and search phases of one sharded call)."""
     if a is None or b is None:
         return a or b
-    return {k: a[k] + b[k] for k in a}
+    return merge_stat_dicts(a, b)
 
 
 def classify_refine(model: Model, q, ws, gkey, stream=None) -> torch.Tensor:
@@ -355,7 +372,8 @@ WORKSPACE_BUDGET = 48 << 30  # bytes of classify workspace per call before queri
 
 
 def classify(model: Model, q: torch.Tensor, stats: bool = False, check: bool = True,
-             stream=None, workspace_budget: int | None = None) -> Prediction:
+             stream=None, workspace_budget: int | None = None,
+             level_stats: bool = False) -> Prediction:
     """Exact 1-NN of every query (single GPU / single shard, fp64-exact tie resolution).
 
     The workspace holds the bound matrix and a worst-case survivor list (12 bytes per
@@ -372,11 +390,13 @@ def classify(model: Model, q: torch.Tensor, stats: bool = False, check: bool = T
     while blk > 1 and lib.nndtw_classify_workspace_bytes(blk, nt, model.L, model.w) > budget:
         blk = (blk + 1) // 2
     if blk >= nq:
-        key, _, st = classify_keys(model, q, exact=True, stats=stats, stream=stream)
+        key, _, st = classify_keys(model, q, exact=True, stats=stats, stream=stream,
+                                   level_stats=level_stats)
     else:
         keys, st = [], None
         for i in range(0, nq, blk):
-            k, _, s = classify_keys(model, q[i:i + blk], exact=True, stats=stats, stream=stream)
+            k, _, s = classify_keys(model, q[i:i + blk], exact=True, stats=stats, stream=stream,
+                                    level_stats=level_stats)
             keys.append(k)
             st = merge_stats(st, s) if stats else None
         key = torch.cat(keys)

@@ -51,7 +51,7 @@ def test_library_is_sm100a(lib):
 
 
 def test_host_only_calls(lib):
-    assert lib.nndtw_version() == 1
+    assert lib.nndtw_version() == 2
     assert lib.nndtw_launch_count() >= 0
     ws = lib.nndtw_classify_workspace_bytes(100, 1000, 128, 13)
     # LB matrix + worst-case item list dominate: 100*1000*(4+8) bytes
@@ -74,3 +74,38 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "nndtw_oracle" not in txt, f
+
+
+def test_stats_struct_matches_header(tmp_path):
+    """The ctypes Stats mirror of nndtw_stats has the header's field order, offsets and size
+    (compiled against include/nndtw.h with gcc)."""
+    import ctypes as C
+    from paper_1808_09617_b200 import nndtw
+    names = [f for f, _ in nndtw.Stats._fields_]
+    for f in ("pruned_kim", "pruned_bands", "pruned_keogh", "ms_envelopes"):
+        assert f in names
+    src = tmp_path / "s.c"
+    body = "".join(f'printf("{f} %zu\\n", offsetof(nndtw_stats, {f}));' for f in names)
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "nndtw.h"\n'
+                   'int main(void){' + body +
+                   'printf("size %zu\\n", sizeof(nndtw_stats)); return 0;}\n')
+    exe = tmp_path / "s"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = dict(line.split() for line in subprocess.check_output([str(exe)], text=True).split("\n")
+               if line)
+    for f in names:
+        assert int(out[f]) == getattr(nndtw.Stats, f).offset, f
+    assert int(out["size"]) == C.sizeof(nndtw.Stats)
+
+
+def test_dtw_kernel_name_rule(lib):
+    """nndtw_dtw_kernel_name (host-only) names the S4 kernel dispatch_dtw picks: w = 0 is the
+    squared-ED kernel, narrow bands the wavefront kernel, config 4's full window the strips."""
+    name = lambda L, w: lib.nndtw_dtw_kernel_name(L, w).decode()  # noqa: E731
+    assert name(300, 0) == "k_dtw_w0"
+    assert name(512, 103) == "k_dtw_band"
+    assert name(256, 26) == "k_dtw_band"
+    assert name(2048, 2047) == "k_dtw_strip"
+    assert name(2048, 5000) == "k_dtw_strip"      # clamped to L-1
+    assert name(1024, 511) == "k_dtw_band"        # R = 32 is the only band layout (2w+2 = 1024)
+    assert name(1, 0) == "" and name(16, -1) == ""

@@ -426,3 +426,31 @@ def test_lb_new_is_min_over_window_cells(oracle_lib):
             cand = [win[j] for j in (k - 1, k) if 0 <= j < win.size]
             tot += min((float(a[i]) - c) ** 2 for c in cand)
         assert o.lb_new(a, b, w) == tot
+
+
+def test_tightness_hand_example(oracle_lib):
+    """oracle.tightness = mean of LB/DTW in the root domain (reading C20: the squared
+    values are square-rooted first; pairs with DTW = 0 are excluded).  Worked by hand:
+    pairs (lb, dtw^2) = (1,4), (4,16), (9,9), (0,0), (2,8) -> ratios 1/2, 2/4, 3/3, -, 1/2
+    -> mean 2.5/4 = 0.625 over 4 pairs.  Without the square roots the mean would be 0.4375;
+    counting the DTW = 0 pair would change the count to 5."""
+    t, n = oracle_lib.tightness([1, 4, 9, 0, 2], [4, 16, 9, 0, 8])
+    assert n == 4
+    assert t == 0.625
+
+
+def test_tightness_special_cases(oracle_lib):
+    """At W = 0 the envelope of B is B itself, so LB_Keogh = squared ED = DTW_0:
+    tightness exactly 1 on pairs with distinct series; any admissible bound gives <= 1."""
+    rng = np.random.default_rng(37)
+    X = datagen.random_series(rng, 12, 40, "walk")
+    lb = [oracle_lib.lb_keogh(X[i], X[i + 6], X[i + 6]) for i in range(6)]
+    d = [oracle_lib.dtw(X[i], X[i + 6], 0) for i in range(6)]
+    t, n = oracle_lib.tightness(lb, d)
+    assert n == 6 and abs(t - 1.0) < 1e-12
+    w = 5
+    U, Lo = oracle_lib.envelopes(X, w)
+    lb = [oracle_lib.lb_enhanced(X[i], X[i + 6], U[i + 6], Lo[i + 6], w, 3)[0] for i in range(6)]
+    d = [oracle_lib.dtw(X[i], X[i + 6], w) for i in range(6)]
+    t, n = oracle_lib.tightness(lb, d)
+    assert n == 6 and 0.0 < t <= 1.0
