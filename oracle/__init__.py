@@ -77,6 +77,8 @@ def _load():
         lib.oracle_lb_improved.argtypes = [fp, fp, fp, fp, C.c_int, C.c_int]
         lib.oracle_lb_new.restype = C.c_double
         lib.oracle_lb_new.argtypes = [fp, fp, C.c_int, C.c_int]
+        lib.oracle_lb_enhanced_improved.restype = C.c_double
+        lib.oracle_lb_enhanced_improved.argtypes = [fp, fp, fp, fp, C.c_int, C.c_int, C.c_int]
         lib.oracle_lb_enhanced_sym.restype = C.c_double
         lib.oracle_lb_enhanced_sym.argtypes = [fp, fp, fp, fp, fp, fp, C.c_int, C.c_int,
                                                C.c_int]
@@ -190,6 +192,17 @@ def lb_new(a, b, w: int) -> float:
     return _load().oracle_lb_new(_ptr(a, C.c_float), _ptr(b, C.c_float), a.size, int(w))
 
 
+def lb_enhanced_improved(a, b, w: int, V: int, UB=None, LB=None) -> float:
+    """LB_Enhanced^V with the LB_Improved bridge (reading C21)."""
+    a, b = _f32(a), _f32(b)
+    if UB is None:
+        UB, LB = envelope(b, w)
+    UB, LB = _f32(UB), _f32(LB)
+    return _load().oracle_lb_enhanced_improved(_ptr(a, C.c_float), _ptr(b, C.c_float),
+                                               _ptr(UB, C.c_float), _ptr(LB, C.c_float),
+                                               a.size, int(w), int(V))
+
+
 def lb_enhanced_sym(a, b, w: int, V: int) -> float:
     """max(LB_Enhanced(A,B), LB_Enhanced(B,A)) (P:745-747)."""
     a, b = _f32(a), _f32(b)
@@ -203,7 +216,7 @@ def lb_enhanced_sym(a, b, w: int, V: int) -> float:
 
 def bound_matrix(kind: str, Q, T, w: int, V: int = 5) -> np.ndarray:
     """All-pairs bound matrix [nq][nt] (fp64) for kind in {keogh, enhanced, cascade, sym,
-    improved, new}; plain loops over the single-pair functions above (small inputs only)."""
+    improved, new, enhanced_improved}; plain loops over the single-pair functions above (small inputs only)."""
     Q, T = _f32(Q), _f32(T)
     UT, LT = envelopes(T, w)
     out = np.empty((Q.shape[0], T.shape[0]), dtype=np.float64)
@@ -221,6 +234,8 @@ def bound_matrix(kind: str, Q, T, w: int, V: int = 5) -> np.ndarray:
                 out[i, j] = lb_improved(a, b, w, UT[j], LT[j])
             elif kind == "new":
                 out[i, j] = lb_new(a, b, w)
+            elif kind == "enhanced_improved":
+                out[i, j] = lb_enhanced_improved(a, b, w, V, UT[j], LT[j])
             else:
                 raise ValueError(kind)
     return out

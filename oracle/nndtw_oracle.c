@@ -261,6 +261,38 @@ double oracle_lb_enhanced_sym(const float *A, const float *B, const float *UA, c
     return x > y ? x : y;
 }
 
+/* ---------------------------------------------------------------------------------------
+ * LB_Enhanced^V with the LB_Improved bridge ("replace LB_Keogh by LB_Improved within
+ * LB_Enhanced"), reading C21:
+ *   LB_Enhanced^V_W(A,B)  [bands + LB_Keogh bridge over rows n_bands+1 .. L-n_bands]
+ *   + sum over the bridge columns j = n_bands+1 .. L-n_bands (1-based) of the LB_Keogh term of
+ *     B_j against the envelope (Eq. 3-4, naive scan) of A', the projection of A onto the
+ *     envelope of B (Eq. "projection").
+ * Admissible: a cell (i,j) with |i-j| <= W has B_j in [L_i, U_i], so (A_i-B_j)^2 >=
+ * (A_i-A'_i)^2 + (A'_i-B_j)^2; the first parts are counted once per bridge row (the LB_Keogh
+ * terms), the second once per bridge column, and no cell of a bridge column lies in a band
+ * (band cells have max(i,j) <= n_bands or min(i,j) > L-n_bands) -- LB_Improved's argument
+ * next to Theorem 2's bands.
+ * ------------------------------------------------------------------------------------- */
+double oracle_lb_enhanced_improved(const float *A, const float *B, const float *UB,
+                                   const float *LB, int L, int W, int V) {
+    W = clamp_w(L, W);
+    double res = oracle_lb_enhanced(A, B, UB, LB, L, W, V, ORACLE_INF, 0.0, NULL);
+    int n_bands = L / 2 < V ? L / 2 : V;
+    float *Ap = (float *)malloc(sizeof(float) * (size_t)L);
+    float *Ua = (float *)malloc(sizeof(float) * (size_t)L);
+    float *La = (float *)malloc(sizeof(float) * (size_t)L);
+    for (int i = 0; i < L; ++i) {
+        if (A[i] > UB[i]) Ap[i] = UB[i];
+        else if (A[i] < LB[i]) Ap[i] = LB[i];
+        else Ap[i] = A[i];
+    }
+    oracle_envelope(Ap, L, W, Ua, La);
+    res = res + oracle_lb_keogh_range(B, Ua, La, n_bands + 1, L - n_bands);
+    free(Ap); free(Ua); free(La);
+    return res;
+}
+
 /* The cascade value used by the search (P:299-304 cascading, P:619-621 Kim):
  * max(LB_Kim_sum, LB_Enhanced) with no abort. */
 double oracle_lb_cascade(const float *A, const float *B, const float *U, const float *Lo,

@@ -25,8 +25,8 @@ MUTATIONS = [
      "delta(Ax(L - i + 1), Bx(L - j)));"),
     ("alg1_band_window_start", "int j0 = i - W > 1 ? i - W : 1;",
      "int j0 = i - W + 1 > 1 ? i - W + 1 : 1;"),
-    ("n_bands_rounding", "int n_bands = L / 2 < V ? L / 2 : V;",
-     "int n_bands = (L + 1) / 2 < V ? (L + 1) / 2 : V;"),
+    ("n_bands_rounding", "/* line 2 */\n    int n_bands = L / 2 < V ? L / 2 : V;",
+     "/* line 2 */\n    int n_bands = (L + 1) / 2 < V ? (L + 1) / 2 : V;"),
     ("bridge_overlaps_bands", "for (int i = n_bands + 1; i <= L - n_bands; ++i) {\n        if (Ax(i)",
      "for (int i = n_bands; i <= L - n_bands + 1; ++i) {\n        if (Ax(i)"),
     ("envelope_window_short", "        int hi = i + w > L ? L : i + w;\n        float u",
@@ -43,10 +43,15 @@ MUTATIONS = [
      "if (d <= D || nn < 0) { D = d; nn = n; }"),
     ("keogh_upper_side_dropped", "if (a > (double)U[i - 1]) res = res + delta(a, (double)U[i - 1]);",
      "if (a > (double)U[i - 1]) res = res + 0.0;"),
-    ("lb_improved_no_projection", "if (A[i] > UB[i]) Ap[i] = UB[i];",
-     "if (A[i] > UB[i]) Ap[i] = A[i];"),
+    ("lb_improved_no_projection", "        else Ap[i] = A[i];\n    }\n    oracle_envelope(Ap, L, W, Ua, La);\n    double res",
+     "        else Ap[i] = A[i];\n        Ap[i] = A[i];\n    }\n    oracle_envelope(Ap, L, W, Ua, La);\n    double res"),
     ("lb_new_window_short", "        int hi = i + W > L ? L : i + W;\n        double m",
      "        int hi = i + W - 1 > L ? L : i + W - 1;\n        double m"),
+    ("enh_improved_columns_into_bands",
+     "res = res + oracle_lb_keogh_range(B, Ua, La, n_bands + 1, L - n_bands);",
+     "res = res + oracle_lb_keogh_range(B, Ua, La, n_bands, L - n_bands + 1);"),
+    ("enh_improved_no_projection", "        else Ap[i] = A[i];\n    }\n    oracle_envelope(Ap, L, W, Ua, La);\n    res = res + oracle_lb_keogh_range",
+     "        else Ap[i] = A[i];\n        Ap[i] = A[i];\n    }\n    oracle_envelope(Ap, L, W, Ua, La);\n    res = res + oracle_lb_keogh_range"),
 ]
 # mutations of the Python side of the oracle (oracle/__init__.py)
 PY_MUTATIONS = [

@@ -454,3 +454,35 @@ def test_tightness_special_cases(oracle_lib):
     d = [oracle_lib.dtw(X[i], X[i + 6], w) for i in range(6)]
     t, n = oracle_lib.tightness(lb, d)
     assert n == 6 and 0.0 < t <= 1.0
+
+
+def test_enhanced_improved_admissible_and_dominant(oracle_lib):
+    """LB_Enhanced^V with the LB_Improved bridge (reading C21): <= DTW_W (brute-force
+    path enumeration, L <= 8, every W and V), >= LB_Enhanced^V (it adds non-negative terms),
+    equal to it at W = 0 (A' = B, so env A' = B) and when the bridge is empty (V >= L/2), and
+    strictly tighter on some pairs (the second pass is live)."""
+    o = oracle_lib
+    strict = 0
+    for a, b in rng_pairs(42, 90, 8, kinds=("walk", "normal")):
+        L = a.size
+        for w in range(0, L):
+            d = brute_dtw(a, b, w)
+            tol = 1e-12 * max(1.0, d)
+            U, Lo = o.envelope(b, w)
+            for V in range(1, L // 2 + 1):
+                e = o.lb_enhanced(a, b, U, Lo, w, V)[0]
+                ei = o.lb_enhanced_improved(a, b, w, V)
+                assert ei <= d + tol, (a, b, w, V, ei, d)
+                assert ei >= e - tol
+                if w == 0 or 2 * min(L // 2, V) >= L:
+                    assert ei == e
+                strict += ei > e * (1 + 1e-9) + 1e-12
+    assert strict > 50
+    # larger series against the (pinned) DP DTW
+    rng = np.random.default_rng(43)
+    X = datagen.random_series(rng, 40, 64, "walk")
+    for i in range(20):
+        for w in (1, 3, 6, 20, 63):
+            d = o.dtw(X[i], X[i + 20], w)
+            for V in (1, 3, 5, 16):
+                assert o.lb_enhanced_improved(X[i], X[i + 20], w, V) <= d * (1 + 1e-12)
