@@ -152,18 +152,26 @@ NNDTW_API int nndtw_lb_enhanced_symmetric(const float *q, const float *q_upper,
                                           void *stream);
 
 /*
- * Comparison bounds of the paper's evaluation, all pairs:
- * nndtw_lb_improved: LB_Improved_W(q_i, t_j) = LB_Keogh(q_i, env t_j) + LB_Keogh(t_j, env q'),
- *   q' the projection of q_i onto t_j's envelope (§2.3.3); t_upper / t_lower are
- *   t's envelopes (nndtw_envelopes with the same w).
+ * Comparison bounds of the paper's evaluation, all pairs
+ * (q: [nq][L]; t: [nt][L]; lb: [nq][ldlb] out, ldlb >= nt; fp32; asynchronous):
+ * nndtw_lb_improved: LB_Improved_W(q_i, t_j) = LB_Keogh(q_i, env t_j) + LB_Keogh(t_j, env q')
+ *   (§2.3.3), q' the projection of q_i onto t_j's envelope; env q' by the O(L)
+ *   van Herk sliding max/min per pair ("the optimised algorithm to compute the projection
+ *   envelopes").  t_upper / t_lower: t's envelopes (nndtw_envelopes, same w).
+ *   L <= 10240 (E_LENGTH otherwise).
+ * nndtw_lb_enhanced_improved: LB_Enhanced^V_W with the LB_Improved bridge (reading
+ *   C21): nndtw_lb_enhanced's value plus, over the bridge columns n_bands+1 .. L-n_bands, the
+ *   LB_Keogh terms of t_j against the envelope of q'.  Admissible; >= LB_Enhanced^V.
  * nndtw_lb_new: LB_New_W(q_i, t_j) = delta(first) + delta(last) + sum over the inner i of the
- *   minimum delta(q_i, t_j') over the window (§2.3.4).
- * Measurement kernels (tightness tables, Fig. 1/2, 10/11 analogues): O(L*w) per pair.
- * q: [nq][L]; t: [nt][L]; lb: [nq][ldlb] out, ldlb >= nt.  fp32.  Asynchronous.
+ *   minimum delta(q_i, t_j') over the window (§2.3.4); O(L*w) per pair, as defined.
  */
 NNDTW_API int nndtw_lb_improved(const float *q, int64_t nq, const float *t,
                                 const float *t_upper, const float *t_lower, int64_t nt,
                                 int32_t L, int32_t w, float *lb, int64_t ldlb, void *stream);
+NNDTW_API int nndtw_lb_enhanced_improved(const float *q, int64_t nq, const float *t,
+                                         const float *t_upper, const float *t_lower, int64_t nt,
+                                         int32_t L, int32_t w, int32_t v, float *lb,
+                                         int64_t ldlb, void *stream);
 NNDTW_API int nndtw_lb_new(const float *q, int64_t nq, const float *t, int64_t nt, int32_t L,
                            int32_t w, float *lb, int64_t ldlb, void *stream);
 
@@ -235,6 +243,20 @@ NNDTW_API int nndtw_dtw_batch(const float *a, const float *b, const int32_t *ia,
 /* flags & NNDTW_CLASSIFY_LEVEL_STATS (with non-NULL stats): fill the per-level prune counters
  * pruned_kim / pruned_bands / pruned_keogh (one extra bands-only pass, no bridge). */
 #define NNDTW_CLASSIFY_LEVEL_STATS 128u
+/* Alternative S2 bounds (the paper's NN-DTW time per bound,
+ * Fig. 9-11).  At most one of them, not with BOUND_KEOGH / BOUND_SYMMETRIC; the
+ * answer never changes (every bound is admissible, Thm 2):
+ *   BOUND_IMPROVED           max(LB_Kim, LB_Improved)
+ *   BOUND_NEW                max(LB_Kim, LB_New)
+ *   BOUND_ENHANCED_IMPROVED  max(LB_Kim, LB_Enhanced^V with the LB_Improved bridge)
+ *   BOUND_NONE               no lower bound: every pair is a survivor, DTW with early
+ *                            abandoning only (the no-LB baseline).
+ * With LEVEL_STATS the bridge-level counter pruned_keogh counts the pairs pruned by the full
+ * bound (pruned_bands is 0 except for BOUND_ENHANCED_IMPROVED). */
+#define NNDTW_CLASSIFY_BOUND_IMPROVED 256u
+#define NNDTW_CLASSIFY_BOUND_NEW 512u
+#define NNDTW_CLASSIFY_BOUND_ENHANCED_IMPROVED 1024u
+#define NNDTW_CLASSIFY_BOUND_NONE 2048u
 NNDTW_API size_t nndtw_classify_workspace_bytes(int64_t nq, int64_t nt, int32_t L, int32_t w);
 NNDTW_API int nndtw_classify(const float *q, int64_t nq, const float *t, const float *upper,
                    const float *lower, const nndtw_kim *tkim, int64_t nt, int64_t index_base,

@@ -254,6 +254,20 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     }();
     const int keogh = (flags & NNDTW_CLASSIFY_BOUND_KEOGH) ? 1 : 0;
     const bool sym = (flags & NNDTW_CLASSIFY_BOUND_SYMMETRIC) != 0;
+    // alternative S2 bounds (NEXT-1 / NEXT-4): assembled outside the tile kernel, then finished
+    const uint32_t alt = flags & (NNDTW_CLASSIFY_BOUND_IMPROVED | NNDTW_CLASSIFY_BOUND_NEW |
+                                  NNDTW_CLASSIFY_BOUND_ENHANCED_IMPROVED |
+                                  NNDTW_CLASSIFY_BOUND_NONE);
+    if (alt & (alt - 1)) return fail(NNDTW_E_ARG, "more than one alternative bound flag");
+    if (alt && (keogh || sym))
+        return fail(NNDTW_E_ARG, "an alternative bound cannot be combined with KEOGH/SYMMETRIC");
+    if ((alt & (NNDTW_CLASSIFY_BOUND_IMPROVED | NNDTW_CLASSIFY_BOUND_ENHANCED_IMPROVED)) &&
+        L > 10240)
+        return fail(NNDTW_E_LENGTH, "the LB_Improved passes need L <= 10240");
+    const bool alt_none = (alt & NNDTW_CLASSIFY_BOUND_NONE) != 0;
+    // cascade levels for the level counters: band level only where Algorithm 1's bands exist
+    const int count_no_bands = (keogh || (alt && !(alt & NNDTW_CLASSIFY_BOUND_ENHANCED_IMPROVED)))
+                                   ? 1 : 0;
     TieLog log{W.log, W.log_count, W.log_cap, W.overflow};
     unsigned long long *cnt = stats ? W.counters : nullptr;
 
@@ -273,7 +287,29 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         if (nt > 0 && sym) launch_envelopes(q, nq, L, w, W.qU, W.qL, nullptr, st);
     }
     tm.mark();  // 2
-    if (do_seed) {
+    if (do_seed && nt > 0 && alt) {
+        // S2 with an alternative bound: matrix, then max with LB_Kim / self pair / argmin seed
+        int lrc = 0;
+        if (alt & NNDTW_CLASSIFY_BOUND_IMPROVED) {
+            lrc = launch_lb(q, nq, nullptr, t, U, Lo, nullptr, nt, L, w, v, 0, -1, W.lb, W.ldlb,
+                            nullptr, st, 1) ||
+                  launch_lb_improved_pass(q, nq, t, U, Lo, nt, L, w, 0, L, W.lb, W.ldlb, sms, st);
+        } else if (alt & NNDTW_CLASSIFY_BOUND_ENHANCED_IMPROVED) {
+            const int nb = (L / 2) < v ? (L / 2) : v;
+            lrc = launch_lb(q, nq, nullptr, t, U, Lo, nullptr, nt, L, w, v, 0, -1, W.lb, W.ldlb,
+                            nullptr, st, 0) ||
+                  launch_lb_improved_pass(q, nq, t, U, Lo, nt, L, w, nb, L - nb, W.lb, W.ldlb, sms,
+                                          st);
+        } else if (alt & NNDTW_CLASSIFY_BOUND_NEW) {
+            lrc = launch_lb_pairs(0, q, nq, t, nullptr, nullptr, nt, L, w, W.lb, W.ldlb, st);
+        } else {  // BOUND_NONE: the bound is 0 for every pair
+            cudaMemsetAsync(W.lb, 0, sizeof(float) * (size_t)nq * (size_t)W.ldlb, st);
+        }
+        if (lrc) return fail(NNDTW_E_ARG, "bound kernel launch failed (shape)");
+        launch_bound_finish(W.lb, W.ldlb, nq, nt, q, t, alt_none ? nullptr : W.qkim, tkim, L,
+                            self_offset, W.minkey, st);
+    }
+    if (do_seed && !alt) {
         // S2: cascade bound for all pairs + per-query argmin-LB candidate
         if (nt > 0 && launch_lb(q, nq, W.qkim, t, U, Lo, tkim, nt, L, w, v, 1, self_offset,
                                 W.lb, W.ldlb, sym ? nullptr : W.minkey, st, keogh))
@@ -298,9 +334,9 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     const bool level_stats = stats != nullptr && (flags & NNDTW_CLASSIFY_LEVEL_STATS) != 0;
     if (nt > 0 && do_compact && level_stats) {
         // stats: pairs pruned per cascade level against the same threshold as the compaction
-        launch_lb_level_counts(q, nq, W.qkim, t, tkim, nt, L, w, v, 1, keogh, self_offset, W.lb,
-                               W.ldlb, key, W.minkey, seed2, eps_p,
-                               W.counters + CNT_PRUNED_KIM, st);
+        launch_lb_level_counts(q, nq, W.qkim, t, tkim, nt, L, w, v, alt_none ? 0 : 1,
+                               count_no_bands, self_offset, W.lb, W.ldlb, key, W.minkey, seed2,
+                               eps_p, W.counters + CNT_PRUNED_KIM, st);
     }
     if (nt > 0 && do_compact) {
         // S3: prune + compact the survivors against the seeded best-so-far
@@ -513,11 +549,38 @@ int nndtw_lb_improved(const float *q, int64_t nq, const float *t, const float *t
     if ((rc = check_common(nq, L, w))) return rc;
     if (nt < 0) return fail(NNDTW_E_ARG, "negative nt");
     if (ldlb < nt) return fail(NNDTW_E_ARG, "ldlb < nt");
+    if (L > 10240) return fail(NNDTW_E_LENGTH, "LB_Improved needs L <= 10240");
     if (nq > 0 && nt > 0 && (!q || !t || !t_upper || !t_lower || !lb))
         return fail(NNDTW_E_ARG, "null pointer argument");
-    if (launch_lb_pairs(1, q, nq, t, t_upper, t_lower, nt, L, w, lb, ldlb, (cudaStream_t)stream))
-        return fail(NNDTW_E_LENGTH, "L too long for the LB_Improved kernel's shared memory");
+    cudaStream_t st = (cudaStream_t)stream;
+    // first pass LB_Keogh(q, env t) over all columns (tile kernel), then LB_Keogh(t, env q')
+    if (launch_lb(q, nq, nullptr, t, t_upper, t_lower, nullptr, nt, L, w, 1, 0, -1, lb, ldlb,
+                  nullptr, st, 1) ||
+        launch_lb_improved_pass(q, nq, t, t_upper, t_lower, nt, L, w, 0, L, lb, ldlb, sms, st))
+        return fail(NNDTW_E_ARG, "too many series for one launch");
     return cuda_fail("nndtw_lb_improved");
+}
+
+int nndtw_lb_enhanced_improved(const float *q, int64_t nq, const float *t, const float *t_upper,
+                               const float *t_lower, int64_t nt, int32_t L, int32_t w, int32_t v,
+                               float *lb, int64_t ldlb, void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if ((rc = check_common(nq, L, w))) return rc;
+    if (nt < 0) return fail(NNDTW_E_ARG, "negative nt");
+    if (v < 1) return fail(NNDTW_E_V, "V must be >= 1");
+    if (ldlb < nt) return fail(NNDTW_E_ARG, "ldlb < nt");
+    if (L > 10240) return fail(NNDTW_E_LENGTH, "the LB_Improved bridge needs L <= 10240");
+    if (nq > 0 && nt > 0 && (!q || !t || !t_upper || !t_lower || !lb))
+        return fail(NNDTW_E_ARG, "null pointer argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nb = (L / 2) < v ? (L / 2) : v;
+    if (launch_lb(q, nq, nullptr, t, t_upper, t_lower, nullptr, nt, L, w, v, 0, -1, lb, ldlb,
+                  nullptr, st, 0) ||
+        launch_lb_improved_pass(q, nq, t, t_upper, t_lower, nt, L, w, nb, L - nb, lb, ldlb, sms,
+                                st))
+        return fail(NNDTW_E_ARG, "too many series for one launch");
+    return cuda_fail("nndtw_lb_enhanced_improved");
 }
 
 int nndtw_lb_new(const float *q, int64_t nq, const float *t, int64_t nt, int32_t L, int32_t w,

@@ -1,30 +1,24 @@
-// bounds_next.cu -- SURVEY §8(f) next rows: the comparison bounds of the paper's evaluation
-// (LB_Improved, LB_New), the symmetric-bound helpers, and the tightness reduction.
+// bounds_next.cu -- SURVEY §8(f) next rows: LB_New (a comparison bound of the paper's
+// evaluation), the symmetric-bound helpers, and the tightness reduction.  LB_Improved is
+// in bounds_improved.cu.
 //
 // LB_New_W(A,B) = delta(A_1,B_1) + delta(A_L,B_L) + sum_{i=2}^{L-1} min_{j in win(i)} delta(A_i,B_j)
 //   (§2.3.4).  min_j (a-b_j)^2 is taken as (min_j |a-b_j|)^2: squaring a rounded
 //   non-negative difference is monotone, so the fp32 result is the same as the minimum of the
 //   fp32 squares.
-// LB_Improved_W(A,B) = LB_Keogh(A, env B) + LB_Keogh(B, env A'), A'_j = clamp(A_j, L^B_j, U^B_j)
-//   (§2.3.3).
 //
-// Both are evaluated for all (query, train) pairs as measurement kernels (tightness tables,
-// Fig. 1/2 and 10/11 analogues), not on the hot path: a CTA stages 8 query rows and 16 train
-// rows in shared memory (odd row stride, conflict-free) and each thread owns one pair.  The
-// windowed minima are direct scans of the 2w+1 window, O(L*w) per pair -- the cost these bounds
-// pay and LB_Enhanced avoids.
+// Evaluated for all (query, train) pairs: a CTA stages 8 query rows and 16 train rows in shared
+// memory (odd row stride, conflict-free) and each thread owns one pair.  The windowed minima are
+// direct scans of the 2w+1 window, O(L*w) per pair: the bound's definition takes a minimum over
+// every cell of the window (no sliding-window shortcut applies to a min of |a_i - b_j|), the cost
+// LB_Enhanced avoids.
 #include "launchers.cuh"
 
 namespace nndtw {
 
 constexpr int NB_TQ = 8, NB_TN = 16;  // 128 pairs per CTA, one per thread
 
-__device__ __forceinline__ float keogh_term(float a, float u, float l) {
-    const float t = fmaxf(fmaxf(a - u, l - a), 0.0f);
-    return t * t;
-}
-
-// kind 0: LB_New; kind 1: LB_Improved (needs the train envelopes U, Lo)
+// kind 0: LB_New (the only kind; the template parameter is kept for the launcher's switch)
 template <int KIND>
 __global__ void __launch_bounds__(128) k_lb_pairs(const float *__restrict__ q, int64_t nq,
                                                   const float *__restrict__ t,
@@ -36,8 +30,6 @@ __global__ void __launch_bounds__(128) k_lb_pairs(const float *__restrict__ q, i
     const int stride = L + 1;
     float *sA = nb_smem;                    // [NB_TQ][stride]
     float *sB = sA + NB_TQ * stride;        // [NB_TN][stride]
-    float *sU = sB + NB_TN * stride;        // [NB_TN][stride] (LB_Improved)
-    float *sL = sU + NB_TN * stride;
     const int64_t q0 = (int64_t)blockIdx.x * NB_TQ, n0 = (int64_t)blockIdx.y * NB_TN;
     for (int e = threadIdx.x; e < NB_TQ * L; e += blockDim.x) {
         const int r = e / L, c = e - r * L;
@@ -48,40 +40,18 @@ __global__ void __launch_bounds__(128) k_lb_pairs(const float *__restrict__ q, i
         const int r = e / L, c = e - r * L;
         const int64_t nn = n0 + r < nt ? n0 + r : nt - 1;
         sB[r * stride + c] = t[nn * L + c];
-        if (KIND == 1) {
-            sU[r * stride + c] = U[nn * L + c];
-            sL[r * stride + c] = Lo[nn * L + c];
-        }
     }
     __syncthreads();
     const int qi = threadIdx.x / NB_TN, ni = threadIdx.x % NB_TN;
     const float *a = sA + qi * stride, *b = sB + ni * stride;
-    float res = 0.0f;
-    if (KIND == 0) {
-        res = sq(a[0] - b[0]);
-        if (L > 1) res += sq(a[L - 1] - b[L - 1]);
-        for (int i = 1; i < L - 1; ++i) {
-            const float ai = a[i];
-            const int lo = i - w > 0 ? i - w : 0, hi = i + w < L - 1 ? i + w : L - 1;
-            float m = kInf;
-            for (int j = lo; j <= hi; ++j) m = fminf(m, fabsf(ai - b[j]));
-            res += m * m;
-        }
-    } else {
-        const float *u = sU + ni * stride, *l = sL + ni * stride;
-        float k1 = 0.0f, k2 = 0.0f;
-        for (int i = 0; i < L; ++i) k1 += keogh_term(a[i], u[i], l[i]);
-        for (int i = 0; i < L; ++i) {
-            const int lo = i - w > 0 ? i - w : 0, hi = i + w < L - 1 ? i + w : L - 1;
-            float mx = -kInf, mn = kInf;
-            for (int j = lo; j <= hi; ++j) {
-                const float ap = fminf(fmaxf(a[j], l[j]), u[j]);  // projection A'_j
-                mx = fmaxf(mx, ap);
-                mn = fminf(mn, ap);
-            }
-            k2 += keogh_term(b[i], mx, mn);
-        }
-        res = k1 + k2;
+    float res = sq(a[0] - b[0]);
+    if (L > 1) res += sq(a[L - 1] - b[L - 1]);
+    for (int i = 1; i < L - 1; ++i) {
+        const float ai = a[i];
+        const int lo = i - w > 0 ? i - w : 0, hi = i + w < L - 1 ? i + w : L - 1;
+        float m = kInf;
+        for (int j = lo; j <= hi; ++j) m = fminf(m, fabsf(ai - b[j]));
+        res += m * m;
     }
     const int64_t qq = q0 + qi, nn = n0 + ni;
     if (qq < nq && nn < nt) lb[qq * ldlb + nn] = res;
@@ -92,18 +62,14 @@ int launch_lb_pairs(int kind, const float *q, int64_t nq, const float *t, const 
                     cudaStream_t st) {
     if (nq == 0 || nt == 0) return 0;
     if (w > L - 1) w = L - 1;
-    const size_t rows = NB_TQ + NB_TN * (kind == 1 ? 3 : 1);
+    if (kind != 0) return -1;
+    const size_t rows = NB_TQ + NB_TN;
     const size_t smem = rows * (size_t)(L + 1) * sizeof(float);
     if (smem > 227 * 1024) return -1;
     dim3 grid((unsigned)((nq + NB_TQ - 1) / NB_TQ), (unsigned)((nt + NB_TN - 1) / NB_TN));
     if (grid.y > 65535u) return -1;
-    if (kind == 0) {
-        cudaFuncSetAttribute(k_lb_pairs<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_lb_pairs<0><<<grid, 128, smem, st>>>(q, nq, t, U, Lo, nt, L, w, lb, ldlb);
-    } else {
-        cudaFuncSetAttribute(k_lb_pairs<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_lb_pairs<1><<<grid, 128, smem, st>>>(q, nq, t, U, Lo, nt, L, w, lb, ldlb);
-    }
+    cudaFuncSetAttribute(k_lb_pairs<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_lb_pairs<0><<<grid, 128, smem, st>>>(q, nq, t, U, Lo, nt, L, w, lb, ldlb);
     count_launch(1, __func__);
     return 0;
 }

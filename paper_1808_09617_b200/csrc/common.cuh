@@ -129,6 +129,21 @@ __device__ __forceinline__ void cp_async_wait_group1() {
     asm volatile("cp.async.wait_group 1;" ::: "memory");
 }
 
+// ---- LB_Kim, sum variant "without repetitions" (reading C7) -----------------------
+// features first, last, min, max in that order; a feature is dropped if its index in either
+// series is already used (first/last indices are 0 and L-1); ties -> lowest index (the
+// nndtw_kim features).  qf/ql, tf/tl = first/last values of the two series.
+__device__ __forceinline__ float kim_sum(float qf, float ql, float tf, float tl,
+                                         const nndtw_kim &ka, const nndtw_kim &kb, int L) {
+    float kim = (qf - tf) * (qf - tf) + (ql - tl) * (ql - tl);
+    const bool okmin = ka.imin != 0 && ka.imin != L - 1 && kb.imin != 0 && kb.imin != L - 1;
+    if (okmin) kim = kim + (ka.vmin - kb.vmin) * (ka.vmin - kb.vmin);
+    const bool okmax = ka.imax != 0 && ka.imax != L - 1 && kb.imax != 0 && kb.imax != L - 1 &&
+                       !(okmin && (ka.imax == ka.imin || kb.imax == kb.imin));
+    if (okmax) kim = kim + (ka.vmax - kb.vmax) * (ka.vmax - kb.vmax);
+    return kim;
+}
+
 // ---- work items ---------------------------------------------------------------------------
 // A DTW work item: query (row of A), train (row of B), local indices, and the pair's cascade
 // bound (survivor items are skipped at fetch time when it exceeds the live best-so-far).

@@ -19,7 +19,17 @@ int launch_lb_level_counts(const float *q, int64_t nq, const nndtw_kim *qkim, co
                            const unsigned long long *key, const unsigned long long *minkey,
                            const int32_t *seed2, float eps_p, unsigned long long *level_cnt,
                            cudaStream_t st);
-// S2 extras (bounds_next.cu): kind 0 = LB_New, 1 = LB_Improved (all pairs, measurement kernels)
+// NEXT-4 (bounds_improved.cu): lb[q][n] += sum over columns [c_lo, c_hi) of the LB_Keogh term of
+// t_n against the envelope of q's projection onto t_n's envelope (LB_Improved's second pass, O(L))
+int launch_lb_improved_pass(const float *q, int64_t nq, const float *t, const float *U,
+                            const float *Lo, int64_t nt, int L, int w, int c_lo, int c_hi,
+                            float *lb, int64_t ldlb, int num_sms, cudaStream_t st);
+// S2 finish for bounds assembled outside the tile kernel: max with LB_Kim (qkim non-null), the
+// leave-one-out self pair -> NaN, per-query argmin key (atomicMin into minkey, pre-filled kNone)
+int launch_bound_finish(float *lb, int64_t ldlb, int64_t nq, int64_t nt, const float *q,
+                        const float *t, const nndtw_kim *qkim, const nndtw_kim *tkim, int L,
+                        int64_t self_offset, unsigned long long *minkey, cudaStream_t st);
+// S2 extras (bounds_next.cu): LB_New, all pairs (kind 0; O(L*w) per pair as the bound is defined)
 int launch_lb_pairs(int kind, const float *q, int64_t nq, const float *t, const float *U,
                     const float *Lo, int64_t nt, int L, int w, float *lb, int64_t ldlb,
                     cudaStream_t st);

@@ -286,16 +286,9 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
                     (unsigned)nn == s1 || (unsigned)nn == s2)
                     continue;
                 const float full = p.lb[qq * p.ldlb + nn];
-                float kim = 0.0f;
-                if (p.with_kim) {
-                    nndtw_kim ka = S.qk[rq], kb = S.tk[rn];
-                    kim = sq(qhv(qi, 0) - thv(j, 0)) + sq(qtv(qi, 0) - ttv(j, 0));
-                    bool okmin = ka.imin != 0 && ka.imin != L - 1 && kb.imin != 0 && kb.imin != L - 1;
-                    if (okmin) kim = kim + sq(ka.vmin - kb.vmin);
-                    bool okmax = ka.imax != 0 && ka.imax != L - 1 && kb.imax != 0 &&
-                                 kb.imax != L - 1 && !(okmin && (ka.imax == ka.imin || kb.imax == kb.imin));
-                    if (okmax) kim = kim + sq(ka.vmax - kb.vmax);
-                }
+                const float kim = p.with_kim ? kim_sum(qhv(qi, 0), qtv(qi, 0), thv(j, 0),
+                                                       ttv(j, 0), S.qk[rq], S.tk[rn], L)
+                                             : 0.0f;
                 if (kim > thr) c0 += 1;
                 else if (full > thr) {
                     if (acc[qi][j] > thr) c1 += 1;
@@ -328,16 +321,9 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
             const int rn = lane + 32 * j;
             const int64_t nn = n0 + rn;
             float v = acc[qi][j];
-            if (p.with_kim) {
-                nndtw_kim ka = S.qk[rq], kb = S.tk[rn];
-                float kim = sq(qhv(qi, 0) - thv(j, 0)) + sq(qtv(qi, 0) - ttv(j, 0));
-                bool okmin = ka.imin != 0 && ka.imin != L - 1 && kb.imin != 0 && kb.imin != L - 1;
-                if (okmin) kim = kim + sq(ka.vmin - kb.vmin);
-                bool okmax = ka.imax != 0 && ka.imax != L - 1 && kb.imax != 0 &&
-                             kb.imax != L - 1 && !(okmin && (ka.imax == ka.imin || kb.imax == kb.imin));
-                if (okmax) kim = kim + sq(ka.vmax - kb.vmax);
-                v = fmaxf(v, kim);
-            }
+            if (p.with_kim)
+                v = fmaxf(v, kim_sum(qhv(qi, 0), qtv(qi, 0), thv(j, 0), ttv(j, 0), S.qk[rq],
+                                     S.tk[rn], L));
             if (p.transposed) {
                 if (qq < p.nq && nn < p.nt) {
                     float *dst = p.lb + nn * p.ldlb + qq;

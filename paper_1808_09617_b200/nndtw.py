@@ -29,6 +29,15 @@ NNDTW_CLASSIFY_PHASE_SEARCH = 16
 NNDTW_CLASSIFY_PHASE_SEARCH_A = 32
 NNDTW_CLASSIFY_PHASE_SEARCH_B = 64
 NNDTW_CLASSIFY_LEVEL_STATS = 128
+NNDTW_CLASSIFY_BOUND_IMPROVED = 256
+NNDTW_CLASSIFY_BOUND_NEW = 512
+NNDTW_CLASSIFY_BOUND_ENHANCED_IMPROVED = 1024
+NNDTW_CLASSIFY_BOUND_NONE = 2048
+# S2 bound of Model(bound=...) -> classify flag
+BOUND_FLAGS = {"enhanced": 0, "keogh": NNDTW_CLASSIFY_BOUND_KEOGH,
+               "improved": NNDTW_CLASSIFY_BOUND_IMPROVED, "new": NNDTW_CLASSIFY_BOUND_NEW,
+               "enhanced_improved": NNDTW_CLASSIFY_BOUND_ENHANCED_IMPROVED,
+               "none": NNDTW_CLASSIFY_BOUND_NONE}
 KEY_INIT = 0x7F800000FFFFFFFF
 
 
@@ -79,6 +88,8 @@ _SIGS = {
     "nndtw_lb_enhanced_symmetric": (C.c_int, [_P, _P, _P, _P, _I64, _P, _P, _P, _P, _I64, _I32,
                                               _I32, _I32, C.c_uint32, _P, _I64, _P]),
     "nndtw_lb_improved": (C.c_int, [_P, _I64, _P, _P, _P, _I64, _I32, _I32, _P, _I64, _P]),
+    "nndtw_lb_enhanced_improved": (C.c_int, [_P, _I64, _P, _P, _P, _I64, _I32, _I32, _I32, _P,
+                                             _I64, _P]),
     "nndtw_lb_new": (C.c_int, [_P, _I64, _P, _I64, _I32, _I32, _P, _I64, _P]),
     "nndtw_tightness": (C.c_int, [_P, _P, _I64, _P, _P, _P, _P]),
     "nndtw_dtw_batch": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P]),
@@ -212,6 +223,19 @@ def lb_improved(q, t, w: int, t_env=None, stream=None) -> torch.Tensor:
     return out
 
 
+def lb_enhanced_improved(q, t, w: int, v: int, t_env=None, stream=None) -> torch.Tensor:
+    """LB_Enhanced^V with the LB_Improved bridge for all pairs [nq][nt]."""
+    _series(q, "q"); _series(t, "t")
+    nq, L = q.shape
+    nt = t.shape[0]
+    tU, tL = (t_env[0], t_env[1]) if t_env is not None else envelopes(t, w, False, stream)[:2]
+    out = torch.empty((nq, nt), dtype=torch.float32, device=q.device)
+    _check(load().nndtw_lb_enhanced_improved(_ptr(q), nq, _ptr(t), _ptr(tU), _ptr(tL), nt, L,
+                                             int(w), int(v), _ptr(out), nt, _stream(stream)),
+           "nndtw_lb_enhanced_improved")
+    return out
+
+
 def lb_new(q, t, w: int, stream=None) -> torch.Tensor:
     """LB_New_W for all pairs [nq][nt]."""
     _series(q, "q"); _series(t, "t")
@@ -279,8 +303,10 @@ class Model:
         self.w = min(int(w), self.L - 1)
         self.v = int(v)
         self.index_base = int(index_base)
-        if bound not in ("enhanced", "keogh"):
-            raise NNDTWError("bound must be 'enhanced' or 'keogh'")
+        if bound not in BOUND_FLAGS:
+            raise NNDTWError(f"bound must be one of {sorted(BOUND_FLAGS)}")
+        if symmetric and bound not in ("enhanced", "keogh"):
+            raise NNDTWError("symmetric applies to the 'enhanced' and 'keogh' bounds only")
         self.bound = bound
         self.symmetric = bool(symmetric)
         self.U, self.Lo, self.kim = envelopes(train, self.w, True, stream)
@@ -314,7 +340,7 @@ def classify_keys(model: Model, q: torch.Tensor, exact: bool = True, self_offset
         ws = model.workspace(nq)
         key = torch.empty(nq, dtype=torch.int64, device=q.device)
     flags = ((NNDTW_CLASSIFY_EXACT if exact else 0) |
-             (NNDTW_CLASSIFY_BOUND_KEOGH if model.bound == "keogh" else 0) |
+             BOUND_FLAGS[model.bound] |
              (NNDTW_CLASSIFY_BOUND_SYMMETRIC if model.symmetric else 0) |
              (NNDTW_CLASSIFY_LEVEL_STATS if (stats and level_stats) else 0) |
              {None: 0, "seed": NNDTW_CLASSIFY_PHASE_SEED,

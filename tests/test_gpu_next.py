@@ -1,6 +1,7 @@
 """GPU parity for SURVEY.md §8(f)'s next rows through the C ABI, against the fp64 oracle:
-symmetric LB_Enhanced (NEXT-2), the tightness reduction (NEXT-3), LB_Improved and LB_New
-(NEXT-4).  Bounds within relative 1e-5 (fp32 storage and accumulation, as for S2); NN indices
+symmetric LB_Enhanced (NEXT-2), the tightness reduction (NEXT-3), LB_Improved (O(L) projection
+envelope), LB_New and LB_Enhanced with the LB_Improved bridge (NEXT-4), and classify with every
+alternative S2 bound including none (NEXT-1).  Bounds within relative 1e-5 (fp32 storage and accumulation, as for S2); NN indices
 and labels bit-exact; tightness means within 1e-5 relative, pair counts exact."""
 import numpy as np
 import pytest
@@ -20,6 +21,10 @@ def _sets(seed, nq, nt, L, kinds=("walk", "int")):
 
 
 SHAPES = [(2, 0), (3, 1), (5, 4), (17, 3), (64, 0), (64, 63), (128, 13), (256, 26), (300, 30)]
+# LB_Improved's van Herk scans: chunks of 128 elements per warp, blocks of 2w+1 aligned at -w;
+# lengths around the chunk size, windows whose blocks straddle chunks and the row end
+IMP_SHAPES = SHAPES + [(127, 5), (128, 64), (129, 1), (200, 199), (257, 12), (384, 100),
+                       (512, 103), (1000, 333), (2048, 409), (2048, 2047)]
 
 
 @pytest.mark.parametrize("L,w", SHAPES)
@@ -30,12 +35,67 @@ def test_lb_new_parity(dev, oracle_lib, L, w):
     assert_rel(lb, oracle_lib.bound_matrix("new", Q, Tn, w), what="LB_New")
 
 
-@pytest.mark.parametrize("L,w", SHAPES)
+@pytest.mark.parametrize("L,w", IMP_SHAPES)
 def test_lb_improved_parity(dev, oracle_lib, L, w):
     from paper_1808_09617_b200 import nndtw
-    Q, Tn = _sets(L * 5 + w, 12, 34, L)
+    nq, nt = (12, 34) if L <= 512 else (4, 10)
+    Q, Tn = _sets(L * 5 + w, nq, nt, L)
     lb = nndtw.lb_improved(T(Q, dev), T(Tn, dev), w).cpu().numpy()
     assert_rel(lb, oracle_lib.bound_matrix("improved", Q, Tn, w), what="LB_Improved")
+
+
+@pytest.mark.parametrize("L,w", IMP_SHAPES)
+@pytest.mark.parametrize("V", [1, 5])
+def test_lb_enhanced_improved_parity(dev, oracle_lib, L, w, V):
+    from paper_1808_09617_b200 import nndtw
+    nq, nt = (12, 34) if L <= 512 else (4, 10)
+    Q, Tn = _sets(L * 3 + w + V, nq, nt, L)
+    lb = nndtw.lb_enhanced_improved(T(Q, dev), T(Tn, dev), w, V).cpu().numpy()
+    assert_rel(lb, oracle_lib.bound_matrix("enhanced_improved", Q, Tn, w, V),
+               what="LB_Enhanced with the LB_Improved bridge")
+
+
+@pytest.mark.parametrize("bound", ["improved", "new", "enhanced_improved", "none"])
+def test_classify_alternative_bounds_same_answer(dev, oracle_lib, bound):
+    """Every S2 bound (and none) gives the exact 1-NN: configs 0/1 and an integer tie grid."""
+    from paper_1808_09617_b200 import nndtw
+    cases = [(0, 100, 10), (1, 80, 20), (1, 50, 1)]
+    for cfg, nq, p in cases:
+        ds = datagen.make_dataset(cfg)
+        w = ds.cfg.windows()[0] if cfg == 0 else datagen.window_from_percent(p, 256)
+        model = nndtw.Model(T(ds.train, dev), T(ds.train_labels, dev), w, 5, bound=bound)
+        pred = nndtw.classify(model, T(ds.test[:nq], dev), stats=True, level_stats=True)
+        _check_nn(oracle_lib, ds.train, ds.train_labels, ds.test[:nq], w,
+                  pred.idx.cpu().numpy(), pred.label.cpu().numpy(), pred.dist.cpu().numpy())
+        st = pred.stats
+        pruned = st["pruned_kim"] + st["pruned_bands"] + st["pruned_keogh"]
+        assert pruned + st["survivors"] + nq == st["lb_pairs"], (bound, st)
+        if bound == "none":
+            assert pruned == 0 and st["survivors"] == st["lb_pairs"] - nq
+    rng = np.random.default_rng(91)
+    Tr = datagen.random_series(rng, 70, 29, "int")
+    Tr = np.concatenate([Tr, Tr[:20]])
+    Q = datagen.random_series(rng, 30, 29, "int")
+    lab = np.arange(Tr.shape[0], dtype=np.int32) % 5
+    model = nndtw.Model(T(Tr, dev), T(lab, dev), 3, 2, bound=bound)
+    pred = nndtw.classify(model, T(Q, dev))
+    _check_nn(oracle_lib, Tr, lab, Q, 3, pred.idx.cpu().numpy(), pred.label.cpu().numpy(),
+              pred.dist.cpu().numpy(), V=2)
+
+
+@pytest.mark.parametrize("bound", ["improved", "enhanced_improved", "none"])
+def test_loocv_style_self_exclusion_alternative_bounds(dev, oracle_lib, bound):
+    """classify with self_offset (the leave-one-out self pair) under an alternative bound: the
+    held-out series is never its own neighbour."""
+    from paper_1808_09617_b200 import nndtw
+    ds = datagen.make_dataset(3, n_train=150)
+    X, lab = ds.train, ds.train_labels
+    w = 15
+    model = nndtw.Model(T(X, dev), T(lab, dev), w, 5, bound=bound)
+    key, _, _ = nndtw.classify_keys(model, T(X, dev), exact=True, self_offset=0)
+    idx, _, _ = nndtw.finalize(key, model.labels)
+    _, rnn = oracle_lib.loocv(X, lab, [w], V=5)
+    assert np.array_equal(idx.cpu().numpy(), rnn[0])
 
 
 @pytest.mark.parametrize("L,w,V", [(2, 1, 1), (16, 3, 2), (64, 0, 5), (128, 13, 5),
@@ -105,6 +165,7 @@ def test_tightness_parity(dev, oracle_lib, L, w):
         "keogh": nndtw.lb_enhanced(q, t, U, Lo, w, 5, keogh=True),
         "enhanced": nndtw.lb_enhanced(q, t, U, Lo, w, 5),
         "improved": nndtw.lb_improved(q, t, w),
+        "enhanced_improved": nndtw.lb_enhanced_improved(q, t, w, 5),
         "new": nndtw.lb_new(q, t, w),
         "sym": nndtw.lb_enhanced_symmetric(q, t, w, 5),
     }
