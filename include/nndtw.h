@@ -158,7 +158,6 @@ NNDTW_API int nndtw_lb_enhanced_symmetric(const float *q, const float *q_upper,
  *   (§2.3.3), q' the projection of q_i onto t_j's envelope; env q' by the O(L)
  *   van Herk sliding max/min per pair ("the optimised algorithm to compute the projection
  *   envelopes").  t_upper / t_lower: t's envelopes (nndtw_envelopes, same w).
- *   L <= 10240 (E_LENGTH otherwise).
  * nndtw_lb_enhanced_improved: LB_Enhanced^V_W with the LB_Improved bridge (reading
  *   C21): nndtw_lb_enhanced's value plus, over the bridge columns n_bands+1 .. L-n_bands, the
  *   LB_Keogh terms of t_j against the envelope of q'.  Admissible; >= LB_Enhanced^V.

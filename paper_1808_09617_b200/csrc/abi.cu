@@ -194,7 +194,6 @@ static void exact_local(ClassifyWs &W, const float *q, int64_t nq, const float *
                         int L, int w, int64_t index_base, unsigned long long *key,
                         unsigned long long *cnt, int sms, cudaStream_t st) {
     const float eps_p = eps_prune(L), eps_t = eps_tie(L);
-    cudaMemsetAsync(W.tiecnt, 0, 4 * (size_t)nq, st);
     launch_tie_count(W.log, W.log_count, W.log_cap, key, eps_t, W.tiecnt, sms, st);
     launch_refine(W.log, W.log_count, W.log_cap, q, t, L, w, key, eps_t, W.f64key, cnt,
                   W.tiecnt, W.overflow, sms, st);
@@ -261,9 +260,6 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     if (alt & (alt - 1)) return fail(NNDTW_E_ARG, "more than one alternative bound flag");
     if (alt && (keogh || sym))
         return fail(NNDTW_E_ARG, "an alternative bound cannot be combined with KEOGH/SYMMETRIC");
-    if ((alt & (NNDTW_CLASSIFY_BOUND_IMPROVED | NNDTW_CLASSIFY_BOUND_ENHANCED_IMPROVED)) &&
-        L > 10240)
-        return fail(NNDTW_E_LENGTH, "the LB_Improved passes need L <= 10240");
     const bool alt_none = (alt & NNDTW_CLASSIFY_BOUND_NONE) != 0;
     // cascade levels for the level counters: band level only where Algorithm 1's bands exist
     const int count_no_bands = (keogh || (alt && !(alt & NNDTW_CLASSIFY_BOUND_ENHANCED_IMPROVED)))
@@ -273,12 +269,8 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
 
     tm.mark();  // 0
     if (do_seed) {
-        cudaMemsetAsync(W.counters, 0, sizeof(unsigned long long) * (CNT_N + 3), st);
-        launch_fill_u64(key, nq, kKeyInit, st);
-        cudaMemsetAsync(W.minkey, 0xff, 8 * (size_t)nq, st);
-        launch_fill_u64(W.f64key, nq, kNone64, st);
-        launch_fill_u64(W.resolve_out, nq, kNone64, st);
-        cudaMemsetAsync(W.overflow, 0, 4 * (size_t)nq, st);
+        launch_classify_init(nq, key, W.minkey, W.f64key, W.resolve_out, W.overflow, W.tiecnt,
+                             W.counters, CNT_N + 3, W.buckets, st);
         launch_cells_prefix(L, w, W.cells_prefix, st);
     }
     tm.mark();  // 1
@@ -549,7 +541,6 @@ int nndtw_lb_improved(const float *q, int64_t nq, const float *t, const float *t
     if ((rc = check_common(nq, L, w))) return rc;
     if (nt < 0) return fail(NNDTW_E_ARG, "negative nt");
     if (ldlb < nt) return fail(NNDTW_E_ARG, "ldlb < nt");
-    if (L > 10240) return fail(NNDTW_E_LENGTH, "LB_Improved needs L <= 10240");
     if (nq > 0 && nt > 0 && (!q || !t || !t_upper || !t_lower || !lb))
         return fail(NNDTW_E_ARG, "null pointer argument");
     cudaStream_t st = (cudaStream_t)stream;
@@ -570,7 +561,6 @@ int nndtw_lb_enhanced_improved(const float *q, int64_t nq, const float *t, const
     if (nt < 0) return fail(NNDTW_E_ARG, "negative nt");
     if (v < 1) return fail(NNDTW_E_V, "V must be >= 1");
     if (ldlb < nt) return fail(NNDTW_E_ARG, "ldlb < nt");
-    if (L > 10240) return fail(NNDTW_E_LENGTH, "the LB_Improved bridge needs L <= 10240");
     if (nq > 0 && nt > 0 && (!q || !t || !t_upper || !t_lower || !lb))
         return fail(NNDTW_E_ARG, "null pointer argument");
     cudaStream_t st = (cudaStream_t)stream;

@@ -11,27 +11,28 @@
 //   U'_j = max(h[j-w], g[j+w])                       (one block boundary inside the window)
 // with h[j-w] = h[0] for j-w < 0 (the pads of block 0 are -inf) and g[j+w] = g[L-1] when j+w
 // lies past the end in L-1's block, -inf when it lies in a later block (h[j-w] then already
-// covers [j-w, L-1]).  The prefix / suffix scans are warp-segmented scans (resets at block
-// starts / ends) over chunks of 32*CE elements with a carry across chunks: O(1) work per
-// element, independent of w.
+// covers [j-w, L-1]).  The projection of the whole row is computed first (all of its loads in
+// flight at once, float4 where aligned) into shared memory; the prefix / suffix scans are
+// warp-segmented scans (resets at block starts / ends) over chunks of 32*CE elements with a
+// carry across chunks: O(1) work per element, independent of w.
 //
 // The kernel computes only the SECOND pass, sum over columns j in [c_lo, c_hi) of
 // keogh(B_j, L'_j, U'_j), and ADDS it to lb[q][n]; the first pass is the LB tile kernel
 // (lb.cu):
 //   * LB_Improved           = tile kernel in LB_Keogh mode            + pass over [0, L)
 //   * LB_Enhanced^V with the LB_Improved bridge (reading C21)
-//                           = tile kernel (bands + LB_Keogh bridge)   + pass over
-//                             [nb + w, L - nb - w), the columns whose window lies inside the
-//                             bridge rows [nb, L - nb).
+//                           = tile kernel (bands + LB_Keogh bridge)   + pass over the bridge
+//                             columns [nb, L - nb).
 // Both stay admissible: for a path cell (i, j) with |i-j| <= w, B_j is inside [L^B_i, U^B_i],
 // so (A_i - B_j)^2 >= (A_i - A'_i)^2 + (A'_i - B_j)^2 (the cross term is >= 0); the first
-// terms are counted once per row (the Keogh terms), the second once per column of the range
-// (every path visits each such column in some bridge row), reading C21.
+// parts are counted once per (bridge) row -- the Keogh terms --, the second once per column of
+// the range, and no cell of a bridge column lies in one of Algorithm 1's bands (DESIGN.md
+// reading C21).
 #include "launchers.cuh"
 
 namespace nndtw {
 
-constexpr int IMP_CE = 4;                 // elements per lane per chunk
+constexpr int IMP_CE = 8;                 // elements per lane per chunk
 constexpr int IMP_CH = 32 * IMP_CE;       // elements per chunk
 
 struct MaxMin {
@@ -56,6 +57,21 @@ __device__ __forceinline__ void seg_scan(int &f, MaxMin &v, int lane) {
     }
 }
 
+// 8 consecutive floats of a row (vectorised when the row is 16-byte aligned)
+template <bool VEC>
+__device__ __forceinline__ void load8(const float *p, int j0, int L, float (&x)[IMP_CE]) {
+    if (VEC && j0 + IMP_CE <= L) {
+        const float4 lo = __ldg(reinterpret_cast<const float4 *>(p + j0));
+        const float4 hi = __ldg(reinterpret_cast<const float4 *>(p + j0 + 4));
+        x[0] = lo.x; x[1] = lo.y; x[2] = lo.z; x[3] = lo.w;
+        x[4] = hi.x; x[5] = hi.y; x[6] = hi.z; x[7] = hi.w;
+    } else {
+#pragma unroll
+        for (int e = 0; e < IMP_CE; ++e) x[e] = j0 + e < L ? __ldg(p + j0 + e) : 0.0f;
+    }
+}
+
+template <bool VEC>
 __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restrict__ q, int64_t nq,
                                                           const float *__restrict__ t,
                                                           const float *__restrict__ U,
@@ -63,111 +79,149 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
                                                           int64_t nt, int L, int w, int c_lo,
                                                           int c_hi, float *lb, int64_t ldlb,
                                                           int rows_per_warp) {
-    extern __shared__ float imp_smem[];
+    extern __shared__ __align__(16) float imp_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
-    float *ap = imp_smem + (size_t)warp * 5 * L;  // A' [L]
-    float *gx = ap + L, *gn = gx + L, *hx = gn + L, *hn = hx + L;
+    const int Lp = (L + IMP_CH - 1) / IMP_CH * IMP_CH;  // rows padded to whole chunks
+    float *ap = imp_smem + (size_t)warp * 6 * Lp;      // A' [Lp]
+    float *gx = ap + Lp, *gn = gx + Lp, *hx = gn + Lp, *hn = hx + Lp, *bs = hn + Lp;
     const int K = 2 * w + 1;
-    const int nch = (L + IMP_CH - 1) / IMP_CH;
+    const int nch = Lp / IMP_CH;
     const int64_t npairs = nq * nt;
-    for (int64_t pr = ((int64_t)blockIdx.x * nwarps + warp) * rows_per_warp, pe = pr + rows_per_warp;
-         pr < pe && pr < npairs; ++pr) {
+    // last index of the block holding L-1: g[j+w] for j+w in L-1..blast_end is g[L-1]
+    const int blast_end = ((L - 1 + w) / K + 1) * K - w - 1;
+    const int64_t pr0 = ((int64_t)blockIdx.x * nwarps + warp) * rows_per_warp;
+    const int64_t pe = pr0 + rows_per_warp < npairs ? pr0 + rows_per_warp : npairs;
+    // the next pair's first chunk is loaded while this pair is scanned (software pipeline: the
+    // per-pair chain of load -> scans -> gather is latency-bound otherwise)
+    float na[IMP_CE], nl[IMP_CE], nu[IMP_CE], nb[IMP_CE];
+    auto load_chunk0 = [&](int64_t pr) {
+        const int64_t qi = pr / nt, ni = pr - qi * nt;
+        const int j0 = lane * IMP_CE;
+        load8<VEC>(q + qi * L, j0, L, na);
+        load8<VEC>(Lo + ni * L, j0, L, nl);
+        load8<VEC>(U + ni * L, j0, L, nu);
+        load8<VEC>(t + ni * L, j0, L, nb);
+    };
+    if (pr0 < pe) load_chunk0(pr0);
+    for (int64_t pr = pr0; pr < pe; ++pr) {
         const int64_t qi = pr / nt, ni = pr - qi * nt;
         const float *a = q + qi * L, *b = t + ni * L, *u = U + ni * L, *lo = Lo + ni * L;
-        // ---- projection A' and the forward (prefix) segmented scan ----------------------
+        // ---- projection A' (and the row of B) into shared memory ---------------------------
+        {
+            const int j0 = lane * IMP_CE;
+#pragma unroll
+            for (int e = 0; e < IMP_CE; ++e) {
+                ap[j0 + e] = fminf(fmaxf(na[e], nl[e]), nu[e]);
+                bs[j0 + e] = nb[e];
+            }
+        }
+#pragma unroll 2
+        for (int c = 1; c < nch; ++c) {
+            const int j0 = c * IMP_CH + lane * IMP_CE;
+            float xa[IMP_CE], xl[IMP_CE], xu[IMP_CE], xb[IMP_CE];
+            load8<VEC>(a, j0, L, xa);
+            load8<VEC>(lo, j0, L, xl);
+            load8<VEC>(u, j0, L, xu);
+            load8<VEC>(b, j0, L, xb);
+#pragma unroll
+            for (int e = 0; e < IMP_CE; ++e) {
+                ap[j0 + e] = fminf(fmaxf(xa[e], xl[e]), xu[e]);
+                bs[j0 + e] = xb[e];
+            }
+        }
+        if (pr + 1 < pe) load_chunk0(pr + 1);
+        __syncwarp();
+        // ---- forward (prefix) segmented scan: resets at block starts (j + w) % K == 0 ------
         MaxMin carry{-kInf, kInf};
         for (int c = 0; c < nch; ++c) {
             const int j0 = c * IMP_CH + lane * IMP_CE;
             float x[IMP_CE];
+            bool rs[IMP_CE];
+            int pos = (j0 + w) % K;
+#pragma unroll
+            for (int e = 0; e < IMP_CE; ++e) {
+                x[e] = ap[j0 + e];
+                rs[e] = pos == 0 && j0 + e < L;
+                pos = pos + 1 == K ? 0 : pos + 1;
+            }
             MaxMin run{-kInf, kInf};
             int f = 0;
 #pragma unroll
             for (int e = 0; e < IMP_CE; ++e) {
-                const int j = j0 + e;
-                float v = 0.0f;
-                if (j < L) v = fminf(fmaxf(__ldg(a + j), __ldg(lo + j)), __ldg(u + j));
-                x[e] = v;
-                if (j < L) ap[j] = v;
-                const bool reset = ((j + w) % K) == 0;
-                if (j < L) {
-                    if (reset) { run.mx = v; run.mn = v; f = 1; }
-                    else { run.mx = fmaxf(run.mx, v); run.mn = fminf(run.mn, v); }
-                }
+                if (rs[e]) { run.mx = x[e]; run.mn = x[e]; f = 1; }
+                else { run.mx = fmaxf(run.mx, x[e]); run.mn = fminf(run.mn, x[e]); }
             }
             MaxMin inc = run;
             int fi = f;
             seg_scan<true>(fi, inc, lane);
             // carry into this lane = inclusive result of lane-1 (combined with the chunk carry)
             MaxMin cin;
-            int fprev;
             cin.mx = __shfl_up_sync(0xffffffffu, inc.mx, 1);
             cin.mn = __shfl_up_sync(0xffffffffu, inc.mn, 1);
-            fprev = __shfl_up_sync(0xffffffffu, fi, 1);
-            if (lane == 0) { cin = carry; fprev = 1; }
+            const int fprev = __shfl_up_sync(0xffffffffu, fi, 1);
+            if (lane == 0) cin = carry;
             else if (!fprev) { cin.mx = fmaxf(cin.mx, carry.mx); cin.mn = fminf(cin.mn, carry.mn); }
-            // rewrite this lane's prefix values: carry applies until the lane's first reset
-            MaxMin r = cin;
+            MaxMin r = cin;  // the carry applies until the lane's first reset
 #pragma unroll
             for (int e = 0; e < IMP_CE; ++e) {
-                const int j = j0 + e;
-                if (j < L) {
-                    if (((j + w) % K) == 0) { r.mx = x[e]; r.mn = x[e]; }
-                    else { r.mx = fmaxf(r.mx, x[e]); r.mn = fminf(r.mn, x[e]); }
-                    gx[j] = r.mx;
-                    gn[j] = r.mn;
-                }
+                if (rs[e]) { r.mx = x[e]; r.mn = x[e]; }
+                else { r.mx = fmaxf(r.mx, x[e]); r.mn = fminf(r.mn, x[e]); }
+                gx[j0 + e] = r.mx;
+                gn[j0 + e] = r.mn;
             }
-            // chunk carry = value after the last element of the chunk (lane 31)
             carry.mx = __shfl_sync(0xffffffffu, r.mx, 31);
             carry.mn = __shfl_sync(0xffffffffu, r.mn, 31);
         }
-        __syncwarp();
-        // ---- backward (suffix) segmented scan: resets at block ends ---------------------
+        // ---- backward (suffix) segmented scan: resets at block ends (j + w + 1) % K == 0 ---
+        // (elements past L-1 are the +-inf pads: identities, never resets)
         carry = MaxMin{-kInf, kInf};
         for (int c = nch - 1; c >= 0; --c) {
             const int j0 = c * IMP_CH + lane * IMP_CE;
             float x[IMP_CE];
+            bool re[IMP_CE];
+            int pos = (j0 + w) % K;
+#pragma unroll
+            for (int e = 0; e < IMP_CE; ++e) {
+                const bool in = j0 + e < L;
+                x[e] = ap[j0 + e];
+                re[e] = pos == K - 1 && in;
+                pos = pos + 1 == K ? 0 : pos + 1;
+            }
             MaxMin run{-kInf, kInf};
             int f = 0;
 #pragma unroll
             for (int e = IMP_CE - 1; e >= 0; --e) {
-                const int j = j0 + e;
-                x[e] = j < L ? ap[j] : 0.0f;
-                const bool reset = ((j + w + 1) % K) == 0;  // j is the last index of its block
-                if (j < L) {
-                    if (reset) { run.mx = x[e]; run.mn = x[e]; f = 1; }
-                    else { run.mx = fmaxf(run.mx, x[e]); run.mn = fminf(run.mn, x[e]); }
-                }
+                if (j0 + e >= L) continue;
+                if (re[e]) { run.mx = x[e]; run.mn = x[e]; f = 1; }
+                else { run.mx = fmaxf(run.mx, x[e]); run.mn = fminf(run.mn, x[e]); }
             }
             MaxMin inc = run;
             int fi = f;
             seg_scan<false>(fi, inc, lane);
             MaxMin cin;
-            int fnext;
             cin.mx = __shfl_down_sync(0xffffffffu, inc.mx, 1);
             cin.mn = __shfl_down_sync(0xffffffffu, inc.mn, 1);
-            fnext = __shfl_down_sync(0xffffffffu, fi, 1);
-            if (lane == 31) { cin = carry; fnext = 1; }
+            const int fnext = __shfl_down_sync(0xffffffffu, fi, 1);
+            if (lane == 31) cin = carry;
             else if (!fnext) { cin.mx = fmaxf(cin.mx, carry.mx); cin.mn = fminf(cin.mn, carry.mn); }
             MaxMin r = cin;
 #pragma unroll
             for (int e = IMP_CE - 1; e >= 0; --e) {
-                const int j = j0 + e;
-                if (j < L) {
-                    if (((j + w + 1) % K) == 0) { r.mx = x[e]; r.mn = x[e]; }
+                if (j0 + e < L) {
+                    if (re[e]) { r.mx = x[e]; r.mn = x[e]; }
                     else { r.mx = fmaxf(r.mx, x[e]); r.mn = fminf(r.mn, x[e]); }
-                    hx[j] = r.mx;
-                    hn[j] = r.mn;
                 }
+                hx[j0 + e] = r.mx;
+                hn[j0 + e] = r.mn;
             }
             carry.mx = __shfl_sync(0xffffffffu, r.mx, 0);
             carry.mn = __shfl_sync(0xffffffffu, r.mn, 0);
         }
         __syncwarp();
         // ---- envelope of A' at column j and the LB_Keogh(B, env A') terms ---------------
-        const int blast = (L - 1 + w) / K;  // block of index L-1
         float acc = 0.0f;
+#pragma unroll 4
         for (int j = c_lo + lane; j < c_hi; j += 32) {
             const int jl = j - w < 0 ? 0 : j - w;
             const int jr = j + w;
@@ -175,11 +229,11 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
             if (jr <= L - 1) {
                 ux = fmaxf(ux, gx[jr]);
                 un = fminf(un, gn[jr]);
-            } else if ((jr + w) / K == blast) {
+            } else if (jr <= blast_end) {
                 ux = fmaxf(ux, gx[L - 1]);
                 un = fminf(un, gn[L - 1]);
             }
-            const float bj = __ldg(b + j);
+            const float bj = bs[j];
             const float d = fmaxf(fmaxf(bj - ux, un - bj), 0.0f);
             acc = fmaf(d, d, acc);
         }
@@ -198,19 +252,31 @@ int launch_lb_improved_pass(const float *q, int64_t nq, const float *t, const fl
     if (c_lo < 0) c_lo = 0;
     if (c_hi > L) c_hi = L;
     if (c_hi <= c_lo) return 0;
-    const size_t warp_bytes = (size_t)5 * L * sizeof(float);
-    int warps = (int)((200 * 1024) / warp_bytes);
-    if (warps < 1) return -1;  // L > 10240
+    const int Lp = (L + IMP_CH - 1) / IMP_CH * IMP_CH;
+    const size_t warp_bytes = (size_t)6 * Lp * sizeof(float);
+    int warps = (int)((110 * 1024) / warp_bytes);  // two CTAs per SM
+    if (warps < 1) warps = (int)((220 * 1024) / warp_bytes);
+    if (warps < 1) return -1;  // L > 9216
     if (warps > 8) warps = 8;
     const size_t smem = warps * warp_bytes;
     const int64_t npairs = nq * nt;
-    int64_t want = (int64_t)num_sms * 8 * warps;  // warps in flight
-    int rows = (int)((npairs + want - 1) / want);
+    const int64_t want = (int64_t)num_sms * 2 * warps;  // warps resident
+    int rows = (int)((npairs + want * 4 - 1) / (want * 4));  // ~4 waves of pairs per warp slot
     if (rows < 1) rows = 1;
     const int64_t grid = (npairs + (int64_t)warps * rows - 1) / ((int64_t)warps * rows);
-    cudaFuncSetAttribute(k_lb_improved_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_lb_improved_pass<<<(unsigned)grid, 32 * warps, smem, st>>>(q, nq, t, U, Lo, nt, L, w, c_lo,
-                                                                  c_hi, lb, ldlb, rows);
+    const bool vec = (L % 4) == 0 && ((uintptr_t)q % 16) == 0 && ((uintptr_t)U % 16) == 0 &&
+                     ((uintptr_t)Lo % 16) == 0;
+    if (vec) {
+        cudaFuncSetAttribute(k_lb_improved_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        k_lb_improved_pass<true><<<(unsigned)grid, 32 * warps, smem, st>>>(
+            q, nq, t, U, Lo, nt, L, w, c_lo, c_hi, lb, ldlb, rows);
+    } else {
+        cudaFuncSetAttribute(k_lb_improved_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        k_lb_improved_pass<false><<<(unsigned)grid, 32 * warps, smem, st>>>(
+            q, nq, t, U, Lo, nt, L, w, c_lo, c_hi, lb, ldlb, rows);
+    }
     count_launch(1, __func__);
     return 0;
 }

@@ -115,6 +115,12 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
                 a[r] = i < L ? __ldg(ga + i) : 0x1p64f * 3.0f;  // rows past the end: +inf cells
                 Dl[r] = kInf;                                    // D(i, -1) = +inf
             }
+            // rows of a sub-block in aligned register pairs: the differences of two rows against
+            // the sub-block's one column value are one FADD2 with a broadcast operand
+            // (a_R - b, a_R+1 - b) -- bit-identical to two FADDs, half the issue slots
+            unsigned long long ap[RR / 2 > 0 ? RR / 2 : 1];
+#pragma unroll
+            for (int m = 0; m < RR / 2; ++m) ap[m] = f2_pack(a[2 * m], a[2 * m + 1]);
             // Block suffix minima of the row above (the previous strip's bottom row):
             // bsuf[m] = min over columns >= 32m.  With the lanes' frontier they form a cut of
             // every warping path at any step of the strip (see the checkpoint below).
@@ -165,10 +171,20 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
                     float dgv = (k == 0) ? up_prev : pb2[k - 1];
                     float upv = (k == 0) ? up : Dl[k * RB - 1];
                     nb2[k] = Dl[k * RB + RB - 1];
+                    float tt[RB];
 #pragma unroll
                     for (int r = 0; r < RB; ++r) {
                         const int R = k * RB + r;
-                        const float t = a[R] - b;
+                        if ((RB % 2) == 0 && (r % 2) == 0) {
+                            f2_unpack(f2_sub(ap[R / 2], f2_pack(b, b)), tt[r], tt[r + 1]);
+                        } else if ((RB % 2) != 0) {
+                            tt[r] = a[R] - b;
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < RB; ++r) {
+                        const int R = k * RB + r;
+                        const float t = tt[r];
                         const float old = Dl[R];
                         float nv = fmaf(t, t, fminf(fminf(old, dgv), upv));
                         if (MASK) {

@@ -39,6 +39,10 @@ int launch_tightness(const float *lb, const float *d, int64_t n, double *sum,
                      unsigned long long *count, unsigned *max_bits, int num_sms,
                      cudaStream_t st);
 int launch_fill_u64(unsigned long long *p, int64_t n, unsigned long long v, cudaStream_t st);
+int launch_classify_init(int64_t nq, unsigned long long *key, unsigned long long *minkey,
+                         unsigned long long *f64key, unsigned long long *resolve_out,
+                         unsigned *overflow, unsigned *tiecnt, unsigned long long *counters,
+                         int ncounters, unsigned long long *bucket_count, cudaStream_t st);
 int launch_seed_items(const unsigned long long *minkey, const int32_t *seed2, int64_t nq,
                       int64_t nt, Item *items, unsigned long long *count, cudaStream_t st);
 int launch_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,

@@ -22,6 +22,41 @@ int launch_fill_u64(unsigned long long *p, int64_t n, unsigned long long v, cuda
     return 0;
 }
 
+// ---- classify call initialisation: every per-query slot and the counters in one launch --------
+// key = (+inf, none), minkey = none, f64key = resolve_out = kNone64, overflow = tiecnt = 0,
+// counters = 0, survivor-bucket counts = 0 (config-1-sized calls are a chain of small
+// launches; this replaces seven)
+__global__ void k_classify_init(int64_t nq, unsigned long long *key,
+                                unsigned long long *minkey, unsigned long long *f64key,
+                                unsigned long long *resolve_out, unsigned *overflow,
+                                unsigned *tiecnt, unsigned long long *counters, int ncounters,
+                                unsigned long long *bucket_count) {
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i0 < ncounters) counters[i0] = 0ull;
+    if (i0 < NBUCKET) bucket_count[i0] = 0ull;
+    for (int64_t i = i0; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
+        key[i] = kKeyInit;
+        minkey[i] = kNone;
+        f64key[i] = kNone64;
+        resolve_out[i] = kNone64;
+        overflow[i] = 0u;
+        tiecnt[i] = 0u;
+    }
+}
+
+int launch_classify_init(int64_t nq, unsigned long long *key, unsigned long long *minkey,
+                         unsigned long long *f64key, unsigned long long *resolve_out,
+                         unsigned *overflow, unsigned *tiecnt, unsigned long long *counters,
+                         int ncounters, unsigned long long *bucket_count, cudaStream_t st) {
+    int64_t grid = (nq + 255) / 256;
+    if (grid < 1) grid = 1;
+    if (grid > 4096) grid = 4096;
+    k_classify_init<<<(unsigned)grid, 256, 0, st>>>(nq, key, minkey, f64key, resolve_out, overflow,
+                                                    tiecnt, counters, ncounters, bucket_count);
+    count_launch(1, __func__);
+    return 0;
+}
+
 // ---- S3 seeds: the argmin-LB candidate of every query (and optionally a second candidate) -----
 __global__ void k_seed_items(const unsigned long long *minkey, const int32_t *seed2, int64_t nq,
                              int64_t nt, Item *items, unsigned long long *count) {
@@ -163,9 +198,8 @@ int launch_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
                    unsigned long long *buckets, unsigned long long capacity, int num_sms,
                    cudaStream_t st) {
     if (nq == 0 || nt == 0) return 0;
-    // buckets: [count | base | fill] x NBUCKET, zeroed here
+    // buckets: [count | base | fill] x NBUCKET; the counts were zeroed by k_classify_init
     unsigned long long *bcount = buckets, *bbase = buckets + NBUCKET, *bfill = buckets + 2 * NBUCKET;
-    cudaMemsetAsync(bcount, 0, sizeof(unsigned long long) * NBUCKET, st);
     int64_t ntiles = ((nt + CT_N - 1) / CT_N) * nq;
     int64_t grid = ntiles < (int64_t)num_sms * 8 ? ntiles : (int64_t)num_sms * 8;
     static const char *ob = getenv("NNDTW_ONE_BUCKET");  // experiments: q-major order
