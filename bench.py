@@ -162,10 +162,31 @@ def cpu_baseline_oracle(ds, w, V, target_s=15.0):
         oracle.nn(ds.test[n:n + n2], ds.train, w, V=V, mode="pruned", envelopes_UL=(U, Lo))
         el += time.perf_counter() - t0
     total = n + n2
+    # one thread on a small query subset (the single-core rate), ~target_s/3
+    n1 = max(1, min(ds.test.shape[0], int(total / max(el, 1e-3) / cores * target_s / 3)))
+    t0 = time.perf_counter()
+    oracle.nn(ds.test[:n1], ds.train, w, V=V, mode="pruned", envelopes_UL=(U, Lo), threads=1)
+    el1 = time.perf_counter() - t0
     return {"value": total / el, "unit": "queries/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"first {total} queries of the {ds.test.shape[0]} against all "
                       f"{ds.train.shape[0]} train series (fp64 oracle, paper-pruned mode ii, "
-                      f"{el:.1f} s; envelopes precomputed, not timed, as P:583)"}
+                      f"{el:.1f} s; envelopes precomputed, not timed, as P:583)",
+            "one_thread": {"value": n1 / el1, "unit": "queries/s", "cores": 1,
+                           "sample": f"first {n1} queries ({100.0 * n1 / ds.test.shape[0]:.2g} "
+                                     f"% of the {ds.test.shape[0]}), {el1:.1f} s"}}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
 
 
 def run_reference(args, cfg, ds, w, V):
@@ -199,7 +220,7 @@ def run_reference(args, cfg, ds, w, V):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_json(cfg, w, V, args.gpus),
             "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores,
-                             "kind": "oracle",
+                             "kind": "oracle", "cpu_model": cpu_model(),
                              "sample": f"{nper} queries per step (rolling through the "
                                        f"{Q.shape[0]}) against all {ds.train.shape[0]} "
                                        "train series, fp64 oracle paper-pruned search"},

@@ -71,6 +71,19 @@ __device__ __forceinline__ void load8(const float *p, int j0, int L, float (&x)[
     }
 }
 
+// 8 consecutive shared-memory floats of a lane as two 16-byte accesses: a warp's 32 lanes then
+// touch 1 KB contiguously (4 wavefronts) instead of 8-way bank conflicts at stride 8 words
+__device__ __forceinline__ void lds8(const float *p, float (&x)[IMP_CE]) {
+    const float4 lo = *reinterpret_cast<const float4 *>(p);
+    const float4 hi = *reinterpret_cast<const float4 *>(p + 4);
+    x[0] = lo.x; x[1] = lo.y; x[2] = lo.z; x[3] = lo.w;
+    x[4] = hi.x; x[5] = hi.y; x[6] = hi.z; x[7] = hi.w;
+}
+__device__ __forceinline__ void sts8(float *p, const float (&x)[IMP_CE]) {
+    *reinterpret_cast<float4 *>(p) = make_float4(x[0], x[1], x[2], x[3]);
+    *reinterpret_cast<float4 *>(p + 4) = make_float4(x[4], x[5], x[6], x[7]);
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restrict__ q, int64_t nq,
                                                           const float *__restrict__ t,
@@ -110,11 +123,11 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
         // ---- projection A' (and the row of B) into shared memory ---------------------------
         {
             const int j0 = lane * IMP_CE;
+            float xp[IMP_CE];
 #pragma unroll
-            for (int e = 0; e < IMP_CE; ++e) {
-                ap[j0 + e] = fminf(fmaxf(na[e], nl[e]), nu[e]);
-                bs[j0 + e] = nb[e];
-            }
+            for (int e = 0; e < IMP_CE; ++e) xp[e] = fminf(fmaxf(na[e], nl[e]), nu[e]);
+            sts8(ap + j0, xp);
+            sts8(bs + j0, nb);
         }
 #pragma unroll 2
         for (int c = 1; c < nch; ++c) {
@@ -124,11 +137,11 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
             load8<VEC>(lo, j0, L, xl);
             load8<VEC>(u, j0, L, xu);
             load8<VEC>(b, j0, L, xb);
+            float xp[IMP_CE];
 #pragma unroll
-            for (int e = 0; e < IMP_CE; ++e) {
-                ap[j0 + e] = fminf(fmaxf(xa[e], xl[e]), xu[e]);
-                bs[j0 + e] = xb[e];
-            }
+            for (int e = 0; e < IMP_CE; ++e) xp[e] = fminf(fmaxf(xa[e], xl[e]), xu[e]);
+            sts8(ap + j0, xp);
+            sts8(bs + j0, xb);
         }
         if (pr + 1 < pe) load_chunk0(pr + 1);
         __syncwarp();
@@ -138,10 +151,10 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
             const int j0 = c * IMP_CH + lane * IMP_CE;
             float x[IMP_CE];
             bool rs[IMP_CE];
+            lds8(ap + j0, x);
             int pos = (j0 + w) % K;
 #pragma unroll
             for (int e = 0; e < IMP_CE; ++e) {
-                x[e] = ap[j0 + e];
                 rs[e] = pos == 0 && j0 + e < L;
                 pos = pos + 1 == K ? 0 : pos + 1;
             }
@@ -163,13 +176,16 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
             if (lane == 0) cin = carry;
             else if (!fprev) { cin.mx = fmaxf(cin.mx, carry.mx); cin.mn = fminf(cin.mn, carry.mn); }
             MaxMin r = cin;  // the carry applies until the lane's first reset
+            float vx[IMP_CE], vn[IMP_CE];
 #pragma unroll
             for (int e = 0; e < IMP_CE; ++e) {
                 if (rs[e]) { r.mx = x[e]; r.mn = x[e]; }
                 else { r.mx = fmaxf(r.mx, x[e]); r.mn = fminf(r.mn, x[e]); }
-                gx[j0 + e] = r.mx;
-                gn[j0 + e] = r.mn;
+                vx[e] = r.mx;
+                vn[e] = r.mn;
             }
+            sts8(gx + j0, vx);
+            sts8(gn + j0, vn);
             carry.mx = __shfl_sync(0xffffffffu, r.mx, 31);
             carry.mn = __shfl_sync(0xffffffffu, r.mn, 31);
         }
@@ -180,12 +196,11 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
             const int j0 = c * IMP_CH + lane * IMP_CE;
             float x[IMP_CE];
             bool re[IMP_CE];
+            lds8(ap + j0, x);
             int pos = (j0 + w) % K;
 #pragma unroll
             for (int e = 0; e < IMP_CE; ++e) {
-                const bool in = j0 + e < L;
-                x[e] = ap[j0 + e];
-                re[e] = pos == K - 1 && in;
+                re[e] = pos == K - 1 && j0 + e < L;
                 pos = pos + 1 == K ? 0 : pos + 1;
             }
             MaxMin run{-kInf, kInf};
@@ -206,15 +221,18 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
             if (lane == 31) cin = carry;
             else if (!fnext) { cin.mx = fmaxf(cin.mx, carry.mx); cin.mn = fminf(cin.mn, carry.mn); }
             MaxMin r = cin;
+            float vx[IMP_CE], vn[IMP_CE];
 #pragma unroll
             for (int e = IMP_CE - 1; e >= 0; --e) {
                 if (j0 + e < L) {
                     if (re[e]) { r.mx = x[e]; r.mn = x[e]; }
                     else { r.mx = fmaxf(r.mx, x[e]); r.mn = fminf(r.mn, x[e]); }
                 }
-                hx[j0 + e] = r.mx;
-                hn[j0 + e] = r.mn;
+                vx[e] = r.mx;
+                vn[e] = r.mn;
             }
+            sts8(hx + j0, vx);
+            sts8(hn + j0, vn);
             carry.mx = __shfl_sync(0xffffffffu, r.mx, 0);
             carry.mn = __shfl_sync(0xffffffffu, r.mn, 0);
         }
