@@ -28,7 +28,7 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 def golden(c):
     f = os.path.join(GOLDEN, f"cfg{c}.npz")
     if not os.path.exists(f):
-        pytest.skip(f"{f} missing: run tests/golden/make_golden.py")
+        pytest.fail(f"{f} missing: run tests/golden/make_golden.py")
     return np.load(f)
 
 
