@@ -24,7 +24,8 @@ SHAPES = [(2, 0), (3, 1), (5, 4), (17, 3), (64, 0), (64, 63), (128, 13), (256, 2
 # LB_Improved's van Herk scans: chunks of 128 elements per warp, blocks of 2w+1 aligned at -w;
 # lengths around the chunk size, windows whose blocks straddle chunks and the row end
 IMP_SHAPES = SHAPES + [(127, 5), (128, 64), (129, 1), (200, 199), (257, 12), (384, 100),
-                       (512, 103), (1000, 333), (2048, 409), (2048, 2047)]
+                       (512, 103), (1000, 333), (2048, 409), (2048, 2047),
+                       (5000, 700)]  # > 4608: one pair per warp (the two-pair rows do not fit)
 
 
 @pytest.mark.parametrize("L,w", SHAPES)
@@ -38,7 +39,7 @@ def test_lb_new_parity(dev, oracle_lib, L, w):
 @pytest.mark.parametrize("L,w", IMP_SHAPES)
 def test_lb_improved_parity(dev, oracle_lib, L, w):
     from paper_1808_09617_b200 import nndtw
-    nq, nt = (12, 34) if L <= 512 else (4, 10)
+    nq, nt = (12, 34) if L <= 512 else ((4, 10) if L <= 2048 else (3, 5))
     Q, Tn = _sets(L * 5 + w, nq, nt, L)
     lb = nndtw.lb_improved(T(Q, dev), T(Tn, dev), w).cpu().numpy()
     assert_rel(lb, oracle_lib.bound_matrix("improved", Q, Tn, w), what="LB_Improved")
@@ -48,7 +49,7 @@ def test_lb_improved_parity(dev, oracle_lib, L, w):
 @pytest.mark.parametrize("V", [1, 5])
 def test_lb_enhanced_improved_parity(dev, oracle_lib, L, w, V):
     from paper_1808_09617_b200 import nndtw
-    nq, nt = (12, 34) if L <= 512 else (4, 10)
+    nq, nt = (12, 34) if L <= 512 else ((4, 10) if L <= 2048 else (3, 5))
     Q, Tn = _sets(L * 3 + w + V, nq, nt, L)
     lb = nndtw.lb_enhanced_improved(T(Q, dev), T(Tn, dev), w, V).cpu().numpy()
     assert_rel(lb, oracle_lib.bound_matrix("enhanced_improved", Q, Tn, w, V),
