@@ -48,12 +48,12 @@ __device__ __forceinline__ void seg_scan(int &f, MaxMin &v, int lane) {
         const int of = UP ? __shfl_up_sync(0xffffffffu, f, off) : __shfl_down_sync(0xffffffffu, f, off);
         const float ox = UP ? __shfl_up_sync(0xffffffffu, v.mx, off) : __shfl_down_sync(0xffffffffu, v.mx, off);
         const float on = UP ? __shfl_up_sync(0xffffffffu, v.mn, off) : __shfl_down_sync(0xffffffffu, v.mn, off);
-        const bool in = UP ? lane >= off : lane + off < 32;
-        if (in && !f) {
-            v.mx = fmaxf(v.mx, ox);
-            v.mn = fminf(v.mn, on);
-            f = of;
-        }
+        // branch-free (selects): no divergent control flow between the shuffles, so the
+        // compiler emits plain SHFLs instead of WARPSYNC/ENDCOLLECTIVE sequences
+        const bool take = (UP ? lane >= off : lane + off < 32) && !f;
+        v.mx = take ? fmaxf(v.mx, ox) : v.mx;
+        v.mn = take ? fminf(v.mn, on) : v.mn;
+        f = take ? of : f;
     }
 }
 
@@ -93,7 +93,9 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
                                                           int c_hi, float *lb, int64_t ldlb,
                                                           int rows_per_warp) {
     extern __shared__ __align__(16) float imp_smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // warp index through a shuffle: provably warp-uniform, so the pair loop's bounds are too and
+    // the shuffles below need no divergence handling (WARPSYNC / collective sequences)
+    const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);
     const int nwarps = blockDim.x >> 5;
     const int Lp = (L + IMP_CH - 1) / IMP_CH * IMP_CH;  // rows padded to whole chunks
     float *ap = imp_smem + (size_t)warp * 6 * Lp;      // A' [Lp]
@@ -162,8 +164,9 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
             int f = 0;
 #pragma unroll
             for (int e = 0; e < IMP_CE; ++e) {
-                if (rs[e]) { run.mx = x[e]; run.mn = x[e]; f = 1; }
-                else { run.mx = fmaxf(run.mx, x[e]); run.mn = fminf(run.mn, x[e]); }
+                run.mx = fmaxf(rs[e] ? -kInf : run.mx, x[e]);
+                run.mn = fminf(rs[e] ? kInf : run.mn, x[e]);
+                f |= rs[e] ? 1 : 0;
             }
             MaxMin inc = run;
             int fi = f;
@@ -173,14 +176,17 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
             cin.mx = __shfl_up_sync(0xffffffffu, inc.mx, 1);
             cin.mn = __shfl_up_sync(0xffffffffu, inc.mn, 1);
             const int fprev = __shfl_up_sync(0xffffffffu, fi, 1);
-            if (lane == 0) cin = carry;
-            else if (!fprev) { cin.mx = fmaxf(cin.mx, carry.mx); cin.mn = fminf(cin.mn, carry.mn); }
+            {
+                const bool first = lane == 0, addc = lane == 0 || !fprev;
+                cin.mx = first ? carry.mx : (addc ? fmaxf(cin.mx, carry.mx) : cin.mx);
+                cin.mn = first ? carry.mn : (addc ? fminf(cin.mn, carry.mn) : cin.mn);
+            }
             MaxMin r = cin;  // the carry applies until the lane's first reset
             float vx[IMP_CE], vn[IMP_CE];
 #pragma unroll
             for (int e = 0; e < IMP_CE; ++e) {
-                if (rs[e]) { r.mx = x[e]; r.mn = x[e]; }
-                else { r.mx = fmaxf(r.mx, x[e]); r.mn = fminf(r.mn, x[e]); }
+                r.mx = fmaxf(rs[e] ? -kInf : r.mx, x[e]);
+                r.mn = fminf(rs[e] ? kInf : r.mn, x[e]);
                 vx[e] = r.mx;
                 vn[e] = r.mn;
             }
@@ -207,9 +213,11 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
             int f = 0;
 #pragma unroll
             for (int e = IMP_CE - 1; e >= 0; --e) {
-                if (j0 + e >= L) continue;
-                if (re[e]) { run.mx = x[e]; run.mn = x[e]; f = 1; }
-                else { run.mx = fmaxf(run.mx, x[e]); run.mn = fminf(run.mn, x[e]); }
+                // past L-1: the pads (identities), never resets
+                const float xv = j0 + e < L ? x[e] : -kInf, xn = j0 + e < L ? x[e] : kInf;
+                run.mx = fmaxf(re[e] ? -kInf : run.mx, xv);
+                run.mn = fminf(re[e] ? kInf : run.mn, xn);
+                f |= re[e] ? 1 : 0;
             }
             MaxMin inc = run;
             int fi = f;
@@ -218,16 +226,18 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
             cin.mx = __shfl_down_sync(0xffffffffu, inc.mx, 1);
             cin.mn = __shfl_down_sync(0xffffffffu, inc.mn, 1);
             const int fnext = __shfl_down_sync(0xffffffffu, fi, 1);
-            if (lane == 31) cin = carry;
-            else if (!fnext) { cin.mx = fmaxf(cin.mx, carry.mx); cin.mn = fminf(cin.mn, carry.mn); }
+            {
+                const bool first = lane == 31, addc = lane == 31 || !fnext;
+                cin.mx = first ? carry.mx : (addc ? fmaxf(cin.mx, carry.mx) : cin.mx);
+                cin.mn = first ? carry.mn : (addc ? fminf(cin.mn, carry.mn) : cin.mn);
+            }
             MaxMin r = cin;
             float vx[IMP_CE], vn[IMP_CE];
 #pragma unroll
             for (int e = IMP_CE - 1; e >= 0; --e) {
-                if (j0 + e < L) {
-                    if (re[e]) { r.mx = x[e]; r.mn = x[e]; }
-                    else { r.mx = fmaxf(r.mx, x[e]); r.mn = fminf(r.mn, x[e]); }
-                }
+                const float xv = j0 + e < L ? x[e] : -kInf, xn = j0 + e < L ? x[e] : kInf;
+                r.mx = fmaxf(re[e] ? -kInf : r.mx, xv);
+                r.mn = fminf(re[e] ? kInf : r.mn, xn);
                 vx[e] = r.mx;
                 vn[e] = r.mn;
             }
@@ -243,14 +253,11 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
         for (int j = c_lo + lane; j < c_hi; j += 32) {
             const int jl = j - w < 0 ? 0 : j - w;
             const int jr = j + w;
-            float ux = hx[jl], un = hn[jl];
-            if (jr <= L - 1) {
-                ux = fmaxf(ux, gx[jr]);
-                un = fminf(un, gn[jr]);
-            } else if (jr <= blast_end) {
-                ux = fmaxf(ux, gx[L - 1]);
-                un = fminf(un, gn[L - 1]);
-            }
+            const int jg = jr < L - 1 ? jr : L - 1;  // past L-1 in L-1's block: g[L-1]
+            const bool gok = jr <= blast_end;         // in a later block: -inf (no term)
+            const float gxv = gx[jg], gnv = gn[jg];
+            const float ux = fmaxf(hx[jl], gok ? gxv : -kInf);
+            const float un = fminf(hn[jl], gok ? gnv : kInf);
             const float bj = bs[j];
             const float d = fmaxf(fmaxf(bj - ux, un - bj), 0.0f);
             acc = fmaf(d, d, acc);

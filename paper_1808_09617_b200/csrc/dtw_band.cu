@@ -570,7 +570,10 @@ int launch_dtw_band(BandParams p, cudaStream_t st, int num_sms) {
 // ---- w = 0: DTW_0 is the squared Euclidean distance; one warp per item -------------
 __global__ void __launch_bounds__(256) k_dtw_w0(BandParams p) {
     const int lane = threadIdx.x & 31;
-    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // warp id through a shuffle and the skip test through a vote: provably warp-uniform loop
+    // control, so the reduction's shuffles need no divergence handling
+    const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) +
+                        __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     int64_t nitems = p.nitems_host;
     if (p.mode == 0) {
@@ -585,7 +588,7 @@ __global__ void __launch_bounds__(256) k_dtw_w0(BandParams p) {
             b_idx = itm.n;
             float live = key_dist(ld_relaxed_u64(p.key + a_idx));
             live = __shfl_sync(0xffffffffu, live, 0);
-            if (itm.lb > live * (1.0f + p.eps_p)) {  // pruned by the live best-so-far
+            if (__any_sync(0xffffffffu, itm.lb > live * (1.0f + p.eps_p))) {  // pruned by the live best
                 if (lane == 0 && p.counters) atomicAdd(p.counters + CNT_SKIPPED, 1ull);
                 continue;
             }

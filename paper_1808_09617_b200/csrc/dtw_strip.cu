@@ -53,7 +53,10 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
     constexpr int RB = RR / KS;
     extern __shared__ __align__(16) float smem_s[];
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+    // warp index through a shuffle and every data-dependent branch through a vote: the loop
+    // bounds and exits are then provably warp-uniform, and the per-step shuffles compile to
+    // plain SHFLs instead of divergence-safe WARPSYNC / collective sequences
+    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);
     const int L = p.L, w = p.w;
     float *sB = smem_s + (size_t)warp * p.rowlen;           // B[j] at sB[PAD + j]
     float *bsuf = sB + (L + 2 * STRIP_PAD) + (L + 32 * KS + 1);  // [ceil(L/32)]
@@ -84,7 +87,7 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
             b_idx = itm.n;
             float live = key_dist(ld_relaxed_u64(p.key + a_idx));
             live = __shfl_sync(0xffffffffu, live, 0);
-            if (itm.lb > live * (1.0f + p.eps_p)) {  // pruned by the live best-so-far
+            if (__any_sync(0xffffffffu, itm.lb > live * (1.0f + p.eps_p))) {  // pruned by the live best-so-far
                 ++my_skipped;
                 continue;
             }
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
                     float th = thr_batch;
                     if (p.mode == 0) th = key_dist(ld_relaxed_u64(p.key + a_idx)) * (1.0f + p.eps_t);
                     th = __shfl_sync(0xffffffffu, th, 0);  // one view of the live best per warp
-                    if (!(mv <= th)) {
+                    if (__any_sync(0xffffffffu, !(mv <= th))) {
                         cut_abandon = true;
                         break;
                     }
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
             ++strips_done;
             if (!last) {
                 const float rm = __shfl_sync(0xffffffffu, rowmin, 31);
-                if (!(rm <= thr)) {
+                if (__any_sync(0xffffffffu, !(rm <= thr))) {
                     abandoned = true;
                     break;
                 }
