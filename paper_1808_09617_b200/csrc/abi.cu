@@ -386,6 +386,11 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         // (the counters accumulate from the seed phase on: the call that finishes the survivor
         // round reports them once)
         if (do_compact) stats->survivors += (int64_t)h[CNT_N + 1];
+#ifdef NNDTW_PROFILE_SETUP
+        if (do_finish)
+            fprintf(stderr, "NNDTW_PROFILE_SETUP setup_cycles %llu warp_cycles %llu share %.4f\n",
+                    h[6], h[7], h[7] ? (double)h[6] / (double)h[7] : 0.0);
+#endif
         if (do_compact && level_stats) {
             stats->pruned_kim = (stats->pruned_kim < 0 ? 0 : stats->pruned_kim) + (int64_t)h[CNT_PRUNED_KIM];
             stats->pruned_bands = (stats->pruned_bands < 0 ? 0 : stats->pruned_bands) + (int64_t)h[CNT_PRUNED_BANDS];

@@ -142,7 +142,15 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
     bool skipping = false;
     long long my_skipped = 0;
     unsigned long long kstart = 0;
+#ifdef NNDTW_PROFILE_SETUP
+    // instrumentation build only (tools/setup_share.sh): cycles spent waiting for item setups
+    long long prof_setup = 0;
+    const long long prof_t0 = clock64();
+#endif
     auto setup = [&]() {
+#ifdef NNDTW_PROFILE_SETUP
+        const long long ps0 = clock64();
+#endif
         unsigned a_idx, b_idx;
         float ilb = 0.0f;
         if (p.mode == 0) {
@@ -187,6 +195,9 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
         }
         if (p.mode == 0) kstart = ld_relaxed_u64(p.key + a_idx);
         cp_async_wait_all();
+#ifdef NNDTW_PROFILE_SETUP
+        prof_setup += clock64() - ps0;  // (no __syncwarp here: setup runs in divergent code)
+#endif
         skipping = false;
         if (p.mode == 0) {
             // (all lanes of the group read the same address in one instruction)
@@ -369,6 +380,16 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
         }
         __syncwarp();
     }
+#ifdef NNDTW_PROFILE_SETUP
+    if (p.counters != nullptr) {  // per warp: setup cycles summed over its groups, warp cycles
+        unsigned long long ws = (valid_lane && g == 0) ? (unsigned long long)prof_setup : 0ull;
+        for (int off = 1; off < 32; off <<= 1) ws += __shfl_xor_sync(0xffffffffu, ws, off);
+        if (lane == 0) {
+            atomicAdd(p.counters + 6, ws);
+            atomicAdd(p.counters + 7, (unsigned long long)(clock64() - prof_t0));
+        }
+    }
+#endif
     if (p.counters != nullptr && valid_lane && g == 0 && my_skipped > 0)
         atomicAdd(p.counters + CNT_SKIPPED, (unsigned long long)my_skipped);
     if (p.counters != nullptr && valid_lane && g == 0 && my_items > 0) {
