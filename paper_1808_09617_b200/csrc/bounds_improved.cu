@@ -111,7 +111,9 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
     // per-pair chain of load -> scans -> gather is latency-bound otherwise)
     float na[IMP_CE], nl[IMP_CE], nu[IMP_CE], nb[IMP_CE];
     auto load_chunk0 = [&](int64_t pr) {
-        const int64_t qi = pr / nt, ni = pr - qi * nt;
+        // train-major pair order: a warp's consecutive pairs share the train series (its
+        // envelope and row stay in L1/L2 across queries; the queries are the small set)
+        const int64_t ni = pr / nq, qi = pr - ni * nq;
         const int j0 = lane * IMP_CE;
         load8<VEC>(q + qi * L, j0, L, na);
         load8<VEC>(Lo + ni * L, j0, L, nl);
@@ -120,7 +122,9 @@ __global__ void __launch_bounds__(256) k_lb_improved_pass(const float *__restric
     };
     if (pr0 < pe) load_chunk0(pr0);
     for (int64_t pr = pr0; pr < pe; ++pr) {
-        const int64_t qi = pr / nt, ni = pr - qi * nt;
+        // train-major pair order: a warp's consecutive pairs share the train series (its
+        // envelope and row stay in L1/L2 across queries; the queries are the small set)
+        const int64_t ni = pr / nq, qi = pr - ni * nq;
         const float *a = q + qi * L, *b = t + ni * L, *u = U + ni * L, *lo = Lo + ni * L;
         // ---- projection A' (and the row of B) into shared memory ---------------------------
         {
