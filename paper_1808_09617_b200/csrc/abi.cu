@@ -109,6 +109,9 @@ struct ClassifyWs {
     unsigned long long log_cap;
     long long *cells_prefix;
     float *qU, *qL;  // query envelopes (symmetric bound)
+    // two-stage S2 (lb_sparse.cu): per-train-series lists of the queries left after stage A
+    long long *col_count, *col_off, *col_fill;
+    unsigned long long *minkey2;  // argmin of the full cascade value (second seed)
     size_t bytes;
 };
 
@@ -148,6 +151,11 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
     W.cells_prefix = (long long *)take(sizeof(long long) * (size_t)(2 * L));
     W.qU = (float *)take(sizeof(float) * q1 * (size_t)L);  // symmetric bound: query envelopes
     W.qL = (float *)take(sizeof(float) * q1 * (size_t)L);
+    const size_t t1 = (size_t)(nt > 0 ? nt : 1);
+    W.col_count = (long long *)take(sizeof(long long) * t1);
+    W.col_off = (long long *)take(sizeof(long long) * (t1 + 1));
+    W.col_fill = (long long *)take(sizeof(long long) * t1);
+    W.minkey2 = (unsigned long long *)take(8 * q1);
     W.bytes = off;
     return W;
 }
@@ -264,6 +272,15 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     // cascade levels for the level counters: band level only where Algorithm 1's bands exist
     const int count_no_bands = (keogh || (alt && !(alt & NNDTW_CLASSIFY_BOUND_ENHANCED_IMPROVED)))
                                    ? 1 : 0;
+    // Two-stage S2 for the default cascade (lb_sparse.cu): stage A = LB_Kim + Algorithm 1's
+    // bands for all pairs, a seed round, stage B = the bridge only for the pairs the partial
+    // cascade kept, a second seed round.  NNDTW_S2_ONE_STAGE=1: the bridge for every pair.
+    static const bool one_stage_env = [] {
+        const char *e = getenv("NNDTW_S2_ONE_STAGE");
+        return e && e[0] == '1';
+    }();
+    const bool two_stage = !alt && !sym && !keogh && ((L / 2) < v ? (L / 2) : v) <= 16 &&
+                           !one_stage_env;
     TieLog log{W.log, W.log_count, W.log_cap, W.overflow};
     unsigned long long *cnt = stats ? W.counters : nullptr;
 
@@ -301,7 +318,37 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         launch_bound_finish(W.lb, W.ldlb, nq, nt, q, t, alt_none ? nullptr : W.qkim, tkim, L,
                             self_offset, W.minkey, st);
     }
-    if (do_seed && !alt) {
+    if (do_seed && two_stage && nt > 0) {
+        // stage A: max(LB_Kim, boundary + bands) for all pairs + its argmin (first seed)
+        if (launch_lb(q, nq, W.qkim, t, U, Lo, tkim, nt, L, w, v, 1, self_offset, W.lb, W.ldlb,
+                      W.minkey, st, 0, 0, 1))
+            return fail(NNDTW_E_ARG, "too many train series for one launch");
+        // first seed round -> best-so-far bsf1 in key
+        launch_seed_items(W.minkey, seed2, nq, nt, W.seed_items, W.seed_count, st);
+        rc = dispatch_dtw(q, t, nq, nt, W.seed_items, W.seed_count, 2 * (unsigned long long)nq + 1,
+                          nullptr, nullptr, 0, L, w, 0, key, index_base, eps_t, log, nullptr,
+                          W.cells_prefix, nullptr, nullptr, st, sms);
+        if ((rc = dtw_fail(rc, L, w))) return rc;
+        // stage B: the pairs Algorithm 1's line-12 test keeps (P <= bsf1*(1+eps_p)), per train
+        // series, and the full cascade value for them (+ its argmin: the second seed)
+        launch_col_compact(W.lb, W.ldlb, nq, nt, key, eps_p, W.col_count, W.col_off, W.col_fill,
+                           (int32_t *)W.items, 3 * W.item_cap, sms, st);
+        cudaMemsetAsync(W.minkey2, 0xff, 8 * (size_t)nq, st);
+        if (launch_lb_sparse(q, W.qkim, nq, t, U, Lo, tkim, nt, L, w, v, W.col_off,
+                             (const int32_t *)W.items, W.lb, W.ldlb, W.minkey2, sms, st))
+            return fail(NNDTW_E_ARG, "sparse bridge launch failed");
+        // second seed round: the full-cascade argmin where it differs from the first seeds
+        launch_seed_items2(W.minkey2, W.minkey, seed2, nq, nt, W.seed_items,
+                           W.counters + CNT_SEED2, st);
+        rc = dispatch_dtw(q, t, nq, nt, W.seed_items, W.counters + CNT_SEED2,
+                          2 * (unsigned long long)nq + 1, nullptr, nullptr, 0, L, w, 0, key,
+                          index_base, eps_t, log, nullptr, W.cells_prefix, nullptr, nullptr, st,
+                          sms);
+        if ((rc = dtw_fail(rc, L, w))) return rc;
+        // the compaction and the level counters exclude the full-cascade argmin (and seed2)
+        cudaMemcpyAsync(W.minkey, W.minkey2, 8 * (size_t)nq, cudaMemcpyDeviceToDevice, st);
+    }
+    if (do_seed && !alt && !two_stage) {
         // S2: cascade bound for all pairs + per-query argmin-LB candidate
         if (nt > 0 && launch_lb(q, nq, W.qkim, t, U, Lo, tkim, nt, L, w, v, 1, self_offset,
                                 W.lb, W.ldlb, sym ? nullptr : W.minkey, st, keogh))
@@ -315,7 +362,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     }
     tm.mark();  // 3
     if ((rc = cuda_fail("lb"))) return rc;
-    if (nt > 0 && do_seed) {
+    if (nt > 0 && do_seed && !two_stage) {
         // S3: seed round (argmin-LB candidate, plus seed2 if given)
         launch_seed_items(W.minkey, seed2, nq, nt, W.seed_items, W.seed_count, st);
         rc = dispatch_dtw(q, t, nq, nt, W.seed_items, W.seed_count, 2 * (unsigned long long)nq + 1,
@@ -397,7 +444,8 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
             stats->pruned_keogh = (stats->pruned_keogh < 0 ? 0 : stats->pruned_keogh) + (int64_t)h[CNT_PRUNED_KEOGH];
         }
         if (do_finish) {
-            stats->dtw_calls += (int64_t)h[CNT_ITEMS] + (int64_t)h[CNT_N];  // main + seed items
+            stats->dtw_calls += (int64_t)h[CNT_ITEMS] + (int64_t)h[CNT_N] +
+                                (int64_t)h[CNT_SEED2];  // main + seed items (both rounds)
             stats->dtw_abandoned += (int64_t)h[CNT_ABANDONED];
             stats->cells += (int64_t)h[CNT_CELLS];
             stats->near_tie_pairs += (int64_t)h[CNT_TIES];

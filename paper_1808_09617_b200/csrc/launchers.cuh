@@ -11,7 +11,21 @@ int launch_check_finite(const float *x, int64_t n, int32_t *bad, cudaStream_t st
 int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
               const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L, int w,
               int v, int with_kim, int64_t self_offset, float *lb, int64_t ldlb,
-              unsigned long long *minkey, cudaStream_t st, int keogh = 0, int transposed = 0);
+              unsigned long long *minkey, cudaStream_t st, int keogh = 0, int transposed = 0,
+              int no_bridge = 0);
+// Two-stage S2 (lb_sparse.cu): after stage A (launch_lb with no_bridge) and the first seed
+// round, the LB_Keogh bridge only for the pairs the partial cascade did not prune.
+int launch_col_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
+                       const unsigned long long *key, float eps_p, long long *col_count,
+                       long long *col_off, long long *col_fill, int32_t *qlist,
+                       unsigned long long qlist_cap, int num_sms, cudaStream_t st);
+int launch_lb_sparse(const float *q, const nndtw_kim *qkim, int64_t nq, const float *t,
+                     const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L,
+                     int w, int v, const long long *col_off, const int32_t *qlist, float *lb,
+                     int64_t ldlb, unsigned long long *minkey2, int num_sms, cudaStream_t st);
+int launch_seed_items2(const unsigned long long *minkey2, const unsigned long long *minkey1,
+                       const int32_t *seed2, int64_t nq, int64_t nt, Item *items,
+                       unsigned long long *count, cudaStream_t st);
 // S3 prune counters per cascade level (stats; lb.cu k_lb_tile in level-count mode)
 int launch_lb_level_counts(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
                            const nndtw_kim *tkim, int64_t nt, int L, int w, int v, int with_kim,

@@ -51,6 +51,9 @@ struct LbParams {
     // of the cascade that already exceeds the threshold: Kim, the
     // boundary + band part of Algorithm 1 (its line-12 abort), or the full bound with the
     // LB_Keogh bridge.  level_cnt[0..2] += those counts.
+    // 1: no LB_Keogh bridge -- write max(LB_Kim, boundary + bands) (Algorithm 1 up to its
+    // line-12 abort test) and its per-query argmin key: stage A of the two-stage cascade
+    int no_bridge;
     const unsigned long long *count_key;
     const unsigned long long *seed_minkey;
     const int32_t *seed2;
@@ -110,7 +113,8 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
 
     // ---- column-chunk loader (register prefetch) ------------------------------------------
     const int ch_begin = nbb / LB_CC;
-    const int ch_end = p.count_key ? ch_begin : (L - nbb + LB_CC - 1) / LB_CC;  // exclusive
+    const int ch_end = (p.count_key || p.no_bridge) ? ch_begin
+                                                    : (L - nbb + LB_CC - 1) / LB_CC;  // exclusive
     float ra[4];
     float2 re[8];
     // load slot k of this thread: tile row (tid >> 4) + 16k, column c0 + (tid & 15) -- the same
@@ -357,10 +361,12 @@ static int launch_lb_params(LbParams &p, cudaStream_t st);
 int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
               const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L, int w,
               int v, int with_kim, int64_t self_offset, float *lb, int64_t ldlb,
-              unsigned long long *minkey, cudaStream_t st, int keogh, int transposed) {
+              unsigned long long *minkey, cudaStream_t st, int keogh, int transposed,
+              int no_bridge) {
     if (nq == 0 || nt == 0) return 0;
     if (w > L - 1) w = L - 1;
     LbParams p;
+    p.no_bridge = no_bridge;
     p.q = q;
     p.nq = nq;
     p.qkim = qkim;
@@ -401,6 +407,7 @@ int launch_lb_level_counts(const float *q, int64_t nq, const nndtw_kim *qkim, co
     if (nq == 0 || nt == 0) return 0;
     if (w > L - 1) w = L - 1;
     LbParams p;
+    p.no_bridge = 0;
     p.q = q;
     p.nq = nq;
     p.qkim = qkim;

@@ -1,0 +1,322 @@
+// lb_sparse.cu -- S2 in two stages, in the cascade order of the paper: LB_Kim, then
+// Algorithm 1's boundary terms and bands with the line-12 abort, then the LB_Keogh bridge
+// (lines 13-15) only for the pairs that survived.
+//
+//   stage A  k_lb_tile in no-bridge mode (lb.cu): P = max(LB_Kim, boundary + bands) for every
+//            pair, and the per-query argmin of P -> first seed; the seed's DTW (S3 seed round)
+//            gives a best-so-far bsf1 per query.
+//   stage B  k_col_compact: the pairs with P <= bsf1*(1+eps_p) (the others are pruned: Algorithm
+//            1 returns "infinity" at line 12) as per-train-series lists of queries;
+//            k_lb_sparse: one warp per train series computes the full cascade value
+//            max(LB_Kim, boundary + bands + bridge) for its listed queries, overwriting P, and
+//            the per-query argmin of the full value -> second seed (another S3 seed round).
+// Afterwards the bound matrix holds the full cascade value for every surviving pair and P
+// (> bsf1 >= the final best-so-far) for every pruned one, so S3's compaction keeps exactly the
+// pairs the one-stage path keeps.  On config 2 the partial cascade prunes ~91 % of the pairs
+// (numpy simulation of the seeds: 91.2 % with the partial-argmin seed, the second seed recovers
+// the full-argmin seed's best-so-far), so the O(L) bridge runs on ~9 % of them.
+//
+// B200 design.  Column lists: tiles of 32 queries x 1024 train series read the bound matrix
+// coalesced (float4), count per (tile, series) in registers and reserve with one atomic per
+// (tile, series) -- two passes (count, scatter) around a one-block scan.  Sparse bridge: the
+// warp stages its series' envelope (U, L) in shared memory with the band columns masked to
+// (+inf, -inf) (a zero term), then per listed query: lane l takes 4 consecutive columns per
+// 128 (float4 query loads from L2, where the 20 MB of queries stay), a - U, L - a, max with 0,
+// FFMA; lanes 0 .. 2nb-3 each compute one band minimum of Algorithm 1 (lines 4-10), lane 2nb-2
+// the boundary terms (line 1); one warp sum; lane 0 adds LB_Kim by max.
+#include "launchers.cuh"
+
+namespace nndtw {
+
+constexpr int CC_Q = 32;     // queries per column-compaction tile
+constexpr int CC_N = 1024;   // train series per tile (256 threads x 4)
+
+template <int PASS>
+__global__ void __launch_bounds__(256) k_col_compact(const float *__restrict__ lb, int64_t ldlb,
+                                                     int64_t nq, int64_t nt,
+                                                     const unsigned long long *__restrict__ key,
+                                                     float eps_p, long long *col_count,
+                                                     const long long *__restrict__ col_off,
+                                                     long long *col_fill, int32_t *qlist,
+                                                     unsigned long long qlist_cap) {
+    const int64_t ntq = (nq + CC_Q - 1) / CC_Q, ntn = (nt + CC_N - 1) / CC_N;
+    const bool vec = (ldlb & 3) == 0;
+    for (int64_t tile = blockIdx.x; tile < ntq * ntn; tile += gridDim.x) {
+        const int64_t q0 = (tile / ntn) * CC_Q;
+        const int64_t n0 = (tile % ntn) * CC_N + 4 * threadIdx.x;
+        unsigned live[4] = {0u, 0u, 0u, 0u};  // bit qq: query q0+qq keeps series n0+e
+#pragma unroll 4
+        for (int qq = 0; qq < CC_Q; ++qq) {
+            const int64_t q = q0 + qq;
+            if (q >= nq) break;
+            const float thr = key_dist(key[q]) * (1.0f + eps_p);
+            const float *row = lb + q * ldlb;
+            float v[4];
+            if (vec && n0 + 3 < nt) {
+                const float4 f = *reinterpret_cast<const float4 *>(row + n0);
+                v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) v[e] = n0 + e < nt ? row[n0 + e] : kInf;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e)  // (NaN -- the leave-one-out self pair -- is never kept)
+                live[e] |= (n0 + e < nt && v[e] <= thr) ? (1u << qq) : 0u;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int c = __popc(live[e]);
+            if (c == 0) continue;
+            const int64_t n = n0 + e;
+            if (PASS == 0) {
+                atomicAdd((unsigned long long *)(col_count + n), (unsigned long long)c);
+            } else {
+                long long pos = col_off[n] +
+                                (long long)atomicAdd((unsigned long long *)(col_fill + n),
+                                                     (unsigned long long)c);
+                unsigned m = live[e];
+                while (m) {
+                    const int qq = __ffs(m) - 1;
+                    m &= m - 1;
+                    if ((unsigned long long)pos < qlist_cap) qlist[pos] = (int32_t)(q0 + qq);
+                    ++pos;
+                }
+            }
+        }
+    }
+}
+
+// counts -> offsets (col_off[n] = sum of counts before n; col_off[nt] = total), fill = 0
+__global__ void __launch_bounds__(1024) k_col_scan(const long long *count, long long *off,
+                                                   long long *fill, int64_t nt) {
+    __shared__ long long part[1024];
+    const int64_t per = (nt + blockDim.x - 1) / blockDim.x;
+    const int64_t b = threadIdx.x * per, e = b + per < nt ? b + per : nt;
+    long long s = 0;
+    for (int64_t i = b; i < e; ++i) s += count[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long run = 0;
+        for (int i = 0; i < (int)blockDim.x; ++i) {
+            const long long v = part[i];
+            part[i] = run;
+            run += v;
+        }
+        off[nt] = run;
+    }
+    __syncthreads();
+    long long run = part[threadIdx.x];
+    for (int64_t i = b; i < e; ++i) {
+        off[i] = run;
+        run += count[i];
+        fill[i] = 0;
+    }
+}
+
+int launch_col_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
+                       const unsigned long long *key, float eps_p, long long *col_count,
+                       long long *col_off, long long *col_fill, int32_t *qlist,
+                       unsigned long long qlist_cap, int num_sms, cudaStream_t st) {
+    if (nq == 0 || nt == 0) return 0;
+    cudaMemsetAsync(col_count, 0, sizeof(long long) * (size_t)nt, st);
+    const int64_t ntiles = ((nq + CC_Q - 1) / CC_Q) * ((nt + CC_N - 1) / CC_N);
+    const int64_t grid = ntiles < (int64_t)num_sms * 8 ? ntiles : (int64_t)num_sms * 8;
+    k_col_compact<0><<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, eps_p, col_count,
+                                                     col_off, col_fill, qlist, qlist_cap);
+    k_col_scan<<<1, 1024, 0, st>>>(col_count, col_off, col_fill, nt);
+    k_col_compact<1><<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, eps_p, col_count,
+                                                     col_off, col_fill, qlist, qlist_cap);
+    count_launch(3, __func__);
+    return 0;
+}
+
+constexpr int SP_NBMAX = 16;  // bands per side held by lanes (2*nb - 1 <= 31 lanes)
+
+// NCH > 0: the query row is held in registers as NCH float4 per lane (L <= 128*NCH, L % 4 == 0)
+// and the NEXT listed query's row is loaded while this one is reduced (software pipeline: the
+// per-pair chain -- row from L2, terms, warp sum, LB_Kim -- is latency-bound otherwise);
+// NCH == 0: generic scalar path.
+// Batches of 32 listed queries: the warp computes each query's bridge (lanes over the columns,
+// one warp sum; NCH > 0: the row in registers as NCH float4 per lane, L <= 128*NCH, and the next
+// query's row loaded while this one is reduced), lane p keeps query p's bridge sum; then every
+// lane finishes its own query -- Algorithm 1's boundary terms and bands (lines 1-11) and LB_Kim
+// -- so that this O(V*w) tail runs once per 32 pairs of issue slots.  NCH == 0: scalar rows.
+template <int NCH>
+__global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
+                                                   const nndtw_kim *__restrict__ qkim,
+                                                   const float *__restrict__ t,
+                                                   const float *__restrict__ U,
+                                                   const float *__restrict__ Lo,
+                                                   const nndtw_kim *__restrict__ tkim,
+                                                   int64_t nt, int L, int w, int nb,
+                                                   const long long *__restrict__ col_off,
+                                                   const int32_t *__restrict__ qlist, float *lb,
+                                                   int64_t ldlb, unsigned long long *minkey2) {
+    extern __shared__ __align__(16) float sp_smem[];
+    const int lane = threadIdx.x & 31;
+    // warp index through a shuffle: provably warp-uniform loop control (plain SHFL reductions)
+    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);
+    const int Lp = (L + 127) / 128 * 128;
+    float *sU = sp_smem + (size_t)warp * (2 * Lp + 4 * SP_NBMAX);
+    float *sL = sU + Lp;
+    float *th = sL + Lp;              // t[0 .. nb)
+    float *tt = th + 2 * SP_NBMAX;    // t[L-1-i], i < nb
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    auto load_row = [&](int qi, float4 (&r)[NCH > 0 ? NCH : 1]) {
+#pragma unroll
+        for (int h = 0; h < NCH; ++h) {
+            const int c = 128 * h + 4 * lane;
+            r[h] = c < L ? __ldg(reinterpret_cast<const float4 *>(q + (int64_t)qi * L + c))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    for (int64_t n = gw; n < nt; n += nw) {
+        const long long beg = col_off[n], cnt = col_off[n + 1] - beg;
+        if (cnt == 0) continue;
+        // the series' envelope over the bridge columns [nb, L-nb); other columns (+inf, -inf)
+        const float *un = U + n * L, *ln = Lo + n * L, *tn = t + n * L;
+        for (int c = lane; c < Lp; c += 32) {
+            const bool br = c >= nb && c < L - nb;
+            sU[c] = br ? __ldg(un + c) : kInf;
+            sL[c] = br ? __ldg(ln + c) : -kInf;
+        }
+        if (lane < nb) {
+            th[lane] = __ldg(tn + lane);
+            tt[lane] = __ldg(tn + (L - 1 - lane));
+        }
+        const nndtw_kim kb = tkim[n];
+        const float t0 = __ldg(tn), tl = __ldg(tn + L - 1);
+        __syncwarp();
+        for (long long kb0 = 0; kb0 < cnt; kb0 += 32) {
+            const int nbatch = (int)(cnt - kb0 < 32 ? cnt - kb0 : 32);
+            const int myq = lane < nbatch ? qlist[beg + kb0 + lane] : 0;  // coalesced
+            float mybridge = 0.0f;
+            float4 an[NCH > 0 ? NCH : 1];
+            if (NCH > 0) load_row(__shfl_sync(0xffffffffu, myq, 0), an);
+            for (int pp = 0; pp < nbatch; ++pp) {
+                const int qi = __shfl_sync(0xffffffffu, myq, pp);
+                float4 ac[NCH > 0 ? NCH : 1];
+                if (NCH > 0) {
+#pragma unroll
+                    for (int h = 0; h < NCH; ++h) ac[h] = an[h];
+                    if (pp + 1 < nbatch) load_row(__shfl_sync(0xffffffffu, myq, pp + 1), an);
+                }
+                // LB_Keogh bridge (Algorithm 1 lines 13-15)
+                float acc = 0.0f;
+                if (NCH > 0) {
+#pragma unroll
+                    for (int h = 0; h < NCH; ++h) {
+                        const int c = 128 * h + 4 * lane;
+                        const float4 a4 = ac[h];
+                        const float4 u4 = *reinterpret_cast<const float4 *>(sU + c);  // +inf past L
+                        const float4 l4 = *reinterpret_cast<const float4 *>(sL + c);
+                        float d;
+                        d = fmaxf(fmaxf(a4.x - u4.x, l4.x - a4.x), 0.0f); acc = fmaf(d, d, acc);
+                        d = fmaxf(fmaxf(a4.y - u4.y, l4.y - a4.y), 0.0f); acc = fmaf(d, d, acc);
+                        d = fmaxf(fmaxf(a4.z - u4.z, l4.z - a4.z), 0.0f); acc = fmaf(d, d, acc);
+                        d = fmaxf(fmaxf(a4.w - u4.w, l4.w - a4.w), 0.0f); acc = fmaf(d, d, acc);
+                    }
+                } else {
+                    const float *a = q + (int64_t)qi * L;
+                    for (int c = lane; c < L; c += 32) {
+                        const float av = __ldg(a + c);
+                        const float d = fmaxf(fmaxf(av - sU[c], sL[c] - av), 0.0f);
+                        acc = fmaf(d, d, acc);
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                mybridge = lane == pp ? acc : mybridge;
+            }
+            // every lane finishes its own query: boundary terms + bands (Algorithm 1 lines 1-11,
+            // the band minimum over |differences| squared once, as the tile kernel), LB_Kim
+            if (lane < nbatch) {
+                const float *a = q + (int64_t)myq * L;
+                const float a0 = __ldg(a), al = __ldg(a + L - 1);
+                float bands = (a0 - th[0]) * (a0 - th[0]) + (al - tt[0]) * (al - tt[0]);
+                for (int side = 0; side < 2; ++side) {
+                    const float *bs = side ? tt : th;  // bs[x] = t[x] or t[L-1-x]
+                    for (int i = 1; i < nb; ++i) {
+                        const float ai = __ldg(a + (side ? L - 1 - i : i)), bi = bs[i];
+                        float m = fabsf(ai - bi);
+                        for (int jj = i - w > 0 ? i - w : 0; jj < i; ++jj)
+                            m = fminf(m, fminf(fabsf(ai - bs[jj]),
+                                               fabsf(__ldg(a + (side ? L - 1 - jj : jj)) - bi)));
+                        bands = __fadd_rn(bands, __fmul_rn(m, m));
+                    }
+                }
+                const float kim = kim_sum(a0, al, t0, tl, qkim[myq], kb, L);
+                const float full = fmaxf(kim, bands + mybridge);
+                lb[(int64_t)myq * ldlb + n] = full;
+                atomicMin(minkey2 + myq, make_key(full, (unsigned)n));
+            }
+            __syncwarp();
+        }
+        __syncwarp();  // the next series overwrites sU / sL
+    }
+}
+
+int launch_lb_sparse(const float *q, const nndtw_kim *qkim, int64_t nq, const float *t,
+                     const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L,
+                     int w, int v, const long long *col_off, const int32_t *qlist, float *lb,
+                     int64_t ldlb, unsigned long long *minkey2, int num_sms, cudaStream_t st) {
+    if (nq == 0 || nt == 0) return 0;
+    if (w > L - 1) w = L - 1;
+    const int nb = (L / 2) < v ? (L / 2) : v;
+    if (nb > SP_NBMAX) return -1;
+    const int Lp = (L + 127) / 128 * 128;
+    const size_t warp_bytes = (size_t)(2 * Lp + 4 * SP_NBMAX) * sizeof(float);
+    int warps = (int)((200 * 1024) / warp_bytes);
+    if (warps < 1) warps = 1;
+    if (warps > 8) warps = 8;
+    const size_t smem = warps * warp_bytes;
+    const bool vec = (L % 4) == 0 && ((uintptr_t)q % 16) == 0;
+    auto kern = k_lb_sparse<0>;
+    if (vec && L <= 128) kern = k_lb_sparse<1>;
+    else if (vec && L <= 256) kern = k_lb_sparse<2>;
+    else if (vec && L <= 512) kern = k_lb_sparse<4>;
+    else if (vec && L <= 1024) kern = k_lb_sparse<8>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // persistent warps, as many as fit (a latency-bound chain per pair: more warps in flight)
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * warps, smem);
+    if (occ < 1) occ = 1;
+    int64_t grid = (int64_t)num_sms * occ;
+    const int64_t need = (nt + warps - 1) / warps;
+    if (need < grid) grid = need;
+    kern<<<(unsigned)grid, 32 * warps, smem, st>>>(q, qkim, t, U, Lo, tkim, nt, L, w, nb,
+                                                   col_off, qlist, lb, ldlb, minkey2);
+    count_launch(1, __func__);
+    return 0;
+}
+
+// the second seed round's items: the argmin of the full cascade value, where it differs from the
+// first round's candidates (the partial-cascade argmin and the caller's extra seed)
+__global__ void k_seed_items2(const unsigned long long *minkey2, const unsigned long long *minkey1,
+                              const int32_t *seed2, int64_t nq, int64_t nt, Item *items,
+                              unsigned long long *count) {
+    const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= nq) return;
+    const unsigned long long k2 = minkey2[qi];
+    if (k2 == kNone) return;
+    const unsigned n2 = (unsigned)(k2 & 0xffffffffull);
+    const unsigned n1 = (unsigned)(minkey1[qi] & 0xffffffffull);
+    const unsigned s2 = seed2 ? (unsigned)seed2[qi] : 0xffffffffu;
+    if (n2 >= (unsigned)nt || n2 == n1 || n2 == s2) return;
+    const unsigned long long pos = atomicAdd(count, 1ull);
+    items[pos] = Item{(unsigned)qi, n2, 0.0f};
+}
+
+int launch_seed_items2(const unsigned long long *minkey2, const unsigned long long *minkey1,
+                       const int32_t *seed2, int64_t nq, int64_t nt, Item *items,
+                       unsigned long long *count, cudaStream_t st) {
+    if (nq == 0) return 0;
+    k_seed_items2<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(minkey2, minkey1, seed2, nq, nt,
+                                                                items, count);
+    count_launch(1, __func__);
+    return 0;
+}
+
+}  // namespace nndtw
