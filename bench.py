@@ -302,7 +302,8 @@ def main():
     labels_d = labels_h.to(dev)
     stream = torch.cuda.current_stream(dev)
 
-    acc = {"ms_lb": 0.0, "ms_dtw": 0.0, "cells": 0, "lb_pairs": 0, "dtw_calls": 0,
+    acc = {"ms_lb": 0.0, "ms_dtw": 0.0, "ms_lb_bridge": 0.0, "bridge_pairs": 0,
+           "cells": 0, "lb_pairs": 0, "dtw_calls": 0,
            "survivors": 0, "near_tie_pairs": 0, "dtw_abandoned": 0}
 
     env_ev = []
@@ -384,15 +385,18 @@ def main():
         dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
         ms, launches = float(tmax[0]), int(tsum[1])
         a = torch.tensor([acc["ms_dtw"], acc["ms_lb"], float(acc["cells"]),
-                          float(acc["lb_pairs"]), float(acc["dtw_calls"])],
+                          float(acc["lb_pairs"]), float(acc["dtw_calls"]), acc["ms_lb_bridge"],
+                          float(acc["bridge_pairs"])],
                          dtype=torch.float64, device=dev)
         dist.all_reduce(a, op=dist.ReduceOp.SUM)
         acc_tot = {"ms_dtw": float(a[0]), "ms_lb": float(a[1]), "cells": float(a[2]),
-                   "lb_pairs": float(a[3]), "dtw_calls": float(a[4])}
+                   "lb_pairs": float(a[3]), "dtw_calls": float(a[4]),
+                   "ms_lb_bridge": float(a[5]), "bridge_pairs": float(a[6])}
     else:
         acc_tot = dict(acc)
     acc_tot["ms_dtw"] = acc_tot["ms_dtw"] / world
     acc_tot["ms_lb"] = acc_tot["ms_lb"] / world
+    acc_tot["ms_lb_bridge"] = acc_tot["ms_lb_bridge"] / world
     value = Q * args.steps / (ms / 1e3)
 
     # ---- per-level prune counters (one untimed call; the level pass is not in the step) ----
@@ -468,7 +472,27 @@ def main():
                                f"tools/pipebench.cu) x {sm_mhz:.0f} MHz ({src})",
                 "ms_per_step": acc_tot["ms_dtw"] / args.steps}
     lb_bytes = (Q * L + (hi - lo) * (2 * L + 2 * min(L // 2, V)) + Q * (hi - lo)) * 4.0
-    roof_lb = {"kernel": "k_lb_tile (S2 cascade)", "bound": "alu", "achieved": lb_rate,
+    two_stage = acc_tot["ms_lb_bridge"] > 0 and acc_tot["bridge_pairs"] < acc_tot["lb_pairs"]
+    if two_stage:
+        # two-stage S2: stage A (Kim + bands, every pair) and the bridge for the pairs the
+        # partial cascade kept; the roofline figure is the bridge kernel's own pair-columns/s
+        br_rate = (acc_tot["bridge_pairs"] * lb_cols / (acc_tot["ms_lb_bridge"] * 1e-3) / 1e9
+                   / world)
+        roof_lb = {"kernel": "k_lb_sparse (S2 stage B: LB_Keogh bridge on the pairs LB_Kim + "
+                             "Algorithm 1's bands kept)", "bound": "alu",
+                   "achieved": br_rate, "peak": lb_peak, "unit": "G pair-columns/s",
+                   "frac": br_rate / lb_peak if lb_peak else None,
+                   "traffic": traffic.get("k_lb_sparse", {}).get("bytes_per_launch")
+                   if args.config == 2 else None,
+                   "bridge_pairs_per_step": acc_tot["bridge_pairs"] / args.steps,
+                   "bridge_fraction": acc_tot["bridge_pairs"] / max(acc_tot["lb_pairs"], 1),
+                   "peak_source": f"{num_sms} SMs x 42.7 pair-cols/clk (3 FMA-pipe ops each) x "
+                                  f"{sm_mhz:.0f} MHz ({src})",
+                   "ms_per_step": acc_tot["ms_lb_bridge"] / args.steps,
+                   "ms_s2_per_step": acc_tot["ms_lb"] / args.steps}
+    else:
+        roof_lb = None
+    roof_lb = roof_lb or {"kernel": "k_lb_tile (S2 cascade)", "bound": "alu", "achieved": lb_rate,
                "peak": lb_peak, "unit": "G pair-columns/s",
                "frac": lb_rate / lb_peak if lb_peak else None,
                "traffic": traffic.get("k_lb_tile", {}).get("bytes_per_launch")

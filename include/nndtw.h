@@ -69,6 +69,10 @@ typedef struct {
      * Filled only under NNDTW_CLASSIFY_LEVEL_STATS (an extra bands-only pass over the pairs,
      * timed in ms_other); -1 otherwise. */
     int64_t pruned_kim, pruned_bands, pruned_keogh;
+    /* Two-stage S2 (the default cascade): pairs whose LB_Keogh bridge was computed, i.e. kept by
+     * LB_Kim and Algorithm 1's bands against the first seed's best-so-far (line-12 test);
+     * lb_pairs for the one-stage bounds. */
+    int64_t bridge_pairs;
     int64_t dtw_calls;      /* DTW work items started (seeds + survivors) */
     int64_t dtw_abandoned;  /* survivor items stopped by early abandoning */
     int64_t cells;          /* in-band DP cells on the diagonals the survivor round processed */
@@ -77,9 +81,12 @@ typedef struct {
     int32_t launches;       /* kernel launches issued by the call */
     /* CUDA-event stage times on the call's stream: ms_envelopes = the query-side S1 work (Kim
      * features, and the queries' envelopes for the symmetric bound; the train envelopes are
-     * built before the call), ms_lb = the LB cascade kernel(s), ms_dtw = the
-     * survivor-round DTW kernel, ms_other = everything else (seed round, compaction, S7). */
+     * built before the call), ms_lb = the LB cascade kernel(s) (two-stage S2: stage A,
+     * the first seed round, the bridge lists and kernel, the second seed round), ms_dtw = the
+     * survivor-round DTW kernel, ms_other = everything else (compaction, S7). */
     float ms_envelopes, ms_lb, ms_dtw, ms_other;
+    /* the part of ms_lb spent in the sparse bridge kernel (two-stage S2; 0 otherwise) */
+    float ms_lb_bridge;
 } nndtw_stats;
 
 /* Library identity and introspection. */

@@ -274,13 +274,18 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
                                    ? 1 : 0;
     // Two-stage S2 for the default cascade (lb_sparse.cu): stage A = LB_Kim + Algorithm 1's
     // bands for all pairs, a seed round, stage B = the bridge only for the pairs the partial
-    // cascade kept, a second seed round.  NNDTW_S2_ONE_STAGE=1: the bridge for every pair.
-    static const bool one_stage_env = [] {
-        const char *e = getenv("NNDTW_S2_ONE_STAGE");
-        return e && e[0] == '1';
-    }();
-    const bool two_stage = !alt && !sym && !keogh && ((L / 2) < v ? (L / 2) : v) <= 16 &&
-                           !one_stage_env;
+    // cascade kept, a second seed round.
+    // Used where it pays: enough bridge work (nq*nt*(L - 2nb) >= 2^33 pair-columns, ~0.7 ms
+    // of the one-stage tile kernel) to cover its extra seed round and lists, and rows that fit
+    // the sparse kernel's register path (L <= 1024).  NNDTW_S2_STAGES=1 / =2 forces one / two
+    // stages (tests, experiments; read per call).
+    const int nb_ = (L / 2) < v ? (L / 2) : v;
+    bool two_stage = !alt && !sym && !keogh && nb_ <= 16 && L <= 1024 &&
+                     (double)nq * (double)nt * (double)(L - 2 * nb_) >= 8589934592.0;
+    if (const char *e = getenv("NNDTW_S2_STAGES")) {
+        if (e[0] == '1') two_stage = false;
+        if (e[0] == '2') two_stage = !alt && !sym && !keogh && nb_ <= 16;
+    }
     TieLog log{W.log, W.log_count, W.log_cap, W.overflow};
     unsigned long long *cnt = stats ? W.counters : nullptr;
 
@@ -318,6 +323,8 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         launch_bound_finish(W.lb, W.ldlb, nq, nt, q, t, alt_none ? nullptr : W.qkim, tkim, L,
                             self_offset, W.minkey, st);
     }
+    StageTimer bridge_tm(stats != nullptr && outer_tm == nullptr && two_stage, st);
+    long long bridge_pairs_h = 0;
     if (do_seed && two_stage && nt > 0) {
         // stage A: max(LB_Kim, boundary + bands) for all pairs + its argmin (first seed)
         if (launch_lb(q, nq, W.qkim, t, U, Lo, tkim, nt, L, w, v, 1, self_offset, W.lb, W.ldlb,
@@ -334,9 +341,15 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         launch_col_compact(W.lb, W.ldlb, nq, nt, key, eps_p, W.col_count, W.col_off, W.col_fill,
                            (int32_t *)W.items, 3 * W.item_cap, sms, st);
         cudaMemsetAsync(W.minkey2, 0xff, 8 * (size_t)nq, st);
+        if (bridge_tm.on) cudaEventRecord(bridge_tm.ev[0], st);
         if (launch_lb_sparse(q, W.qkim, nq, t, U, Lo, tkim, nt, L, w, v, W.col_off,
                              (const int32_t *)W.items, W.lb, W.ldlb, W.minkey2, sms, st))
             return fail(NNDTW_E_ARG, "sparse bridge launch failed");
+        if (bridge_tm.on) {
+            cudaEventRecord(bridge_tm.ev[1], st);
+            bridge_tm.n = 2;
+        }
+        if (stats) cudaMemcpyAsync(&bridge_pairs_h, W.col_off + nt, 8, cudaMemcpyDeviceToHost, st);
         // second seed round: the full-cascade argmin where it differs from the first seeds
         launch_seed_items2(W.minkey2, W.minkey, seed2, nq, nt, W.seed_items,
                            W.counters + CNT_SEED2, st);
@@ -433,6 +446,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         // (the counters accumulate from the seed phase on: the call that finishes the survivor
         // round reports them once)
         if (do_compact) stats->survivors += (int64_t)h[CNT_N + 1];
+        if (do_seed) stats->bridge_pairs += two_stage ? (int64_t)bridge_pairs_h : nq * nt;
 #ifdef NNDTW_PROFILE_SETUP
         if (do_finish)
             fprintf(stderr, "NNDTW_PROFILE_SETUP setup_cycles %llu warp_cycles %llu share %.4f\n",
@@ -457,6 +471,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
             stats->ms_lb += tm.ms(2, 3);
             stats->ms_dtw += tm.ms(4, 5);
             stats->ms_other += tm.ms(0, 1) + tm.ms(3, 4) + tm.ms(5, 6);
+            stats->ms_lb_bridge += bridge_tm.ms(0, 1);
         }
     }
     return NNDTW_OK;

@@ -133,6 +133,11 @@ int launch_col_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
 
 constexpr int SP_NBMAX = 16;  // bands per side held by lanes (2*nb - 1 <= 31 lanes)
 
+__host__ __device__ inline int sparse_row_len(int L, int nch) {
+    const int lp = (L + 127) / 128 * 128;
+    return nch > 0 && 128 * nch > lp ? 128 * nch : lp;
+}
+
 // NCH > 0: the query row is held in registers as NCH float4 per lane (L <= 128*NCH, L % 4 == 0)
 // and the NEXT listed query's row is loaded while this one is reduced (software pipeline: the
 // per-pair chain -- row from L2, terms, warp sum, LB_Kim -- is latency-bound otherwise);
@@ -157,7 +162,9 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
     const int lane = threadIdx.x & 31;
     // warp index through a shuffle: provably warp-uniform loop control (plain SHFL reductions)
     const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);
-    const int Lp = (L + 127) / 128 * 128;
+    // envelope rows padded to whole 128-column chunks -- NCH of them on the register path,
+    // which reads every chunk (columns past L hold the (+inf, -inf) identity)
+    const int Lp = sparse_row_len(L, NCH);
     float *sU = sp_smem + (size_t)warp * (2 * Lp + 4 * SP_NBMAX);
     float *sL = sU + Lp;
     float *th = sL + Lp;              // t[0 .. nb)
@@ -189,46 +196,72 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
         const nndtw_kim kb = tkim[n];
         const float t0 = __ldg(tn), tl = __ldg(tn + L - 1);
         __syncwarp();
+        // the envelope in registers as well (pipelined path): no shared-memory loads per pair
+        float4 ur[NCH > 0 ? NCH : 1], lr[NCH > 0 ? NCH : 1];
+        if (NCH > 0) {
+#pragma unroll
+            for (int h = 0; h < NCH; ++h) {
+                ur[h] = *reinterpret_cast<const float4 *>(sU + 128 * h + 4 * lane);
+                lr[h] = *reinterpret_cast<const float4 *>(sL + 128 * h + 4 * lane);
+            }
+        }
         for (long long kb0 = 0; kb0 < cnt; kb0 += 32) {
             const int nbatch = (int)(cnt - kb0 < 32 ? cnt - kb0 : 32);
             const int myq = lane < nbatch ? qlist[beg + kb0 + lane] : 0;  // coalesced
             float mybridge = 0.0f;
-            float4 an[NCH > 0 ? NCH : 1];
-            if (NCH > 0) load_row(__shfl_sync(0xffffffffu, myq, 0), an);
-            for (int pp = 0; pp < nbatch; ++pp) {
-                const int qi = __shfl_sync(0xffffffffu, myq, pp);
-                float4 ac[NCH > 0 ? NCH : 1];
-                if (NCH > 0) {
+            if (NCH > 0) {
+                // per-lane partial bridge sums of the batch's 32 queries, one transposing warp
+                // reduction at the end (31 shuffles for 32 sums instead of 5 per sum)
+                float part[32];
+                float4 an[NCH > 0 ? NCH : 1];
+                load_row(__shfl_sync(0xffffffffu, myq, 0), an);
 #pragma unroll
-                    for (int h = 0; h < NCH; ++h) ac[h] = an[h];
-                    if (pp + 1 < nbatch) load_row(__shfl_sync(0xffffffffu, myq, pp + 1), an);
-                }
-                // LB_Keogh bridge (Algorithm 1 lines 13-15)
-                float acc = 0.0f;
-                if (NCH > 0) {
+                for (int pp = 0; pp < 32; ++pp) {
+                    float acc = 0.0f;
+                    if (pp < nbatch) {
+                        float4 ac[NCH > 0 ? NCH : 1];
 #pragma unroll
-                    for (int h = 0; h < NCH; ++h) {
-                        const int c = 128 * h + 4 * lane;
-                        const float4 a4 = ac[h];
-                        const float4 u4 = *reinterpret_cast<const float4 *>(sU + c);  // +inf past L
-                        const float4 l4 = *reinterpret_cast<const float4 *>(sL + c);
-                        float d;
-                        d = fmaxf(fmaxf(a4.x - u4.x, l4.x - a4.x), 0.0f); acc = fmaf(d, d, acc);
-                        d = fmaxf(fmaxf(a4.y - u4.y, l4.y - a4.y), 0.0f); acc = fmaf(d, d, acc);
-                        d = fmaxf(fmaxf(a4.z - u4.z, l4.z - a4.z), 0.0f); acc = fmaf(d, d, acc);
-                        d = fmaxf(fmaxf(a4.w - u4.w, l4.w - a4.w), 0.0f); acc = fmaf(d, d, acc);
+                        for (int h = 0; h < NCH; ++h) ac[h] = an[h];
+                        if (pp + 1 < nbatch) load_row(__shfl_sync(0xffffffffu, myq, pp + 1), an);
+#pragma unroll
+                        for (int h = 0; h < NCH; ++h) {
+                            const float4 a4 = ac[h], u4 = ur[h], l4 = lr[h];
+                            float d;
+                            d = fmaxf(fmaxf(a4.x - u4.x, l4.x - a4.x), 0.0f); acc = fmaf(d, d, acc);
+                            d = fmaxf(fmaxf(a4.y - u4.y, l4.y - a4.y), 0.0f); acc = fmaf(d, d, acc);
+                            d = fmaxf(fmaxf(a4.z - u4.z, l4.z - a4.z), 0.0f); acc = fmaf(d, d, acc);
+                            d = fmaxf(fmaxf(a4.w - u4.w, l4.w - a4.w), 0.0f); acc = fmaf(d, d, acc);
+                        }
                     }
-                } else {
+                    part[pp] = acc;
+                }
+                // transposing reduction: afterwards lane p holds the sum over lanes of part[p]
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const bool up = (lane & o) != 0;
+#pragma unroll
+                    for (int i = 0; i < o; ++i) {
+                        const float send = up ? part[i] : part[i + o];
+                        const float keep = up ? part[i + o] : part[i];
+                        part[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                    }
+                }
+                mybridge = part[0];
+            } else {
+                for (int pp = 0; pp < nbatch; ++pp) {
+                    const int qi = __shfl_sync(0xffffffffu, myq, pp);
                     const float *a = q + (int64_t)qi * L;
+                    float acc = 0.0f;
                     for (int c = lane; c < L; c += 32) {
                         const float av = __ldg(a + c);
                         const float d = fmaxf(fmaxf(av - sU[c], sL[c] - av), 0.0f);
                         acc = fmaf(d, d, acc);
                     }
-                }
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-                mybridge = lane == pp ? acc : mybridge;
+                    for (int off = 16; off > 0; off >>= 1)
+                        acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                    mybridge = lane == pp ? acc : mybridge;
+                }
             }
             // every lane finishes its own query: boundary terms + bands (Algorithm 1 lines 1-11,
             // the band minimum over |differences| squared once, as the tile kernel), LB_Kim
@@ -266,18 +299,19 @@ int launch_lb_sparse(const float *q, const nndtw_kim *qkim, int64_t nq, const fl
     if (w > L - 1) w = L - 1;
     const int nb = (L / 2) < v ? (L / 2) : v;
     if (nb > SP_NBMAX) return -1;
-    const int Lp = (L + 127) / 128 * 128;
+    const bool vec_ = (L % 4) == 0 && ((uintptr_t)q % 16) == 0;
+    const int nch = !vec_ ? 0 : L <= 128 ? 1 : L <= 256 ? 2 : L <= 512 ? 4 : L <= 1024 ? 8 : 0;
+    const int Lp = sparse_row_len(L, nch);
     const size_t warp_bytes = (size_t)(2 * Lp + 4 * SP_NBMAX) * sizeof(float);
     int warps = (int)((200 * 1024) / warp_bytes);
     if (warps < 1) warps = 1;
     if (warps > 8) warps = 8;
     const size_t smem = warps * warp_bytes;
-    const bool vec = (L % 4) == 0 && ((uintptr_t)q % 16) == 0;
     auto kern = k_lb_sparse<0>;
-    if (vec && L <= 128) kern = k_lb_sparse<1>;
-    else if (vec && L <= 256) kern = k_lb_sparse<2>;
-    else if (vec && L <= 512) kern = k_lb_sparse<4>;
-    else if (vec && L <= 1024) kern = k_lb_sparse<8>;
+    if (nch == 1) kern = k_lb_sparse<1>;
+    else if (nch == 2) kern = k_lb_sparse<2>;
+    else if (nch == 4) kern = k_lb_sparse<4>;
+    else if (nch == 8) kern = k_lb_sparse<8>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // persistent warps, as many as fit (a latency-bound chain per pair: more warps in flight)
     int occ = 0;

@@ -47,11 +47,12 @@ class NNDTWError(RuntimeError):
 
 class Stats(C.Structure):
     _fields_ = [("lb_pairs", C.c_int64), ("survivors", C.c_int64), ("pruned_kim", C.c_int64),
-                ("pruned_bands", C.c_int64), ("pruned_keogh", C.c_int64), ("dtw_calls", C.c_int64),
+                ("pruned_bands", C.c_int64), ("pruned_keogh", C.c_int64),
+                ("bridge_pairs", C.c_int64), ("dtw_calls", C.c_int64),
                 ("dtw_abandoned", C.c_int64), ("cells", C.c_int64),
                 ("near_tie_pairs", C.c_int64), ("rounds", C.c_int32), ("launches", C.c_int32),
                 ("ms_envelopes", C.c_float), ("ms_lb", C.c_float), ("ms_dtw", C.c_float),
-                ("ms_other", C.c_float)]
+                ("ms_other", C.c_float), ("ms_lb_bridge", C.c_float)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -134,11 +134,14 @@ def _classify_raw(dev, Tr, trl, Q, w, V, flags, ws_fill, self_offset=-1):
     return key.t.cpu().numpy().copy(), stats.as_dict()
 
 
+@pytest.mark.parametrize("stages", ["1", "2"])
 @pytest.mark.parametrize("flags", [1, 1 | 128, 1 | 2, 1 | 4, 1 | 256, 1 | 512, 1 | 1024, 1 | 2048])
-def test_classify_workspace_guards_and_poisoning(dev, flags):
+def test_classify_workspace_guards_and_poisoning(dev, monkeypatch, flags, stages):
     """All classify variants (EXACT with level counters, the Keogh / symmetric / LB_Improved /
-    LB_New / enhanced+improved / no bound S2): workspace and key guard zones intact, and the
-    same keys with the workspace poisoned with zeros, 0xFF bytes and random bytes."""
+    LB_New / enhanced+improved / no bound S2; the default cascade in one and in two stages):
+    workspace and key guard zones intact, and the same keys with the workspace poisoned with
+    zeros, 0xFF bytes and random bytes."""
+    monkeypatch.setenv("NNDTW_S2_STAGES", stages)
     ds = datagen.make_dataset(1, n_train=300, n_test=70)
     w = datagen.window_from_percent(20, 256)
     keys = [_classify_raw(dev, ds.train, ds.train_labels, ds.test, w, 5, flags, f)[0]
