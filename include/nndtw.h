@@ -247,7 +247,9 @@ NNDTW_API int nndtw_dtw_batch(const float *a, const float *b, const int32_t *ia,
 #define NNDTW_CLASSIFY_PHASE_SEARCH_A 32u
 #define NNDTW_CLASSIFY_PHASE_SEARCH_B 64u
 /* flags & NNDTW_CLASSIFY_LEVEL_STATS (with non-NULL stats): fill the per-level prune counters
- * pruned_kim / pruned_bands / pruned_keogh (one extra bands-only pass, no bridge). */
+ * pruned_kim / pruned_bands / pruned_keogh (one extra bands-only pass, no bridge).  In a
+ * phased (sharded) classify, set it on the SEED call as well: with the two-stage S2 the seed
+ * phase then also stores the full cascade values the counters read. */
 #define NNDTW_CLASSIFY_LEVEL_STATS 128u
 /* Alternative S2 bounds (the paper's NN-DTW time per bound,
  * Fig. 9-11).  At most one of them, not with BOUND_KEOGH / BOUND_SYMMETRIC; the

@@ -111,6 +111,8 @@ struct ClassifyWs {
     float *qU, *qL;  // query envelopes (symmetric bound)
     // two-stage S2 (lb_sparse.cu): per-train-series lists of the queries left after stage A
     long long *col_count, *col_off, *col_fill;
+    int32_t *blist;  // the listed queries, train-series-major (col_off)
+    float *bval;     // their full cascade values (S3 compacts from these lists)
     unsigned long long *minkey2;  // argmin of the full cascade value (second seed)
     size_t bytes;
 };
@@ -156,6 +158,8 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
     W.col_off = (long long *)take(sizeof(long long) * (t1 + 1));
     W.col_fill = (long long *)take(sizeof(long long) * t1);
     W.minkey2 = (unsigned long long *)take(8 * q1);
+    W.blist = (int32_t *)take(sizeof(int32_t) * (size_t)W.item_cap);
+    W.bval = (float *)take(sizeof(float) * (size_t)W.item_cap);
     W.bytes = off;
     return W;
 }
@@ -278,7 +282,8 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     // Used where it pays: enough bridge work (nq*nt*(L - 2nb) >= 2^33 pair-columns, ~0.7 ms
     // of the one-stage tile kernel) to cover its extra seed round and lists, and rows that fit
     // the sparse kernel's register path (L <= 1024).  NNDTW_S2_STAGES=1 / =2 forces one / two
-    // stages (tests, experiments; read per call).
+    // stages (tests, experiments; read per call -- keep it fixed across the phases of one
+    // sharded classify: the search phase compacts from the seed phase's lists).
     const int nb_ = (L / 2) < v ? (L / 2) : v;
     bool two_stage = !alt && !sym && !keogh && nb_ <= 16 && L <= 1024 &&
                      (double)nq * (double)nt * (double)(L - 2 * nb_) >= 8589934592.0;
@@ -323,6 +328,9 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         launch_bound_finish(W.lb, W.ldlb, nq, nt, q, t, alt_none ? nullptr : W.qkim, tkim, L,
                             self_offset, W.minkey, st);
     }
+    // (level counters read the full cascade values from the bound matrix: with them on, the
+    // two-stage S2 writes those there too -- pass the flag to the seed phase as well)
+    const bool level_stats = stats != nullptr && (flags & NNDTW_CLASSIFY_LEVEL_STATS) != 0;
     StageTimer bridge_tm(stats != nullptr && outer_tm == nullptr && two_stage, st);
     long long bridge_pairs_h = 0;
     if (do_seed && two_stage && nt > 0) {
@@ -339,11 +347,12 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         // stage B: the pairs Algorithm 1's line-12 test keeps (P <= bsf1*(1+eps_p)), per train
         // series, and the full cascade value for them (+ its argmin: the second seed)
         launch_col_compact(W.lb, W.ldlb, nq, nt, key, eps_p, W.col_count, W.col_off, W.col_fill,
-                           (int32_t *)W.items, 3 * W.item_cap, sms, st);
+                           W.blist, W.item_cap, sms, st);
         cudaMemsetAsync(W.minkey2, 0xff, 8 * (size_t)nq, st);
         if (bridge_tm.on) cudaEventRecord(bridge_tm.ev[0], st);
         if (launch_lb_sparse(q, W.qkim, nq, t, U, Lo, tkim, nt, L, w, v, W.col_off,
-                             (const int32_t *)W.items, W.lb, W.ldlb, W.minkey2, sms, st))
+                             W.blist, W.bval, level_stats ? W.lb : nullptr, W.ldlb, W.minkey2,
+                             sms, st))
             return fail(NNDTW_E_ARG, "sparse bridge launch failed");
         if (bridge_tm.on) {
             cudaEventRecord(bridge_tm.ev[1], st);
@@ -383,14 +392,17 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
                           W.cells_prefix, nullptr, nullptr, st, sms);
         if ((rc = dtw_fail(rc, L, w))) return rc;
     }
-    const bool level_stats = stats != nullptr && (flags & NNDTW_CLASSIFY_LEVEL_STATS) != 0;
     if (nt > 0 && do_compact && level_stats) {
         // stats: pairs pruned per cascade level against the same threshold as the compaction
         launch_lb_level_counts(q, nq, W.qkim, t, tkim, nt, L, w, v, alt_none ? 0 : 1,
                                count_no_bands, self_offset, W.lb, W.ldlb, key, W.minkey, seed2,
                                eps_p, W.counters + CNT_PRUNED_KIM, st);
     }
-    if (nt > 0 && do_compact) {
+    if (nt > 0 && do_compact && two_stage) {
+        // S3 from the two-stage lists (every possible survivor is listed, with its full value)
+        launch_list_compact(W.col_off, W.blist, W.bval, nt, key, W.minkey, seed2, eps_p, W.items,
+                            W.main_count, W.buckets, W.item_cap, sms, st);
+    } else if (nt > 0 && do_compact) {
         // S3: prune + compact the survivors against the seeded best-so-far
         launch_compact(W.lb, W.ldlb, nq, nt, key, W.minkey, seed2, eps_p, W.items,
                        W.main_count, W.buckets, W.item_cap, sms, st);

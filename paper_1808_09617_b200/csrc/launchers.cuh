@@ -21,8 +21,9 @@ int launch_col_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
                        unsigned long long qlist_cap, int num_sms, cudaStream_t st);
 int launch_lb_sparse(const float *q, const nndtw_kim *qkim, int64_t nq, const float *t,
                      const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L,
-                     int w, int v, const long long *col_off, const int32_t *qlist, float *lb,
-                     int64_t ldlb, unsigned long long *minkey2, int num_sms, cudaStream_t st);
+                     int w, int v, const long long *col_off, const int32_t *qlist, float *bval,
+                     float *lb, int64_t ldlb, unsigned long long *minkey2, int num_sms,
+                     cudaStream_t st);
 int launch_seed_items2(const unsigned long long *minkey2, const unsigned long long *minkey1,
                        const int32_t *seed2, int64_t nq, int64_t nt, Item *items,
                        unsigned long long *count, cudaStream_t st);
@@ -59,6 +60,11 @@ int launch_classify_init(int64_t nq, unsigned long long *key, unsigned long long
                          int ncounters, unsigned long long *bucket_count, cudaStream_t st);
 int launch_seed_items(const unsigned long long *minkey, const int32_t *seed2, int64_t nq,
                       int64_t nt, Item *items, unsigned long long *count, cudaStream_t st);
+int launch_list_compact(const long long *col_off, const int32_t *blist, const float *bval,
+                        int64_t nt, const unsigned long long *key,
+                        const unsigned long long *minkey, const int32_t *seed2, float eps_p,
+                        Item *items, unsigned long long *count, unsigned long long *buckets,
+                        unsigned long long capacity, int num_sms, cudaStream_t st);
 int launch_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
                    const unsigned long long *key, const unsigned long long *minkey,
                    const int32_t *seed2, float eps_p, Item *items, unsigned long long *count,

@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
                                                    const nndtw_kim *__restrict__ tkim,
                                                    int64_t nt, int L, int w, int nb,
                                                    const long long *__restrict__ col_off,
-                                                   const int32_t *__restrict__ qlist, float *lb,
+                                                   const int32_t *__restrict__ qlist,
+                                                   float *__restrict__ bval, float *lb,
                                                    int64_t ldlb, unsigned long long *minkey2) {
     extern __shared__ __align__(16) float sp_smem[];
     const int lane = threadIdx.x & 31;
@@ -282,7 +283,8 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
                 }
                 const float kim = kim_sum(a0, al, t0, tl, qkim[myq], kb, L);
                 const float full = fmaxf(kim, bands + mybridge);
-                lb[(int64_t)myq * ldlb + n] = full;
+                bval[beg + kb0 + lane] = full;  // next to its list entry (coalesced)
+                if (lb) lb[(int64_t)myq * ldlb + n] = full;  // level counters only
                 atomicMin(minkey2 + myq, make_key(full, (unsigned)n));
             }
             __syncwarp();
@@ -293,8 +295,9 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
 
 int launch_lb_sparse(const float *q, const nndtw_kim *qkim, int64_t nq, const float *t,
                      const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L,
-                     int w, int v, const long long *col_off, const int32_t *qlist, float *lb,
-                     int64_t ldlb, unsigned long long *minkey2, int num_sms, cudaStream_t st) {
+                     int w, int v, const long long *col_off, const int32_t *qlist, float *bval,
+                     float *lb, int64_t ldlb, unsigned long long *minkey2, int num_sms,
+                     cudaStream_t st) {
     if (nq == 0 || nt == 0) return 0;
     if (w > L - 1) w = L - 1;
     const int nb = (L / 2) < v ? (L / 2) : v;
@@ -321,7 +324,7 @@ int launch_lb_sparse(const float *q, const nndtw_kim *qkim, int64_t nq, const fl
     const int64_t need = (nt + warps - 1) / warps;
     if (need < grid) grid = need;
     kern<<<(unsigned)grid, 32 * warps, smem, st>>>(q, qkim, t, U, Lo, tkim, nt, L, w, nb,
-                                                   col_off, qlist, lb, ldlb, minkey2);
+                                                   col_off, qlist, bval, lb, ldlb, minkey2);
     count_launch(1, __func__);
     return 0;
 }

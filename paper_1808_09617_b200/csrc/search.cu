@@ -213,6 +213,97 @@ int launch_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
     return 0;
 }
 
+// ---- S3 compaction from the two-stage S2's lists (lb_sparse.cu) --------------------------------
+// After the two-stage S2 every pair that can survive is on a per-train-series list (its partial
+// cascade value passed bsf1*(1+eps_p) >= the final threshold) with its full cascade value next to
+// it, so the survivors are compacted from the lists instead of from the whole bound matrix: the
+// same test (value <= thr, not a seed), the same LB buckets.  A tile = LC_W train series, one
+// warp per series, lanes over the series' entries (coalesced list reads); PASS 1 runs the tile
+// twice -- count, reserve a run per bucket (one global atomic per bucket and tile), scatter --
+// so no per-thread slot storage is needed for lists of any length.  Inside a bucket the items are
+// train-major (a query's candidates of one bucket are spread over the round).
+constexpr int LC_W = 8;
+
+template <int PASS>
+__global__ void __launch_bounds__(32 * LC_W) k_list_compact(
+    const long long *__restrict__ col_off, const int32_t *__restrict__ blist,
+    const float *__restrict__ bval, int64_t nt, const unsigned long long *__restrict__ key,
+    const unsigned long long *__restrict__ minkey, const int32_t *__restrict__ seed2, float eps_p,
+    Item *__restrict__ items, unsigned long long *bucket_count,
+    const unsigned long long *bucket_base, unsigned long long *bucket_fill,
+    unsigned long long capacity, int one_bucket) {
+    __shared__ unsigned hist[NBUCKET];
+    __shared__ unsigned long long base[NBUCKET];
+    const int lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);
+    const int64_t ntiles = (nt + LC_W - 1) / LC_W;
+    // the bucket of a kept entry, or -1
+    auto classify = [&](int64_t n, long long e) -> int {
+        const int32_t q = blist[e];
+        const float v = bval[e];
+        const float thr = key_dist(key[q]) * (1.0f + eps_p);
+        const unsigned s1 = (unsigned)(minkey[q] & 0xffffffffull);
+        const unsigned s2 = seed2 ? (unsigned)seed2[q] : 0xffffffffu;
+        if (!(v <= thr) || (unsigned)n == s1 || (unsigned)n == s2) return -1;
+        const float scale = (thr > 0.0f && !one_bucket) ? (float)NBUCKET / thr : 0.0f;
+        const int b = (int)(v * scale);
+        return b < 0 ? 0 : (b >= NBUCKET ? NBUCKET - 1 : b);
+    };
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (threadIdx.x < NBUCKET) hist[threadIdx.x] = 0u;
+        __syncthreads();
+        const int64_t n = tile * LC_W + warp;
+        const long long beg = n < nt ? col_off[n] : 0, end = n < nt ? col_off[n + 1] : 0;
+        for (long long e = beg + lane; e < end; e += 32) {
+            const int b = classify(n, e);
+            if (b >= 0) atomicAdd(&hist[b], 1u);
+        }
+        __syncthreads();
+        if (PASS == 0) {
+            if (threadIdx.x < NBUCKET && hist[threadIdx.x])
+                atomicAdd(bucket_count + threadIdx.x, (unsigned long long)hist[threadIdx.x]);
+        } else {
+            if (threadIdx.x < NBUCKET) {
+                const unsigned c = hist[threadIdx.x];
+                base[threadIdx.x] = c ? bucket_base[threadIdx.x] +
+                                            atomicAdd(bucket_fill + threadIdx.x, (unsigned long long)c)
+                                      : 0ull;
+                hist[threadIdx.x] = 0u;
+            }
+            __syncthreads();
+            for (long long e = beg + lane; e < end; e += 32) {
+                const int b = classify(n, e);
+                if (b < 0) continue;
+                const unsigned long long pos = base[b] + atomicAdd(&hist[b], 1u);
+                if (pos < capacity) items[pos] = Item{(unsigned)blist[e], (unsigned)n, bval[e]};
+            }
+        }
+        __syncthreads();  // hist / base are reused by the next tile
+    }
+}
+
+int launch_list_compact(const long long *col_off, const int32_t *blist, const float *bval,
+                        int64_t nt, const unsigned long long *key,
+                        const unsigned long long *minkey, const int32_t *seed2, float eps_p,
+                        Item *items, unsigned long long *count, unsigned long long *buckets,
+                        unsigned long long capacity, int num_sms, cudaStream_t st) {
+    if (nt == 0) return 0;
+    unsigned long long *bcount = buckets, *bbase = buckets + NBUCKET, *bfill = buckets + 2 * NBUCKET;
+    const int64_t ntiles = (nt + LC_W - 1) / LC_W;
+    const int64_t grid = ntiles < (int64_t)num_sms * 8 ? ntiles : (int64_t)num_sms * 8;
+    static const char *ob = getenv("NNDTW_ONE_BUCKET");
+    const int one = ob && ob[0] == '1';
+    k_list_compact<0><<<(unsigned)grid, 32 * LC_W, 0, st>>>(col_off, blist, bval, nt, key, minkey,
+                                                            seed2, eps_p, items, bcount, bbase,
+                                                            bfill, capacity, one);
+    k_bucket_scan<<<1, 32, 0, st>>>(bcount, bbase, bfill, count);
+    k_list_compact<1><<<(unsigned)grid, 32 * LC_W, 0, st>>>(col_off, blist, bval, nt, key, minkey,
+                                                            seed2, eps_p, items, bcount, bbase,
+                                                            bfill, capacity, one);
+    count_launch(3, __func__);
+    return 0;
+}
+
 // ---- in-band cells per anti-diagonal, prefix-summed (GCUPS bookkeeping) ----------------------
 __global__ void k_cells_prefix(int L, int w, long long *prefix) {
     __shared__ long long tot[1024];

@@ -133,12 +133,14 @@ def nccl_world1(dev):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("stages", ["1", "2"])
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("c,p", [(0, 10), (1, 10), (1, 100)])
-def test_golden_classify_sharded_nccl(dev, nccl_world1, split, c, p):
+def test_golden_classify_sharded_nccl(dev, nccl_world1, monkeypatch, stages, split, c, p):
     """dist.classify_sharded -- the two-phase seed exchange, the int64 MIN all-reduces of the
     fp32 keys, the fp64 near-tie keys and the resolved indices -- over a real NCCL group (one
-    rank), on every query of configs 0 and 1, against the oracle."""
+    rank), on every query of configs 0 and 1, against the oracle; S2 in one and in two stages."""
+    monkeypatch.setenv("NNDTW_S2_STAGES", stages)
     from paper_1808_09617_b200 import nndtw
     from paper_1808_09617_b200.dist import classify_sharded
     g = golden(c)

@@ -4,7 +4,7 @@ racecheck, synccheck, initcheck -- one tool per run, SURVEY.md §5 "race detecti
   compute-sanitizer --tool racecheck --error-exitcode 99 python tools/sanitize_cases.py
 
 Covered: S1 envelopes (direct kernel for every residue class used, van Herk kernel), Kim
-stats, the S2 tile kernel (LB_Enhanced with/without Kim, LB_Keogh, symmetric, level counts, V
+stats, the S2 tile kernel and the two-stage S2 (column compaction, sparse bridge) (LB_Enhanced with/without Kim, LB_Keogh, symmetric, level counts, V
 above the shared-memory band limit), LB_Improved / LB_Enhanced+Improved / LB_New, the bound
 finish pass, every band-kernel layout class (aligned full-warp KM=2 with and without packing,
 aligned KM=1, general KM=0, R = 32), the strip kernel with KS = 1 / 2 / 4 (masked and full
@@ -46,6 +46,13 @@ def main():
         m = nndtw.Model(T(ds.train), T(ds.train_labels), w0, 5, bound=bound)
         case(f"classify bound={bound}", lambda m=m: nndtw.classify(m, T(ds.test[:24]), stats=True,
                                                                     level_stats=True))
+    # the two-stage S2 (stage A tile, column compaction + scan, sparse bridge, second seed)
+    os.environ["NNDTW_S2_STAGES"] = "2"
+    case("classify two-stage S2", lambda: nndtw.classify(model, T(ds.test[:40]), stats=True))
+    d1 = datagen.make_dataset(1, n_train=300, n_test=40)
+    m1 = nndtw.Model(T(d1.train), T(d1.train_labels), d1.cfg.windows()[0], 5)
+    case("classify two-stage S2 L=256", lambda: nndtw.classify(m1, T(d1.test)))
+    del os.environ["NNDTW_S2_STAGES"]
     ms = nndtw.Model(T(ds.train), T(ds.train_labels), w0, 5, symmetric=True)
     case("classify symmetric", lambda: nndtw.classify(ms, T(ds.test[:24])))
 
