@@ -128,6 +128,11 @@ __device__ __forceinline__ void cp_async_commit() {
 __device__ __forceinline__ void cp_async_wait_group1() {
     asm volatile("cp.async.wait_group 1;" ::: "memory");
 }
+// all but the N most recently committed groups of this thread's copies have landed
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // ---- LB_Kim, sum variant "without repetitions" (reading C7) -----------------------
 // features first, last, min, max in that order; a feature is dropped if its index in either

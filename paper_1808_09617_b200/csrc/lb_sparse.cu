@@ -132,21 +132,33 @@ int launch_col_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
 }
 
 constexpr int SP_NBMAX = 16;  // bands per side held by lanes (2*nb - 1 <= 31 lanes)
+constexpr int SP_D = 4;       // query-row ring depth (register path): D-1 rows in flight
 
 __host__ __device__ inline int sparse_row_len(int L, int nch) {
     const int lp = (L + 127) / 128 * 128;
     return nch > 0 && 128 * nch > lp ? 128 * nch : lp;
 }
 
-// NCH > 0: the query row is held in registers as NCH float4 per lane (L <= 128*NCH, L % 4 == 0)
-// and the NEXT listed query's row is loaded while this one is reduced (software pipeline: the
-// per-pair chain -- row from L2, terms, warp sum, LB_Kim -- is latency-bound otherwise);
-// NCH == 0: generic scalar path.
-// Batches of 32 listed queries: the warp computes each query's bridge (lanes over the columns,
-// one warp sum; NCH > 0: the row in registers as NCH float4 per lane, L <= 128*NCH, and the next
-// query's row loaded while this one is reduced), lane p keeps query p's bridge sum; then every
-// lane finishes its own query -- Algorithm 1's boundary terms and bands (lines 1-11) and LB_Kim
-// -- so that this O(V*w) tail runs once per 32 pairs of issue slots.  NCH == 0: scalar rows.
+// shared memory per warp (floats): NCH > 0 the query-row ring + the series' head / tail values,
+// NCH == 0 the masked envelope rows + head / tail
+__host__ __device__ inline int sparse_warp_floats(int L, int nch) {
+    const int Lp = sparse_row_len(L, nch);
+    // (NCH > 0: after a batch's bridge the ring holds the 32 queries' head / tail values)
+    const int ring = SP_D * Lp > 32 * (2 * SP_NBMAX + 1) ? SP_D * Lp : 32 * (2 * SP_NBMAX + 1);
+    return (nch > 0 ? ring : 2 * Lp) + 2 * SP_NBMAX;
+}
+
+// Batches of 32 listed queries: the warp computes each query's bridge (lanes over the columns),
+// lane p keeps query p's bridge sum; then every lane finishes its own query -- Algorithm 1's
+// boundary terms and bands (lines 1-11) and LB_Kim -- so that this O(V*w) tail runs once per 32
+// pairs of issue slots.
+// NCH > 0 (L <= 128*NCH, L % 4 == 0): the series' envelope over the bridge columns sits in
+// registers (NCH float4 of U and of L per lane, band columns masked to (+inf, -inf)); the listed
+// queries' rows stream through a per-warp shared-memory ring of SP_D rows by cp.async (16 B per
+// lane and chunk; a lane reads back only what it copied, so no warp barrier), SP_D-1 rows in
+// flight.  Groups of 8 queries: per-lane partial sums, one transposing warp reduction (10
+// shuffles for 8 sums).
+// NCH == 0: generic scalar path (envelope rows in shared memory, one warp sum per query).
 template <int NCH>
 __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
                                                    const nndtw_kim *__restrict__ qkim,
@@ -163,32 +175,46 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
     const int lane = threadIdx.x & 31;
     // warp index through a shuffle: provably warp-uniform loop control (plain SHFL reductions)
     const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);
-    // envelope rows padded to whole 128-column chunks -- NCH of them on the register path,
-    // which reads every chunk (columns past L hold the (+inf, -inf) identity)
     const int Lp = sparse_row_len(L, NCH);
-    float *sU = sp_smem + (size_t)warp * (2 * Lp + 4 * SP_NBMAX);
-    float *sL = sU + Lp;
-    float *th = sL + Lp;              // t[0 .. nb)
-    float *tt = th + 2 * SP_NBMAX;    // t[L-1-i], i < nb
+    float *wbase = sp_smem + (size_t)warp * sparse_warp_floats(L, NCH);
+    float *ring = wbase;                          // NCH > 0: SP_D query rows
+    float *sU = wbase, *sL = wbase + Lp;          // NCH == 0: masked envelope rows
+    float *th = wbase + sparse_warp_floats(L, NCH) - 2 * SP_NBMAX;  // t[0 .. nb)
+    float *tt = th + SP_NBMAX;                    // t[L-1-i], i < nb
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    auto load_row = [&](int qi, float4 (&r)[NCH > 0 ? NCH : 1]) {
-#pragma unroll
-        for (int h = 0; h < NCH; ++h) {
-            const int c = 128 * h + 4 * lane;
-            r[h] = c < L ? __ldg(reinterpret_cast<const float4 *>(q + (int64_t)qi * L + c))
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-    };
     for (int64_t n = gw; n < nt; n += nw) {
         const long long beg = col_off[n], cnt = col_off[n + 1] - beg;
         if (cnt == 0) continue;
-        // the series' envelope over the bridge columns [nb, L-nb); other columns (+inf, -inf)
         const float *un = U + n * L, *ln = Lo + n * L, *tn = t + n * L;
-        for (int c = lane; c < Lp; c += 32) {
-            const bool br = c >= nb && c < L - nb;
-            sU[c] = br ? __ldg(un + c) : kInf;
-            sL[c] = br ? __ldg(ln + c) : -kInf;
+        // the series' envelope over the bridge columns [nb, L-nb); other columns (+inf, -inf)
+        float4 ur[NCH > 0 ? NCH : 1], lr[NCH > 0 ? NCH : 1];
+        if (NCH > 0) {
+#pragma unroll
+            for (int h = 0; h < NCH; ++h) {
+                const int c = 128 * h + 4 * lane;
+                float4 u4 = make_float4(kInf, kInf, kInf, kInf);
+                float4 l4 = make_float4(-kInf, -kInf, -kInf, -kInf);
+                if (c < L) {
+                    u4 = __ldg(reinterpret_cast<const float4 *>(un + c));
+                    l4 = __ldg(reinterpret_cast<const float4 *>(ln + c));
+                }
+                float *uu = reinterpret_cast<float *>(&u4), *ll = reinterpret_cast<float *>(&l4);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const bool br = c + e >= nb && c + e < L - nb;
+                    uu[e] = br ? uu[e] : kInf;
+                    ll[e] = br ? ll[e] : -kInf;
+                }
+                ur[h] = u4;
+                lr[h] = l4;
+            }
+        } else {
+            for (int c = lane; c < Lp; c += 32) {
+                const bool br = c >= nb && c < L - nb;
+                sU[c] = br ? __ldg(un + c) : kInf;
+                sL[c] = br ? __ldg(ln + c) : -kInf;
+            }
         }
         if (lane < nb) {
             th[lane] = __ldg(tn + lane);
@@ -197,57 +223,74 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
         const nndtw_kim kb = tkim[n];
         const float t0 = __ldg(tn), tl = __ldg(tn + L - 1);
         __syncwarp();
-        // the envelope in registers as well (pipelined path): no shared-memory loads per pair
-        float4 ur[NCH > 0 ? NCH : 1], lr[NCH > 0 ? NCH : 1];
-        if (NCH > 0) {
-#pragma unroll
-            for (int h = 0; h < NCH; ++h) {
-                ur[h] = *reinterpret_cast<const float4 *>(sU + 128 * h + 4 * lane);
-                lr[h] = *reinterpret_cast<const float4 *>(sL + 128 * h + 4 * lane);
-            }
-        }
         for (long long kb0 = 0; kb0 < cnt; kb0 += 32) {
             const int nbatch = (int)(cnt - kb0 < 32 ? cnt - kb0 : 32);
             const int myq = lane < nbatch ? qlist[beg + kb0 + lane] : 0;  // coalesced
             float mybridge = 0.0f;
             if (NCH > 0) {
-                // per-lane partial bridge sums of the batch's 32 queries, one transposing warp
-                // reduction at the end (31 shuffles for 32 sums instead of 5 per sum)
-                float part[32];
-                float4 an[NCH > 0 ? NCH : 1];
-                load_row(__shfl_sync(0xffffffffu, myq, 0), an);
+                // query row pp of the batch -> ring slot pp % SP_D (this lane's 16-byte pieces)
+                static_assert(8 % SP_D == 0, "ring slots must repeat within a group of 8");
+                auto issue = [&](int pp, int slot) {
+                    const float *a = q + (int64_t)__shfl_sync(0xffffffffu, myq, pp) * L;
+                    float *dst = ring + slot * Lp;
 #pragma unroll
-                for (int pp = 0; pp < 32; ++pp) {
-                    float acc = 0.0f;
-                    if (pp < nbatch) {
-                        float4 ac[NCH > 0 ? NCH : 1];
+                    for (int h = 0; h < NCH; ++h) {
+                        const int c = 128 * h + 4 * lane;
+                        if (c < L) cp_async16(dst + c, a + c);
+                    }
+                };
 #pragma unroll
-                        for (int h = 0; h < NCH; ++h) ac[h] = an[h];
-                        if (pp + 1 < nbatch) load_row(__shfl_sync(0xffffffffu, myq, pp + 1), an);
+                for (int pp = 0; pp < SP_D - 1; ++pp) {
+                    if (pp < nbatch) issue(pp, pp);
+                    cp_async_commit();
+                }
+                // groups of 8 queries (a 32-way unrolled body overflowed the instruction cache)
+#pragma unroll 1
+                for (int g = 0; g < 4; ++g) {
+                    if (8 * g >= nbatch) break;
+                    float part[8];
 #pragma unroll
-                        for (int h = 0; h < NCH; ++h) {
-                            const float4 a4 = ac[h], u4 = ur[h], l4 = lr[h];
-                            float d;
-                            d = fmaxf(fmaxf(a4.x - u4.x, l4.x - a4.x), 0.0f); acc = fmaf(d, d, acc);
-                            d = fmaxf(fmaxf(a4.y - u4.y, l4.y - a4.y), 0.0f); acc = fmaf(d, d, acc);
-                            d = fmaxf(fmaxf(a4.z - u4.z, l4.z - a4.z), 0.0f); acc = fmaf(d, d, acc);
-                            d = fmaxf(fmaxf(a4.w - u4.w, l4.w - a4.w), 0.0f); acc = fmaf(d, d, acc);
+                    for (int i = 0; i < 8; ++i) {
+                        const int pp = 8 * g + i;
+                        if (pp + SP_D - 1 < nbatch) issue(pp + SP_D - 1, (i + SP_D - 1) % SP_D);
+                        cp_async_commit();
+                        cp_async_wait_group<SP_D - 1>();  // row pp has landed (this lane's part)
+                        float acc = 0.0f;
+                        if (pp < nbatch) {
+                            const float *src = ring + (i % SP_D) * Lp;
+#pragma unroll
+                            for (int h = 0; h < NCH; ++h) {
+                                const int c = 128 * h + 4 * lane;
+                                const float4 a4 = c < L
+                                                      ? *reinterpret_cast<const float4 *>(src + c)
+                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                                const float4 u4 = ur[h], l4 = lr[h];
+                                float d;
+                                d = fmaxf(fmaxf(a4.x - u4.x, l4.x - a4.x), 0.0f); acc = fmaf(d, d, acc);
+                                d = fmaxf(fmaxf(a4.y - u4.y, l4.y - a4.y), 0.0f); acc = fmaf(d, d, acc);
+                                d = fmaxf(fmaxf(a4.z - u4.z, l4.z - a4.z), 0.0f); acc = fmaf(d, d, acc);
+                                d = fmaxf(fmaxf(a4.w - u4.w, l4.w - a4.w), 0.0f); acc = fmaf(d, d, acc);
+                            }
+                        }
+                        part[i] = acc;
+                    }
+                    // transposing reduction over lane bits 4, 3, 2 (8 -> 1 value per lane), then
+                    // a butterfly over bits 1, 0: lanes 4i .. 4i+3 hold query 8g+i's bridge
+#pragma unroll
+                    for (int o = 16, nv = 4; o >= 4; o >>= 1, nv >>= 1) {
+                        const bool up = (lane & o) != 0;
+#pragma unroll
+                        for (int k = 0; k < nv; ++k) {
+                            const float send = up ? part[k] : part[k + nv];
+                            const float keep = up ? part[k + nv] : part[k];
+                            part[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                         }
                     }
-                    part[pp] = acc;
+                    part[0] += __shfl_xor_sync(0xffffffffu, part[0], 2);
+                    part[0] += __shfl_xor_sync(0xffffffffu, part[0], 1);
+                    const float r = __shfl_sync(0xffffffffu, part[0], 4 * (lane & 7));
+                    if ((lane >> 3) == g) mybridge = r;
                 }
-                // transposing reduction: afterwards lane p holds the sum over lanes of part[p]
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const bool up = (lane & o) != 0;
-#pragma unroll
-                    for (int i = 0; i < o; ++i) {
-                        const float send = up ? part[i] : part[i + o];
-                        const float keep = up ? part[i + o] : part[i];
-                        part[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-                    }
-                }
-                mybridge = part[0];
             } else {
                 for (int pp = 0; pp < nbatch; ++pp) {
                     const int qi = __shfl_sync(0xffffffffu, myq, pp);
@@ -265,19 +308,38 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
                 }
             }
             // every lane finishes its own query: boundary terms + bands (Algorithm 1 lines 1-11,
-            // the band minimum over |differences| squared once, as the tile kernel), LB_Kim
+            // the band minimum over |differences| squared once, as the tile kernel), LB_Kim.
+            // NCH > 0: the query's a[0 .. nb) and a[L-1-i], i < nb, are first copied into the
+            // (now free) ring in one round trip (hd[x] = a[x], hd[nb + x] = a[L-1-x]); read
+            // one by one from L2 they were a chain of dependent misses.
+            const float *hd = ring + lane * (2 * nb + 1);
+            if (NCH > 0) {
+                __syncwarp();  // every lane's ring reads of this batch are done
+                if (lane < nbatch) {
+                    const float *a = q + (int64_t)myq * L;
+                    float *hw = ring + lane * (2 * nb + 1);
+                    for (int x = 0; x < nb; ++x) {
+                        cp_async4(hw + x, a + x);
+                        cp_async4(hw + nb + x, a + (L - 1 - x));
+                    }
+                }
+                cp_async_commit();
+                cp_async_wait_group<0>();
+            }
             if (lane < nbatch) {
                 const float *a = q + (int64_t)myq * L;
-                const float a0 = __ldg(a), al = __ldg(a + L - 1);
+                auto qv = [&](int side, int x) {  // a[x] or a[L-1-x]
+                    return NCH > 0 ? hd[side * nb + x] : __ldg(a + (side ? L - 1 - x : x));
+                };
+                const float a0 = qv(0, 0), al = qv(1, 0);
                 float bands = (a0 - th[0]) * (a0 - th[0]) + (al - tt[0]) * (al - tt[0]);
                 for (int side = 0; side < 2; ++side) {
                     const float *bs = side ? tt : th;  // bs[x] = t[x] or t[L-1-x]
                     for (int i = 1; i < nb; ++i) {
-                        const float ai = __ldg(a + (side ? L - 1 - i : i)), bi = bs[i];
+                        const float ai = qv(side, i), bi = bs[i];
                         float m = fabsf(ai - bi);
                         for (int jj = i - w > 0 ? i - w : 0; jj < i; ++jj)
-                            m = fminf(m, fminf(fabsf(ai - bs[jj]),
-                                               fabsf(__ldg(a + (side ? L - 1 - jj : jj)) - bi)));
+                            m = fminf(m, fminf(fabsf(ai - bs[jj]), fabsf(qv(side, jj) - bi)));
                         bands = __fadd_rn(bands, __fmul_rn(m, m));
                     }
                 }
@@ -287,9 +349,9 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
                 if (lb) lb[(int64_t)myq * ldlb + n] = full;  // level counters only
                 atomicMin(minkey2 + myq, make_key(full, (unsigned)n));
             }
-            __syncwarp();
+            __syncwarp();  // the next batch's row copies overwrite hd
         }
-        __syncwarp();  // the next series overwrites sU / sL
+        __syncwarp();  // the next series overwrites th / tt (and, NCH == 0, sU / sL)
     }
 }
 
@@ -302,10 +364,11 @@ int launch_lb_sparse(const float *q, const nndtw_kim *qkim, int64_t nq, const fl
     if (w > L - 1) w = L - 1;
     const int nb = (L / 2) < v ? (L / 2) : v;
     if (nb > SP_NBMAX) return -1;
-    const bool vec_ = (L % 4) == 0 && ((uintptr_t)q % 16) == 0;
+    // the register path needs 16-byte rows: L % 4 == 0 and aligned q, U, L bases
+    const bool vec_ = (L % 4) == 0 && ((uintptr_t)q % 16) == 0 && ((uintptr_t)U % 16) == 0 &&
+                      ((uintptr_t)Lo % 16) == 0;
     const int nch = !vec_ ? 0 : L <= 128 ? 1 : L <= 256 ? 2 : L <= 512 ? 4 : L <= 1024 ? 8 : 0;
-    const int Lp = sparse_row_len(L, nch);
-    const size_t warp_bytes = (size_t)(2 * Lp + 4 * SP_NBMAX) * sizeof(float);
+    const size_t warp_bytes = (size_t)sparse_warp_floats(L, nch) * sizeof(float);
     int warps = (int)((200 * 1024) / warp_bytes);
     if (warps < 1) warps = 1;
     if (warps > 8) warps = 8;
@@ -316,7 +379,7 @@ int launch_lb_sparse(const float *q, const nndtw_kim *qkim, int64_t nq, const fl
     else if (nch == 4) kern = k_lb_sparse<4>;
     else if (nch == 8) kern = k_lb_sparse<8>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    // persistent warps, as many as fit (a latency-bound chain per pair: more warps in flight)
+    // persistent warps, as many as fit
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * warps, smem);
     if (occ < 1) occ = 1;
