@@ -285,11 +285,11 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     // stages (tests, experiments; read per call -- keep it fixed across the phases of one
     // sharded classify: the search phase compacts from the seed phase's lists).
     const int nb_ = (L / 2) < v ? (L / 2) : v;
-    bool two_stage = !alt && !sym && !keogh && nb_ <= 16 && L <= 1024 &&
+    bool two_stage = !alt && !sym && !keogh && nb_ >= 1 && nb_ <= 16 && L <= 1024 &&
                      (double)nq * (double)nt * (double)(L - 2 * nb_) >= 8589934592.0;
     if (const char *e = getenv("NNDTW_S2_STAGES")) {
         if (e[0] == '1') two_stage = false;
-        if (e[0] == '2') two_stage = !alt && !sym && !keogh && nb_ <= 16;
+        if (e[0] == '2') two_stage = !alt && !sym && !keogh && nb_ >= 1 && nb_ <= 16;
     }
     TieLog log{W.log, W.log_count, W.log_cap, W.overflow};
     unsigned long long *cnt = stats ? W.counters : nullptr;

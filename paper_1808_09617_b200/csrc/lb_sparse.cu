@@ -183,6 +183,10 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
     float *tt = th + SP_NBMAX;                    // t[L-1-i], i < nb
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    if (NCH > 0) {  // the ring's columns past L are never copied: finite from the start
+        for (int i = lane; i < sparse_warp_floats(L, NCH) - 2 * SP_NBMAX; i += 32) ring[i] = 0.0f;
+        __syncwarp();
+    }
     for (int64_t n = gw; n < nt; n += nw) {
         const long long beg = col_off[n], cnt = col_off[n + 1] - beg;
         if (cnt == 0) continue;
@@ -258,19 +262,35 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
                         float acc = 0.0f;
                         if (pp < nbatch) {
                             const float *src = ring + (i % SP_D) * Lp;
+                            // column pairs in f32x2: a - U and L - a as FADD2, the square-sum
+                            // as FFMA2 (two accumulators, added at the end)
+                            unsigned long long acc2 = 0ull;
 #pragma unroll
                             for (int h = 0; h < NCH; ++h) {
                                 const int c = 128 * h + 4 * lane;
-                                const float4 a4 = c < L
-                                                      ? *reinterpret_cast<const float4 *>(src + c)
-                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                                // (columns past L: stale ring data against (+inf, -inf): 0)
+                                const float4 a4 = *reinterpret_cast<const float4 *>(src + c);
                                 const float4 u4 = ur[h], l4 = lr[h];
-                                float d;
-                                d = fmaxf(fmaxf(a4.x - u4.x, l4.x - a4.x), 0.0f); acc = fmaf(d, d, acc);
-                                d = fmaxf(fmaxf(a4.y - u4.y, l4.y - a4.y), 0.0f); acc = fmaf(d, d, acc);
-                                d = fmaxf(fmaxf(a4.z - u4.z, l4.z - a4.z), 0.0f); acc = fmaf(d, d, acc);
-                                d = fmaxf(fmaxf(a4.w - u4.w, l4.w - a4.w), 0.0f); acc = fmaf(d, d, acc);
+#pragma unroll
+                                for (int hf = 0; hf < 2; ++hf) {
+                                    const unsigned long long av =
+                                        hf ? f2_pack(a4.z, a4.w) : f2_pack(a4.x, a4.y);
+                                    const unsigned long long uv =
+                                        hf ? f2_pack(u4.z, u4.w) : f2_pack(u4.x, u4.y);
+                                    const unsigned long long lv =
+                                        hf ? f2_pack(l4.z, l4.w) : f2_pack(l4.x, l4.y);
+                                    float p0, p1, m0, m1;
+                                    f2_unpack(f2_sub(av, uv), p0, p1);
+                                    f2_unpack(f2_sub(lv, av), m0, m1);
+                                    const float d0 = fmaxf(fmaxf(p0, m0), 0.0f);
+                                    const float d1 = fmaxf(fmaxf(p1, m1), 0.0f);
+                                    const unsigned long long dv = f2_pack(d0, d1);
+                                    acc2 = f2_fma(dv, dv, acc2);
+                                }
                             }
+                            float s0, s1;
+                            f2_unpack(acc2, s0, s1);
+                            acc = s0 + s1;
                         }
                         part[i] = acc;
                     }
@@ -315,16 +335,19 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
             const float *hd = ring + lane * (2 * nb + 1);
             if (NCH > 0) {
                 __syncwarp();  // every lane's ring reads of this batch are done
-                if (lane < nbatch) {
-                    const float *a = q + (int64_t)myq * L;
-                    float *hw = ring + lane * (2 * nb + 1);
-                    for (int x = 0; x < nb; ++x) {
-                        cp_async4(hw + x, a + x);
-                        cp_async4(hw + nb + x, a + (L - 1 - x));
-                    }
+                // per copy instruction 32 / (2nb) queries, 2nb lanes each (lane x < nb: a[x],
+                // else a[L-1-(x-nb)]): few rows per instruction, not 32 scattered ones
+                const int per = 32 / (2 * nb), k = lane / (2 * nb), x = lane % (2 * nb);
+                for (int p0 = 0; p0 < nbatch; p0 += per) {
+                    const int p = p0 + k;
+                    const int qi = __shfl_sync(0xffffffffu, myq, p & 31);
+                    if (k < per && p < nbatch)
+                        cp_async4(ring + p * (2 * nb + 1) + x,
+                                  q + (int64_t)qi * L + (x < nb ? x : L - 1 - (x - nb)));
                 }
                 cp_async_commit();
                 cp_async_wait_group<0>();
+                __syncwarp();  // hd rows were written by other lanes
             }
             if (lane < nbatch) {
                 const float *a = q + (int64_t)myq * L;
@@ -363,7 +386,7 @@ int launch_lb_sparse(const float *q, const nndtw_kim *qkim, int64_t nq, const fl
     if (nq == 0 || nt == 0) return 0;
     if (w > L - 1) w = L - 1;
     const int nb = (L / 2) < v ? (L / 2) : v;
-    if (nb > SP_NBMAX) return -1;
+    if (nb < 1 || nb > SP_NBMAX) return -1;  // (L = 1: the one-stage path)
     // the register path needs 16-byte rows: L % 4 == 0 and aligned q, U, L bases
     const bool vec_ = (L % 4) == 0 && ((uintptr_t)q % 16) == 0 && ((uintptr_t)U % 16) == 0 &&
                       ((uintptr_t)Lo % 16) == 0;
