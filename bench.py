@@ -32,6 +32,8 @@ import numpy as np  # noqa: E402
 import datagen  # noqa: E402
 
 METRIC = "NN-DTW queries/s (LB_Enhanced^V cascade) at 1/2/4/8 B200; DTW GCUPS"
+# L2 -> SM read rate for whole 2 KB rows at 16 warps/SM (tools/l2_roof.cu, measured on B200)
+L2_ROW_GBS = 18301.0
 
 
 def envelope_kernel(L: int, w: int) -> str:
@@ -490,6 +492,16 @@ def main():
                                   f"{sm_mhz:.0f} MHz ({src})",
                    "ms_per_step": acc_tot["ms_lb_bridge"] / args.steps,
                    "ms_s2_per_step": acc_tot["ms_lb"] / args.steps}
+        # the bridge streams every listed pair's query row (L floats) out of L2: its second
+        # roof is the L2 -> SM read rate for 2 KB rows (tools/l2_roof.cu on B200: 18.3 TB/s at
+        # 16 warps/SM, 20.3 TB/s at 32; profiles/round2d_l2_roof.txt)
+        if acc_tot["ms_lb_bridge"] > 0:
+            l2_gbs = (acc_tot["bridge_pairs"] * L * 4 / (acc_tot["ms_lb_bridge"] * 1e-3) / 1e9
+                      / world)
+            roof_lb["l2_rows"] = {"achieved": l2_gbs, "peak": L2_ROW_GBS, "unit": "GB/s",
+                                  "frac": l2_gbs / L2_ROW_GBS,
+                                  "peak_source": "tools/l2_roof.cu, 2 KB rows, 16 warps/SM "
+                                                 "(measured, B200)"}
     else:
         roof_lb = None
     roof_lb = roof_lb or {"kernel": "k_lb_tile (S2 cascade)", "bound": "alu", "achieved": lb_rate,

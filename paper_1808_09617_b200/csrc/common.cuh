@@ -138,15 +138,39 @@ __device__ __forceinline__ void cp_async_wait_group() {
 // features first, last, min, max in that order; a feature is dropped if its index in either
 // series is already used (first/last indices are 0 and L-1); ties -> lowest index (the
 // nndtw_kim features).  qf/ql, tf/tl = first/last values of the two series.
+// Branch-free form: per series the usable-feature flags (bit 0: the min index is interior,
+// bit 1: the max index is interior, bit 2: min and max share an index), then per pair
+//   okmin = both mins interior, okmax = both maxes interior and not (okmin and a shared index)
+// and the feature terms are added by select after an FFMA -- the same roundings in the same
+// order for every caller (tile kernel, sparse bridge, bound finish), so their values agree.
+struct KimF {
+    float vmin, vmax;
+    unsigned flags;
+};
+__device__ __forceinline__ KimF kim_f(const nndtw_kim &k, int L) {
+    KimF f;
+    f.vmin = k.vmin;
+    f.vmax = k.vmax;
+    f.flags = (k.imin != 0 && k.imin != L - 1 ? 1u : 0u) |
+              (k.imax != 0 && k.imax != L - 1 ? 2u : 0u) | (k.imax == k.imin ? 4u : 0u);
+    return f;
+}
+__device__ __forceinline__ float kim_sum_f(float qf, float ql, float tf, float tl, const KimF &a,
+                                           const KimF &b) {
+    const float dl = ql - tl, df = qf - tf;
+    float kim = fmaf(df, df, __fmul_rn(dl, dl));
+    const unsigned both = a.flags & b.flags, any = a.flags | b.flags;
+    const bool okmin = (both & 1u) != 0;
+    const bool okmax = (both & 2u) != 0 && !(okmin && (any & 4u) != 0);
+    const float dmn = a.vmin - b.vmin, dmx = a.vmax - b.vmax;
+    const float k1 = fmaf(dmn, dmn, kim);
+    kim = okmin ? k1 : kim;
+    const float k2 = fmaf(dmx, dmx, kim);
+    return okmax ? k2 : kim;
+}
 __device__ __forceinline__ float kim_sum(float qf, float ql, float tf, float tl,
                                          const nndtw_kim &ka, const nndtw_kim &kb, int L) {
-    float kim = (qf - tf) * (qf - tf) + (ql - tl) * (ql - tl);
-    const bool okmin = ka.imin != 0 && ka.imin != L - 1 && kb.imin != 0 && kb.imin != L - 1;
-    if (okmin) kim = kim + (ka.vmin - kb.vmin) * (ka.vmin - kb.vmin);
-    const bool okmax = ka.imax != 0 && ka.imax != L - 1 && kb.imax != 0 && kb.imax != L - 1 &&
-                       !(okmin && (ka.imax == ka.imin || kb.imax == kb.imin));
-    if (okmax) kim = kim + (ka.vmax - kb.vmax) * (ka.vmax - kb.vmax);
-    return kim;
+    return kim_sum_f(qf, ql, tf, tl, kim_f(ka, L), kim_f(kb, L));
 }
 
 // ---- work items ---------------------------------------------------------------------------

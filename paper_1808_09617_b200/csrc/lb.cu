@@ -64,10 +64,12 @@ struct LbParams {
 struct LbSmem {
     float a[2][LB_CC][LB_SA_STRIDE];
     float2 e[2][LB_CC][LB_SE_STRIDE];  // (U, L)
-    float qh[LB_TQ][2 * LB_NBMAX];   // [0,nb): head x[i]; [NBMAX, NBMAX+nb): tail x[L-1-i]
+    // query head / tail values transposed: qh[i][r] = x_r[i], qh[NBMAX + i][r] = x_r[L-1-i] --
+    // a warp's 8 queries are two broadcast LDS.128 into aligned register pairs (FADD2 operands)
+    float qh[2 * LB_NBMAX][LB_TQ];
     float th[LB_TN][2 * LB_NBMAX + 1];  // odd row stride: lane-indexed reads are conflict-free
-    nndtw_kim qk[LB_TQ];
-    nndtw_kim tk[LB_TN];
+    KimF qk[LB_TQ];
+    KimF tk[LB_TN];
 };
 
 template <bool SMEM_BANDS>
@@ -89,8 +91,8 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
             int r = e / nb, i = e % nb;
             int64_t qq = q0 + r;
             const float *src = p.q + (qq < p.nq ? qq : 0) * (int64_t)L;
-            S.qh[r][i] = src[i];
-            S.qh[r][LB_NBMAX + i] = src[L - 1 - i];
+            S.qh[i][r] = src[i];
+            S.qh[LB_NBMAX + i][r] = src[L - 1 - i];
         }
         for (int e = tid; e < LB_TN * nb; e += 256) {
             int r = e / nb, i = e % nb;
@@ -103,11 +105,11 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
     if (p.with_kim) {
         for (int e = tid; e < LB_TQ; e += 256) {
             int64_t qq = q0 + e;
-            S.qk[e] = p.qkim[qq < p.nq ? qq : 0];
+            S.qk[e] = kim_f(p.qkim[qq < p.nq ? qq : 0], L);
         }
         for (int e = tid; e < LB_TN; e += 256) {
             int64_t nn = n0 + e;
-            S.tk[e] = p.tkim[nn < p.nt ? nn : 0];
+            S.tk[e] = kim_f(p.tkim[nn < p.nt ? nn : 0], L);
         }
     }
 
@@ -163,12 +165,12 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
     // ---- boundary terms + bands (Alg. 1 lines 1-11) --------------------------------------
     float acc[LB_QPT][LB_NPT];
     auto qhv = [&](int qi, int i) -> float {   // head value x[i] of query tq*8+qi
-        if (SMEM_BANDS) return S.qh[tq * LB_QPT + qi][i];
+        if (SMEM_BANDS) return S.qh[i][tq * LB_QPT + qi];
         int64_t qq = q0 + tq * LB_QPT + qi;
         return __ldg(p.q + (qq < p.nq ? qq : 0) * (int64_t)L + i);
     };
     auto qtv = [&](int qi, int i) -> float {   // tail value x[L-1-i]
-        if (SMEM_BANDS) return S.qh[tq * LB_QPT + qi][LB_NBMAX + i];
+        if (SMEM_BANDS) return S.qh[LB_NBMAX + i][tq * LB_QPT + qi];
         int64_t qq = q0 + tq * LB_QPT + qi;
         return __ldg(p.q + (qq < p.nq ? qq : 0) * (int64_t)L + (L - 1 - i));
     };
@@ -188,35 +190,60 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
         for (int j = 0; j < LB_NPT; ++j)
             acc[qi][j] = p.keogh ? 0.0f : sq(qhv(qi, 0) - thv(j, 0)) + sq(qtv(qi, 0) - ttv(j, 0));
 
+    // 8 query values (side 0: x[i], side 1: x[L-1-i]) as four f32x2 pairs (queries 2k, 2k+1)
+    auto q8 = [&](int side, int i, unsigned long long (&v)[LB_QPT / 2]) {
+        if (SMEM_BANDS) {
+            const float *r = &S.qh[side * LB_NBMAX + i][tq * LB_QPT];
+            const float4 x0 = *reinterpret_cast<const float4 *>(r);
+            const float4 x1 = *reinterpret_cast<const float4 *>(r + 4);
+            v[0] = f2_pack(x0.x, x0.y); v[1] = f2_pack(x0.z, x0.w);
+            v[2] = f2_pack(x1.x, x1.y); v[3] = f2_pack(x1.z, x1.w);
+        } else {
+#pragma unroll
+            for (int k = 0; k < LB_QPT / 2; ++k)
+                v[k] = side ? f2_pack(qtv(2 * k, i), qtv(2 * k + 1, i))
+                            : f2_pack(qhv(2 * k, i), qhv(2 * k + 1, i));
+        }
+    };
     for (int i = 1; i < (p.keogh ? 0 : nb); ++i) {
         const int jlo = i - w > 0 ? i - w : 0;
 #pragma unroll
         for (int side = 0; side < 2; ++side) {
             float m[LB_QPT][LB_NPT];
-            float ai[LB_QPT], bi[LB_NPT];
-#pragma unroll
-            for (int qi = 0; qi < LB_QPT; ++qi) ai[qi] = side ? qtv(qi, i) : qhv(qi, i);
+            unsigned long long ai[LB_QPT / 2];
+            float bi[LB_NPT];
+            q8(side, i, ai);
 #pragma unroll
             for (int j = 0; j < LB_NPT; ++j) bi[j] = side ? ttv(j, i) : thv(j, i);
             // min over the band of (x-y)^2 = (min |x-y|)^2 exactly (rounding is monotone in
             // |x-y|): the band minimum runs on |differences| (FMNMX3 with |.| operands, ALU pipe)
-            // and squares once -- one FMA-pipe op per band cell instead of two
+            // and squares once; the differences of two queries against one train value are one
+            // FADD2 (bit-identical to two FADDs)
 #pragma unroll
-            for (int qi = 0; qi < LB_QPT; ++qi)
+            for (int qp = 0; qp < LB_QPT / 2; ++qp)
 #pragma unroll
-                for (int j = 0; j < LB_NPT; ++j) m[qi][j] = fabsf(ai[qi] - bi[j]);
+                for (int j = 0; j < LB_NPT; ++j) {
+                    float d0, d1;
+                    f2_unpack(f2_sub(ai[qp], f2_pack(bi[j], bi[j])), d0, d1);
+                    m[2 * qp][j] = fabsf(d0);
+                    m[2 * qp + 1][j] = fabsf(d1);
+                }
             for (int jj = jlo; jj < i; ++jj) {
-                float aj[LB_QPT], bj[LB_NPT];
-#pragma unroll
-                for (int qi = 0; qi < LB_QPT; ++qi) aj[qi] = side ? qtv(qi, jj) : qhv(qi, jj);
+                unsigned long long aj[LB_QPT / 2];
+                float bj[LB_NPT];
+                q8(side, jj, aj);
 #pragma unroll
                 for (int j = 0; j < LB_NPT; ++j) bj[j] = side ? ttv(j, jj) : thv(j, jj);
 #pragma unroll
-                for (int qi = 0; qi < LB_QPT; ++qi)
+                for (int qp = 0; qp < LB_QPT / 2; ++qp)
 #pragma unroll
-                    for (int j = 0; j < LB_NPT; ++j)
-                        m[qi][j] = fminf(m[qi][j],
-                                         fminf(fabsf(ai[qi] - bj[j]), fabsf(aj[qi] - bi[j])));
+                    for (int j = 0; j < LB_NPT; ++j) {
+                        float x0, x1, y0, y1;
+                        f2_unpack(f2_sub(ai[qp], f2_pack(bj[j], bj[j])), x0, x1);  // a_i - b_jj
+                        f2_unpack(f2_sub(aj[qp], f2_pack(bi[j], bi[j])), y0, y1);  // a_jj - b_i
+                        m[2 * qp][j] = fminf(m[2 * qp][j], fminf(fabsf(x0), fabsf(y0)));
+                        m[2 * qp + 1][j] = fminf(m[2 * qp + 1][j], fminf(fabsf(x1), fabsf(y1)));
+                    }
             }
 #pragma unroll
             for (int qi = 0; qi < LB_QPT; ++qi)
@@ -290,8 +317,8 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
                     (unsigned)nn == s1 || (unsigned)nn == s2)
                     continue;
                 const float full = p.lb[qq * p.ldlb + nn];
-                const float kim = p.with_kim ? kim_sum(qhv(qi, 0), qtv(qi, 0), thv(j, 0),
-                                                       ttv(j, 0), S.qk[rq], S.tk[rn], L)
+                const float kim = p.with_kim ? kim_sum_f(qhv(qi, 0), qtv(qi, 0), thv(j, 0),
+                                                         ttv(j, 0), S.qk[rq], S.tk[rn])
                                              : 0.0f;
                 if (kim > thr) c0 += 1;
                 else if (full > thr) {
@@ -326,8 +353,8 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
             const int64_t nn = n0 + rn;
             float v = acc[qi][j];
             if (p.with_kim)
-                v = fmaxf(v, kim_sum(qhv(qi, 0), qtv(qi, 0), thv(j, 0), ttv(j, 0), S.qk[rq],
-                                     S.tk[rn], L));
+                v = fmaxf(v, kim_sum_f(qhv(qi, 0), qtv(qi, 0), thv(j, 0), ttv(j, 0), S.qk[rq],
+                                       S.tk[rn]));
             if (p.transposed) {
                 if (qq < p.nq && nn < p.nt) {
                     float *dst = p.lb + nn * p.ldlb + qq;

@@ -42,10 +42,14 @@ def test_two_stage_golden_configs_0_1(dev, two_stage):
 @pytest.mark.parametrize("kind,L,w,V", [("int", 8, 2, 3), ("int", 16, 0, 5), ("int", 33, 32, 4),
                                         ("walk", 2, 0, 1), ("walk", 3, 1, 5), ("const", 12, 3, 2),
                                         ("walk", 130, 129, 16), ("int", 64, 5, 1),
-                                        ("walk", 300, 30, 5), ("walk", 1000, 100, 8)])
+                                        ("walk", 300, 30, 5), ("walk", 1000, 100, 8),
+                                        ("walk", 128, 40, 16), ("int", 36, 35, 16),
+                                        ("walk", 4, 3, 2), ("int", 24, 6, 12)])
 def test_two_stage_ties_and_shapes(dev, oracle_lib, two_stage, kind, L, w, V):
     """Exact ties (integer grids, duplicates before and after), constant series, every L mod 4
-    (the sparse kernel's register and scalar row paths), the V limits of the lane bands."""
+    (the sparse kernel's register and scalar row paths), the V limits of the lane bands and of
+    the head/tail copies (nb = 16: one query per copy instruction; the ring smaller than the
+    head/tail area at L <= 128)."""
     rng = np.random.default_rng(L * 37 + w)
     Tr = datagen.random_series(rng, 257, L, kind)
     Tr[200:210] = Tr[17]
