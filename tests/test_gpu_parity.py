@@ -248,7 +248,7 @@ def test_loocv_reduced(dev, oracle_lib):
 
 
 # ---------------------------------------------------------------- S4 long windows (strip kernel)
-# rows per lane RR (strip_rows_per_lane) and sub-blocks KS: 1024/2048/3001 -> RR 16, KS 4;
+# rows per lane RR (strip_rows_per_lane) and sub-blocks KS: 1024/2048/3001 -> RR 32, KS 4;
 # 700/1100 -> 12, 4; 513/600 -> 10, 2; 1792/256 -> 8, 4; each with and without the band mask
 @pytest.mark.parametrize("L,ws", [(1024, (1023, 600, 515)), (2048, (2047, 1500)),
                                   (700, (699, 520)), (1100, (1099,)), (513, (512,)),
