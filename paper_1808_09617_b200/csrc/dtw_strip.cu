@@ -449,6 +449,10 @@ int launch_dtw_strip(const float *A, const float *B, const Item *items,
     // sub-blocks per lane: the stagger costs 32*KS-1 ramp steps per strip of L + 32*KS - 1, so
     // short rows keep fewer sub-blocks (L = 256: KS = 4 would add 50 % steps); KS divides RR
     int ks = L >= 1024 ? 4 : (L >= 512 ? 2 : 1);
+    // search mode with 32-row lanes: most items are abandoned inside the first strip, where
+    // the 127 ramp steps of KS = 4 weigh more than the shorter chains cost (config 4: 6.60 ->
+    // 6.76 Tcells/s; raw full matrices prefer KS = 4: 8.07 vs 7.95)
+    if (mode == 0 && RR == 32 && ks == 4) ks = 2;
     if (RR % ks != 0) ks = 2;
     static const char *kse = getenv("NNDTW_STRIP_KS");  // experiments: force 1, 2 or 4
     if (kse && RR % atoi(kse) == 0) ks = atoi(kse);
