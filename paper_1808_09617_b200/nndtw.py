@@ -403,10 +403,10 @@ def classify(model: Model, q: torch.Tensor, stats: bool = False, check: bool = T
              level_stats: bool = False) -> Prediction:
     """Exact 1-NN of every query (single GPU / single shard, fp64-exact tie resolution).
 
-    The workspace holds the bound matrix and a worst-case survivor list (12 bytes per
-    (query, train) pair); when that exceeds `workspace_budget` (default 48 GB of the B200's
-    180 GB) the queries are processed in blocks -- queries are independent, the answer is
-    the same."""
+    The workspace holds the bound matrix, the two-stage S2's pair lists and a worst-case
+    survivor list (24 bytes per (query, train) pair: 4 + 8 + 12); when that exceeds
+    `workspace_budget` (default 48 GB of the B200's 180 GB) the queries are processed in
+    blocks -- queries are independent, the answer is the same."""
     if check and not check_finite(q, stream):
         raise NNDTWError("queries contain NaN or infinity")
     budget = WORKSPACE_BUDGET if workspace_budget is None else int(workspace_budget)
