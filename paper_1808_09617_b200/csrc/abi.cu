@@ -111,6 +111,8 @@ struct ClassifyWs {
     float *qU, *qL;  // query envelopes (symmetric bound)
     // two-stage S2 (lb_sparse.cu): per-train-series lists of the queries left after stage A
     long long *col_count, *col_off, *col_fill;
+    float *apad;     // the band kernel's padded query rows (survivor round, GA variant)
+    int64_t apad_cap;
     int32_t *blist;  // the listed queries, train-series-major (col_off)
     float *bval;     // their full cascade values (S3 compacts from these lists)
     unsigned long long *minkey2;  // argmin of the full cascade value (second seed)
@@ -158,6 +160,8 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
     W.col_off = (long long *)take(sizeof(long long) * (t1 + 1));
     W.col_fill = (long long *)take(sizeof(long long) * t1);
     W.minkey2 = (unsigned long long *)take(8 * q1);
+    W.apad_cap = (int64_t)q1 * band_apad_row_floats(L);
+    W.apad = (float *)take(sizeof(float) * (size_t)W.apad_cap);
     W.blist = (int32_t *)take(sizeof(int32_t) * (size_t)W.item_cap);
     W.bval = (float *)take(sizeof(float) * (size_t)W.item_cap);
     W.bytes = off;
@@ -412,7 +416,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         // S4/S5: DTW with early abandoning on the survivors
         rc = dispatch_dtw(q, t, nq, nt, W.items, W.main_count, W.item_cap, nullptr, nullptr, 0, L, w, 0,
                           key, index_base, eps_t, log, cnt, W.cells_prefix, nullptr, nullptr,
-                          st, sms);
+                          st, sms, W.apad, W.apad_cap);
         if ((rc = dtw_fail(rc, L, w))) return rc;
     } else if (nt > 0 && dtw_a) {
         // the survivors of buckets < split_b: items [0, base[split_b]) (the bucket-major list)
@@ -420,7 +424,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
                                                          : W.main_count;
         rc = dispatch_dtw(q, t, nq, nt, W.items, na, W.item_cap, nullptr, nullptr, 0, L, w, 0,
                           key, index_base, eps_t, log, cnt, W.cells_prefix, nullptr, nullptr,
-                          st, sms);
+                          st, sms, W.apad, W.apad_cap);
         if ((rc = dtw_fail(rc, L, w))) return rc;
     } else if (nt > 0 && dtw_b) {
         // the rest: items [base[split_b], total) -- the offset is read on the host
@@ -437,7 +441,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         if (nbrest > 0) {
             rc = dispatch_dtw(q, t, nq, nt, W.items + a, W.split_count, W.item_cap - a, nullptr,
                               nullptr, 0, L, w, 0, key, index_base, eps_t, log, cnt,
-                              W.cells_prefix, nullptr, nullptr, st, sms);
+                              W.cells_prefix, nullptr, nullptr, st, sms, W.apad, W.apad_cap);
             if ((rc = dtw_fail(rc, L, w))) return rc;
         }
     }

@@ -43,6 +43,9 @@ struct BandParams {
     const float *cutoff;                  // batch, nullable
     float *out;                           // batch
     int64_t dbg_na, dbg_nb;               // row counts of A and B (debug asserts)
+    const float *Apad;                    // GA variant: A rows with their pads, [na][seglen]
+    float *apad_ws;                       // search mode, nullable: room for Apad
+    int64_t apad_cap;                     // floats available at apad_ws
 };
 
 // An opaque copy: the compiler cannot rematerialise the value (it would otherwise recompute
@@ -66,7 +69,7 @@ constexpr int band_min_blocks() {
     return (R <= 24 || (R == 26 && KM >= 1)) ? 2 : 1;
 }
 
-template <int R, int KM, bool PACK>
+template <int R, int KM, bool PACK, bool GA = false>
 __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(BandParams p) {
     constexpr bool ALIGNED = KM >= 1;
     constexpr bool NOMASK = KM == 2;
@@ -83,8 +86,10 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
     const int64_t ngroups = (int64_t)gridDim.x * warps_per_block * gpw;
     const unsigned gbits = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
 
-    float *sA = smem_f + (size_t)(warp * gpw + (valid_lane ? gw : 0)) * 2 * p.seglen;
-    float *sB = sA + p.seglen;
+    // GA: the A (query) rows are read from a padded global copy through L1 and only B is
+    // staged -- half the shared memory per group, twice the resident warps
+    float *sA = smem_f + (size_t)(warp * gpw + (valid_lane ? gw : 0)) * (GA ? 1 : 2) * p.seglen;
+    float *sB = GA ? sA : sA + p.seglen;
 
     // index-dependent pads, written once (they never change)
     if (valid_lane) {
@@ -92,7 +97,7 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
             int idx = x - p.padl;
             if (idx < 0 || idx >= L) {
                 float v = idx < 0 ? 0x1p64f * (float)idx : 0x1p64f * (float)(idx - L + 1);
-                sA[x] = v;
+                if (!GA) sA[x] = v;
                 sB[x] = v;
             }
         }
@@ -175,12 +180,12 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
         if (p.vec4) {
 #pragma unroll 4
             for (int x = 4 * g; x < L; x += 4 * G) {
-                cp_async16(sA + p.padl + x, ga + x);
+                if (!GA) cp_async16(sA + p.padl + x, ga + x);
                 cp_async16(sB + p.padl + x, gb + x);
             }
         } else {
             for (int x = g; x < L; x += G) {
-                cp_async4(sA + p.padl + x, ga + x);
+                if (!GA) cp_async4(sA + p.padl + x, ga + x);
                 cp_async4(sB + p.padl + x, gb + x);
             }
         }
@@ -222,7 +227,7 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
         const int kp = p.k0 + per * R;
         const int I0 = (kp + w - g * R) >> 1;   // kp + w is even by construction
         const int J0 = (kp - w + g * R) >> 1;
-        const float *pa = sA + p.padl + I0 - (H - 1);
+        const float *pa = (GA ? p.Apad + (size_t)qcur * p.seglen : sA) + p.padl + I0 - (H - 1);
         const float *pb = sB + p.padl + J0;
         NNDTW_ASSERT(p.padl + I0 - (H - 1) >= 0 && p.padl + I0 + H - 1 < p.seglen &&
                          p.padl + J0 >= 0 && p.padl + J0 + R - 1 < p.seglen,
@@ -230,7 +235,7 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
                      J0, p.padl, p.seglen);
         float aw[R - 1];
 #pragma unroll
-        for (int x = 0; x < R - 1; ++x) aw[x] = pa[x];
+        for (int x = 0; x < R - 1; ++x) aw[x] = GA ? __ldg(pa + x) : pa[x];
         if (PACK) {
             // Half-packed cells: on an even diagonal t, cell m reads (a[t/2-m+H-1], b[t/2+m]);
             // on t+1 the same slot index m reads the same a and b one further.  One FADD2 with
@@ -511,11 +516,25 @@ static BandChoice choose_band_pass(int w, int L, bool all_widths) {
 
 bool band_supported(int w, int L) { return choose_band(w, L).R != 0; }
 
-template <int R, int KM, bool PACK>
+// A rows with the kernel's index-dependent pads (GA variant): out[r][x] = A[r][x - padl] inside,
+// the +-2^64 pad values outside
+__global__ void k_pad_rows(const float *__restrict__ A, int64_t na, int L, int padl, int seglen,
+                           float *__restrict__ out) {
+    const int64_t n = na * (int64_t)seglen;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / seglen;
+        const int x = (int)(e - r * seglen), idx = x - padl;
+        out[e] = (idx < 0) ? 0x1p64f * (float)idx
+                           : (idx >= L ? 0x1p64f * (float)(idx - L + 1) : A[r * L + idx]);
+    }
+}
+
+template <int R, int KM, bool PACK, bool GA = false>
 static int launch_band_t(BandParams &p, const BandChoice &c, cudaStream_t st, int num_sms) {
-    auto kern = k_dtw_band<R, KM, PACK>;
+    auto kern = k_dtw_band<R, KM, PACK, GA>;
     const int block = 32 * c.warps;
-    size_t smem = (size_t)c.warps * p.gpw * 2 * p.seglen * sizeof(float);
+    size_t smem = (size_t)c.warps * p.gpw * (GA ? 1 : 2) * p.seglen * sizeof(float);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem);
@@ -566,6 +585,25 @@ int launch_dtw_band(BandParams p, cudaStream_t st, int num_sms) {
     p.seglen = c.seglen;
     p.vec4 = (p.L % 4 == 0 && c.seglen % 4 == 0 && c.padl % 4 == 0 &&
               ((uintptr_t)p.A % 16) == 0 && ((uintptr_t)p.B % 16) == 0) ? 1 : 0;
+    {
+        // Global A rows (GA) for the config-2 layout (R = 26, full warp, half-packed): there two
+        // padded rows per group hold the SM to 8 warps; with the query rows read through L1
+        // from a padded copy (k_pad_rows, once per launch) only B is staged and 16 warps fit
+        // -- the survivor round 198 -> 190 ms.  Other layouts keep both rows in shared memory
+        // (not measured with GA).  NNDTW_BAND_GA=0 disables it (experiments).
+        static const char *ga = getenv("NNDTW_BAND_GA");
+        const bool ga_on = !(ga && ga[0] == '0');
+        if (ga_on && p.mode == 0 && p.apad_ws != nullptr && c.R == 26 && c.km == 2 && c.pack &&
+            p.vec4 && p.dbg_na > 0 && p.dbg_na * (int64_t)c.seglen <= p.apad_cap) {
+            const int64_t n = p.dbg_na * (int64_t)c.seglen;
+            const int64_t blocks = (n + 255) / 256 < 4 * num_sms ? (n + 255) / 256 : 4 * num_sms;
+            k_pad_rows<<<(unsigned)blocks, 256, 0, st>>>(p.A, p.dbg_na, p.L, p.padl, p.seglen,
+                                                         p.apad_ws);
+            count_launch(1, "k_pad_rows");
+            p.Apad = p.apad_ws;
+            return launch_band_t<26, 2, true, true>(p, c, st, num_sms);
+        }
+    }
     switch (c.R) {
         BAND_CASE(2)
         BAND_CASE(4)
@@ -690,7 +728,8 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
                  const int32_t *ia, const int32_t *ib, int64_t nitems_host, int L, int w,
                  int mode, unsigned long long *key, int64_t index_base, float eps_t, TieLog log,
                  unsigned long long *counters, const long long *cells_prefix,
-                 const float *cutoff, float *out, cudaStream_t st, int num_sms) {
+                 const float *cutoff, float *out, cudaStream_t st, int num_sms,
+                 float *apad_ws, int64_t apad_cap) {
     if (w > L - 1) w = L - 1;
     BandParams p;
     p.A = A;
@@ -719,6 +758,9 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
     p.out = out;
     p.dbg_na = na;
     p.dbg_nb = nb;
+    p.Apad = nullptr;
+    p.apad_ws = apad_ws;
+    p.apad_cap = apad_cap;
     const int kind = dtw_kernel_kind(L, w);
     if (kind == 0) return launch_dtw_w0(p, st, num_sms);
     if (kind == 1) {

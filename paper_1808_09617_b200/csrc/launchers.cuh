@@ -106,7 +106,11 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
                  const int32_t *ia, const int32_t *ib, int64_t nitems_host, int L, int w,
                  int mode, unsigned long long *key, int64_t index_base, float eps_t, TieLog log,
                  unsigned long long *counters, const long long *cells_prefix,
-                 const float *cutoff, float *out, cudaStream_t st, int num_sms);
+                 const float *cutoff, float *out, cudaStream_t st, int num_sms,
+                 float *apad_ws = nullptr, int64_t apad_cap = 0);
+// floats per query row of the band kernel's padded A copy (an upper bound of its row length
+// seglen for any window: padl + L + padr <= L + w + R + 48)
+inline int64_t band_apad_row_floats(int L) { return 2 * (int64_t)L + 128; }
 
 int dtw_kernel_kind(int L, int w);  // 0 = k_dtw_w0, 1 = k_dtw_band, 2 = k_dtw_strip
 int strip_rows_per_lane(int L);
