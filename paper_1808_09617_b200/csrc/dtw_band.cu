@@ -589,8 +589,10 @@ int launch_dtw_band(BandParams p, cudaStream_t st, int num_sms) {
         // Global A rows (GA) for the config-2 layout (R = 26, full warp, half-packed): there two
         // padded rows per group hold the SM to 8 warps; with the query rows read through L1
         // from a padded copy (k_pad_rows, once per launch) only B is staged and 16 warps fit
-        // -- the survivor round 198 -> 190 ms.  Other layouts keep both rows in shared memory
-        // (not measured with GA).  NNDTW_BAND_GA=0 disables it (experiments).
+        // -- the survivor round 198 -> 190 ms.  Other layouts keep both rows in shared memory:
+        // forced on for every layout, config 3's LOOCV went 424 -> 434 ms and config 1's
+        // survivor rounds 9.10 -> 9.34 ms (their bands leave room for two CTAs, or the L1
+        // reads cost more than the residency gains).  NNDTW_BAND_GA=0 disables it.
         static const char *ga = getenv("NNDTW_BAND_GA");
         const bool ga_on = !(ga && ga[0] == '0');
         if (ga_on && p.mode == 0 && p.apad_ws != nullptr && c.R == 26 && c.km == 2 && c.pack &&
