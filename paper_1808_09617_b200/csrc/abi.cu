@@ -113,6 +113,7 @@ struct ClassifyWs {
     long long *col_count, *col_off, *col_fill;
     float *apad;     // the band kernel's padded query rows (survivor round, GA variant)
     int64_t apad_cap;
+    unsigned *colmask;  // two-stage lists: live bits per (32-query tile, train series)
     int32_t *blist;  // the listed queries, train-series-major (col_off)
     float *bval;     // their full cascade values (S3 compacts from these lists)
     unsigned long long *minkey2;  // argmin of the full cascade value (second seed)
@@ -162,6 +163,7 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
     W.minkey2 = (unsigned long long *)take(8 * q1);
     W.apad_cap = (int64_t)q1 * band_apad_row_floats(L);
     W.apad = (float *)take(sizeof(float) * (size_t)W.apad_cap);
+    W.colmask = (unsigned *)take(sizeof(unsigned) * ((q1 + 31) / 32) * t1);
     W.blist = (int32_t *)take(sizeof(int32_t) * (size_t)W.item_cap);
     W.bval = (float *)take(sizeof(float) * (size_t)W.item_cap);
     W.bytes = off;
@@ -351,7 +353,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         // stage B: the pairs Algorithm 1's line-12 test keeps (P <= bsf1*(1+eps_p)), per train
         // series, and the full cascade value for them (+ its argmin: the second seed)
         launch_col_compact(W.lb, W.ldlb, nq, nt, key, eps_p, W.col_count, W.col_off, W.col_fill,
-                           W.blist, W.item_cap, sms, st);
+                           W.blist, W.item_cap, W.colmask, sms, st);
         cudaMemsetAsync(W.minkey2, 0xff, 8 * (size_t)nq, st);
         if (bridge_tm.on) cudaEventRecord(bridge_tm.ev[0], st);
         if (launch_lb_sparse(q, W.qkim, nq, t, U, Lo, tkim, nt, L, w, v, W.col_off,

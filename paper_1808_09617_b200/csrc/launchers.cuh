@@ -18,7 +18,8 @@ int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
 int launch_col_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
                        const unsigned long long *key, float eps_p, long long *col_count,
                        long long *col_off, long long *col_fill, int32_t *qlist,
-                       unsigned long long qlist_cap, int num_sms, cudaStream_t st);
+                       unsigned long long qlist_cap, unsigned *colmask, int num_sms,
+                       cudaStream_t st);
 int launch_lb_sparse(const float *q, const nndtw_kim *qkim, int64_t nq, const float *t,
                      const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L,
                      int w, int v, const long long *col_off, const int32_t *qlist, float *bval,

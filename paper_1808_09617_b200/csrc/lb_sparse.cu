@@ -18,7 +18,8 @@
 //
 // B200 design.  Column lists: tiles of 32 queries x 1024 train series read the bound matrix
 // coalesced (float4), count per (tile, series) in registers and reserve with one atomic per
-// (tile, series) -- two passes (count, scatter) around a one-block scan.  Sparse bridge: the
+// (tile, series) -- two passes (count, scatter) around a one-block scan; the count pass stores
+// the 32-bit live mask per (tile, series), so the scatter pass reads 1/32 of the matrix's bytes.  Sparse bridge: the
 // warp stages its series' envelope (U, L) in shared memory with the band columns masked to
 // (+inf, -inf) (a zero term), then per listed query: lane l takes 4 consecutive columns per
 // 128 (float4 query loads from L2, where the 20 MB of queries stay), a - U, L - a, max with 0,
@@ -31,6 +32,9 @@ namespace nndtw {
 constexpr int CC_Q = 32;     // queries per column-compaction tile
 constexpr int CC_N = 1024;   // train series per tile (256 threads x 4)
 
+// PASS 0 reads the bound matrix, counts per (tile, series) and stores the tile's live bits per
+// series (colmask[q-tile][n], 32 bits: 1/8 byte per pair); PASS 1 scatters from the masks
+// alone, so the 4 GB matrix is streamed once, not twice.
 template <int PASS>
 __global__ void __launch_bounds__(256) k_col_compact(const float *__restrict__ lb, int64_t ldlb,
                                                      int64_t nq, int64_t nt,
@@ -38,30 +42,41 @@ __global__ void __launch_bounds__(256) k_col_compact(const float *__restrict__ l
                                                      float eps_p, long long *col_count,
                                                      const long long *__restrict__ col_off,
                                                      long long *col_fill, int32_t *qlist,
-                                                     unsigned long long qlist_cap) {
+                                                     unsigned long long qlist_cap,
+                                                     unsigned *colmask) {
     const int64_t ntq = (nq + CC_Q - 1) / CC_Q, ntn = (nt + CC_N - 1) / CC_N;
     const bool vec = (ldlb & 3) == 0;
     for (int64_t tile = blockIdx.x; tile < ntq * ntn; tile += gridDim.x) {
-        const int64_t q0 = (tile / ntn) * CC_Q;
+        const int64_t tq = tile / ntn;
+        const int64_t q0 = tq * CC_Q;
         const int64_t n0 = (tile % ntn) * CC_N + 4 * threadIdx.x;
         unsigned live[4] = {0u, 0u, 0u, 0u};  // bit qq: query q0+qq keeps series n0+e
+        unsigned *mrow = colmask + tq * nt;
+        if (PASS == 0) {
 #pragma unroll 4
-        for (int qq = 0; qq < CC_Q; ++qq) {
-            const int64_t q = q0 + qq;
-            if (q >= nq) break;
-            const float thr = key_dist(key[q]) * (1.0f + eps_p);
-            const float *row = lb + q * ldlb;
-            float v[4];
-            if (vec && n0 + 3 < nt) {
-                const float4 f = *reinterpret_cast<const float4 *>(row + n0);
-                v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-            } else {
+            for (int qq = 0; qq < CC_Q; ++qq) {
+                const int64_t q = q0 + qq;
+                if (q >= nq) break;
+                const float thr = key_dist(key[q]) * (1.0f + eps_p);
+                const float *row = lb + q * ldlb;
+                float v[4];
+                if (vec && n0 + 3 < nt) {
+                    const float4 f = *reinterpret_cast<const float4 *>(row + n0);
+                    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+                } else {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) v[e] = n0 + e < nt ? row[n0 + e] : kInf;
+                    for (int e = 0; e < 4; ++e) v[e] = n0 + e < nt ? row[n0 + e] : kInf;
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e)  // (NaN -- the leave-one-out self pair -- is never kept)
+                    live[e] |= (n0 + e < nt && v[e] <= thr) ? (1u << qq) : 0u;
             }
 #pragma unroll
-            for (int e = 0; e < 4; ++e)  // (NaN -- the leave-one-out self pair -- is never kept)
-                live[e] |= (n0 + e < nt && v[e] <= thr) ? (1u << qq) : 0u;
+            for (int e = 0; e < 4; ++e)
+                if (n0 + e < nt) mrow[n0 + e] = live[e];
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) live[e] = n0 + e < nt ? mrow[n0 + e] : 0u;
         }
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -117,16 +132,19 @@ __global__ void __launch_bounds__(1024) k_col_scan(const long long *count, long 
 int launch_col_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
                        const unsigned long long *key, float eps_p, long long *col_count,
                        long long *col_off, long long *col_fill, int32_t *qlist,
-                       unsigned long long qlist_cap, int num_sms, cudaStream_t st) {
+                       unsigned long long qlist_cap, unsigned *colmask, int num_sms,
+                       cudaStream_t st) {
     if (nq == 0 || nt == 0) return 0;
     cudaMemsetAsync(col_count, 0, sizeof(long long) * (size_t)nt, st);
     const int64_t ntiles = ((nq + CC_Q - 1) / CC_Q) * ((nt + CC_N - 1) / CC_N);
     const int64_t grid = ntiles < (int64_t)num_sms * 8 ? ntiles : (int64_t)num_sms * 8;
     k_col_compact<0><<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, eps_p, col_count,
-                                                     col_off, col_fill, qlist, qlist_cap);
+                                                     col_off, col_fill, qlist, qlist_cap,
+                                                     colmask);
     k_col_scan<<<1, 1024, 0, st>>>(col_count, col_off, col_fill, nt);
     k_col_compact<1><<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, eps_p, col_count,
-                                                     col_off, col_fill, qlist, qlist_cap);
+                                                     col_off, col_fill, qlist, qlist_cap,
+                                                     colmask);
     count_launch(3, __func__);
     return 0;
 }
