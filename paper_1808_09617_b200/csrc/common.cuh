@@ -173,6 +173,13 @@ __device__ __forceinline__ float kim_sum(float qf, float ql, float tf, float tl,
     return kim_sum_f(qf, ql, tf, tl, kim_f(ka, L), kim_f(kb, L));
 }
 
+// Algorithm 1 line 1: delta(A_1, B_1) + delta(A_L, B_L), one rounding order for every
+// kernel that computes it (tile, sparse bridge), so their band sums agree bit for bit
+__device__ __forceinline__ float boundary_terms(float qf, float ql, float tf, float tl) {
+    const float df = qf - tf, dl = ql - tl;
+    return fmaf(df, df, __fmul_rn(dl, dl));
+}
+
 // ---- work items ---------------------------------------------------------------------------
 // A DTW work item: query (row of A), train (row of B), local indices, and the pair's cascade
 // bound (survivor items are skipped at fetch time when it exceeds the live best-so-far).

@@ -188,7 +188,8 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
     for (int qi = 0; qi < LB_QPT; ++qi)
 #pragma unroll
         for (int j = 0; j < LB_NPT; ++j)
-            acc[qi][j] = p.keogh ? 0.0f : sq(qhv(qi, 0) - thv(j, 0)) + sq(qtv(qi, 0) - ttv(j, 0));
+            acc[qi][j] = p.keogh ? 0.0f : boundary_terms(qhv(qi, 0), qtv(qi, 0), thv(j, 0),
+                                                          ttv(j, 0));
 
     // 8 query values (side 0: x[i], side 1: x[L-1-i]) as four f32x2 pairs (queries 2k, 2k+1)
     auto q8 = [&](int side, int i, unsigned long long (&v)[LB_QPT / 2]) {
@@ -218,17 +219,9 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
             // min over the band of (x-y)^2 = (min |x-y|)^2 exactly (rounding is monotone in
             // |x-y|): the band minimum runs on |differences| (FMNMX3 with |.| operands, ALU pipe)
             // and squares once; the differences of two queries against one train value are one
-            // FADD2 (bit-identical to two FADDs)
-#pragma unroll
-            for (int qp = 0; qp < LB_QPT / 2; ++qp)
-#pragma unroll
-                for (int j = 0; j < LB_NPT; ++j) {
-                    float d0, d1;
-                    f2_unpack(f2_sub(ai[qp], f2_pack(bi[j], bi[j])), d0, d1);
-                    m[2 * qp][j] = fabsf(d0);
-                    m[2 * qp + 1][j] = fabsf(d1);
-                }
-            for (int jj = jlo; jj < i; ++jj) {
+            // FADD2 (bit-identical to two FADDs).  The cell (i, i) joins the first band step's
+            // FMNMX3 (its |.| is then an operand modifier, not an instruction).
+            auto band_step = [&](int jj, bool first) {
                 unsigned long long aj[LB_QPT / 2];
                 float bj[LB_NPT];
                 q8(side, jj, aj);
@@ -241,15 +234,37 @@ __global__ void __launch_bounds__(256, 2) k_lb_tile(LbParams p) {
                         float x0, x1, y0, y1;
                         f2_unpack(f2_sub(ai[qp], f2_pack(bj[j], bj[j])), x0, x1);  // a_i - b_jj
                         f2_unpack(f2_sub(aj[qp], f2_pack(bi[j], bi[j])), y0, y1);  // a_jj - b_i
-                        m[2 * qp][j] = fminf(m[2 * qp][j], fminf(fabsf(x0), fabsf(y0)));
-                        m[2 * qp + 1][j] = fminf(m[2 * qp + 1][j], fminf(fabsf(x1), fabsf(y1)));
+                        if (first) {
+                            float d0, d1;
+                            f2_unpack(f2_sub(ai[qp], f2_pack(bi[j], bi[j])), d0, d1);  // a_i - b_i
+                            m[2 * qp][j] = fminf(fabsf(d0), fminf(fabsf(x0), fabsf(y0)));
+                            m[2 * qp + 1][j] = fminf(fabsf(d1), fminf(fabsf(x1), fabsf(y1)));
+                        } else {
+                            m[2 * qp][j] = fminf(m[2 * qp][j], fminf(fabsf(x0), fabsf(y0)));
+                            m[2 * qp + 1][j] =
+                                fminf(m[2 * qp + 1][j], fminf(fabsf(x1), fabsf(y1)));
+                        }
+                    }
+            };
+            if (jlo < i) {
+                band_step(i - 1, true);
+                for (int jj = jlo; jj < i - 1; ++jj) band_step(jj, false);
+            } else {  // w = 0: the band is the cell (i, i) alone
+#pragma unroll
+                for (int qp = 0; qp < LB_QPT / 2; ++qp)
+#pragma unroll
+                    for (int j = 0; j < LB_NPT; ++j) {
+                        float d0, d1;
+                        f2_unpack(f2_sub(ai[qp], f2_pack(bi[j], bi[j])), d0, d1);
+                        m[2 * qp][j] = fabsf(d0);
+                        m[2 * qp + 1][j] = fabsf(d1);
                     }
             }
 #pragma unroll
             for (int qi = 0; qi < LB_QPT; ++qi)
 #pragma unroll
-                for (int j = 0; j < LB_NPT; ++j)  // rounded square, then add (no FFMA contraction)
-                    acc[qi][j] = __fadd_rn(acc[qi][j], __fmul_rn(m[qi][j], m[qi][j]));
+                for (int j = 0; j < LB_NPT; ++j)  // band term: m^2 added with one rounding
+                    acc[qi][j] = fmaf(m[qi][j], m[qi][j], acc[qi][j]);
         }
     }
 

@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
                     return NCH > 0 ? hd[side * nb + x] : __ldg(a + (side ? L - 1 - x : x));
                 };
                 const float a0 = qv(0, 0), al = qv(1, 0);
-                float bands = (a0 - th[0]) * (a0 - th[0]) + (al - tt[0]) * (al - tt[0]);
+                float bands = boundary_terms(a0, al, th[0], tt[0]);
                 for (int side = 0; side < 2; ++side) {
                     const float *bs = side ? tt : th;  // bs[x] = t[x] or t[L-1-x]
                     for (int i = 1; i < nb; ++i) {
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
                         float m = fabsf(ai - bi);
                         for (int jj = i - w > 0 ? i - w : 0; jj < i; ++jj)
                             m = fminf(m, fminf(fabsf(ai - bs[jj]), fabsf(qv(side, jj) - bi)));
-                        bands = __fadd_rn(bands, __fmul_rn(m, m));
+                        bands = fmaf(m, m, bands);  // as the tile kernel
                     }
                 }
                 const float kim = kim_sum(a0, al, t0, tl, qkim[myq], kb, L);
