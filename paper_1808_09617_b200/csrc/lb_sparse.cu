@@ -10,9 +10,9 @@
 //            k_lb_sparse: one warp per train series computes the full cascade value
 //            max(LB_Kim, boundary + bands + bridge) for its listed queries, overwriting P, and
 //            the per-query argmin of the full value -> second seed (another S3 seed round).
-// Afterwards the bound matrix holds the full cascade value for every surviving pair and P
-// (> bsf1 >= the final best-so-far) for every pruned one, so S3's compaction keeps exactly the
-// pairs the one-stage path keeps.  On config 2 the partial cascade prunes ~91 % of the pairs
+// Afterwards every pair that can survive is listed with its full cascade value (the others have
+// P > bsf1 >= the final best-so-far), so S3's compaction (k_list_compact, search.cu) keeps the
+// pairs the one-stage path keeps, up to the rounding order of the bridge sum.  On config 2 the partial cascade prunes ~91 % of the pairs
 // (numpy simulation of the seeds: 91.2 % with the partial-argmin seed, the second seed recovers
 // the full-argmin seed's best-so-far), so the O(L) bridge runs on ~9 % of them.
 //
