@@ -21,5 +21,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches_${tag}.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1
 ncu --set full --import-source on --clock-control none \
-    -k regex:"k_dtw_band|k_lb_tile|k_lb_sparse|k_col_compact|k_list_compact|k_env_direct|k_compact" -c 10 -o gpurun_out/prof_${tag} \
+    -k regex:"k_dtw_band|k_lb_tile|k_lb_sparse|k_col_compact|k_list_compact|k_env_direct|k_compact|k_pad_rows" -c 12 -o gpurun_out/prof_${tag} \
     python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
