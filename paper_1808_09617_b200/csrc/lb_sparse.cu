@@ -161,8 +161,8 @@ __host__ __device__ inline int sparse_row_len(int L, int nch) {
 // NCH == 0 the masked envelope rows + head / tail
 __host__ __device__ inline int sparse_warp_floats(int L, int nch) {
     const int Lp = sparse_row_len(L, nch);
-    // (NCH > 0: after a batch's bridge the ring holds the 32 queries' head / tail values)
-    const int ring = SP_D * Lp > 32 * (2 * SP_NBMAX + 1) ? SP_D * Lp : 32 * (2 * SP_NBMAX + 1);
+    // (NCH > 0: after a batch's bridge the ring holds the 32 queries' head / tail pairs)
+    const int ring = SP_D * Lp > 32 * (2 * SP_NBMAX + 2) ? SP_D * Lp : 32 * (2 * SP_NBMAX + 2);
     return (nch > 0 ? ring : 2 * Lp) + 2 * SP_NBMAX;
 }
 
@@ -197,8 +197,8 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
     float *wbase = sp_smem + (size_t)warp * sparse_warp_floats(L, NCH);
     float *ring = wbase;                          // NCH > 0: SP_D query rows
     float *sU = wbase, *sL = wbase + Lp;          // NCH == 0: masked envelope rows
-    float *th = wbase + sparse_warp_floats(L, NCH) - 2 * SP_NBMAX;  // t[0 .. nb)
-    float *tt = th + SP_NBMAX;                    // t[L-1-i], i < nb
+    // the series' (t[x], t[L-1-x]) pairs, x < nb (Algorithm 1's left and right bands together)
+    float2 *th2 = reinterpret_cast<float2 *>(wbase + sparse_warp_floats(L, NCH) - 2 * SP_NBMAX);
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     if (NCH > 0) {  // the ring's columns past L are never copied: finite from the start
@@ -238,10 +238,7 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
                 sL[c] = br ? __ldg(ln + c) : -kInf;
             }
         }
-        if (lane < nb) {
-            th[lane] = __ldg(tn + lane);
-            tt[lane] = __ldg(tn + (L - 1 - lane));
-        }
+        if (lane < nb) th2[lane] = make_float2(__ldg(tn + lane), __ldg(tn + (L - 1 - lane)));
         const nndtw_kim kb = tkim[n];
         const float t0 = __ldg(tn), tl = __ldg(tn + L - 1);
         __syncwarp();
@@ -346,43 +343,61 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
                 }
             }
             // every lane finishes its own query: boundary terms + bands (Algorithm 1 lines 1-11,
-            // the band minimum over |differences| squared once, as the tile kernel), LB_Kim.
-            // NCH > 0: the query's a[0 .. nb) and a[L-1-i], i < nb, are first copied into the
-            // (now free) ring in one round trip (hd[x] = a[x], hd[nb + x] = a[L-1-x]); read
-            // one by one from L2 they were a chain of dependent misses.
-            const float *hd = ring + lane * (2 * nb + 1);
+            // the band minimum over |differences| squared once, in the tile kernel's order),
+            // LB_Kim.  The left band of the series and the right band (the left band of the
+            // reversed series) run together as f32x2 pairs (a[x], a[L-1-x]) - (t[y], t[L-1-y]).
+            // NCH > 0: the query's pairs are first copied into the (now free) ring in one round
+            // trip (read one by one from L2 they were a chain of dependent misses).
+            const int s2 = (nb % 2 == 0) ? nb + 1 : nb + 2;  // pairs per lane row (odd: banks)
             if (NCH > 0) {
                 __syncwarp();  // every lane's ring reads of this batch are done
                 // per copy instruction 32 / (2nb) queries, 2nb lanes each (lane x < nb: a[x],
                 // else a[L-1-(x-nb)]): few rows per instruction, not 32 scattered ones
                 const int per = 32 / (2 * nb), k = lane / (2 * nb), x = lane % (2 * nb);
+                const int side = x < nb ? 0 : 1, xx = x < nb ? x : x - nb;
                 for (int p0 = 0; p0 < nbatch; p0 += per) {
                     const int p = p0 + k;
                     const int qi = __shfl_sync(0xffffffffu, myq, p & 31);
                     if (k < per && p < nbatch)
-                        cp_async4(ring + p * (2 * nb + 1) + x,
-                                  q + (int64_t)qi * L + (x < nb ? x : L - 1 - (x - nb)));
+                        cp_async4(ring + 2 * (p * s2 + xx) + side,
+                                  q + (int64_t)qi * L + (side ? L - 1 - xx : xx));
                 }
                 cp_async_commit();
                 cp_async_wait_group<0>();
-                __syncwarp();  // hd rows were written by other lanes
+                __syncwarp();  // the pair rows were written by other lanes
             }
             if (lane < nbatch) {
                 const float *a = q + (int64_t)myq * L;
-                auto qv = [&](int side, int x) {  // a[x] or a[L-1-x]
-                    return NCH > 0 ? hd[side * nb + x] : __ldg(a + (side ? L - 1 - x : x));
-                };
-                const float a0 = qv(0, 0), al = qv(1, 0);
-                float bands = boundary_terms(a0, al, th[0], tt[0]);
-                for (int side = 0; side < 2; ++side) {
-                    const float *bs = side ? tt : th;  // bs[x] = t[x] or t[L-1-x]
-                    for (int i = 1; i < nb; ++i) {
-                        const float ai = qv(side, i), bi = bs[i];
-                        float m = fabsf(ai - bi);
-                        for (int jj = i - w > 0 ? i - w : 0; jj < i; ++jj)
-                            m = fminf(m, fminf(fabsf(ai - bs[jj]), fabsf(qv(side, jj) - bi)));
-                        bands = fmaf(m, m, bands);  // as the tile kernel
+                const float2 *hd2 = reinterpret_cast<const float2 *>(ring) + lane * s2;
+                auto qa = [&](int x) {  // (a[x], a[L-1-x])
+                    if (NCH > 0) {
+                        const float2 v = hd2[x];
+                        return f2_pack(v.x, v.y);
                     }
+                    return f2_pack(__ldg(a + x), __ldg(a + (L - 1 - x)));
+                };
+                auto tb = [&](int x) {  // (t[x], t[L-1-x])
+                    const float2 v = th2[x];
+                    return f2_pack(v.x, v.y);
+                };
+                float a0, al;
+                f2_unpack(qa(0), a0, al);
+                float bands = boundary_terms(a0, al, t0, tl);
+                for (int i = 1; i < nb; ++i) {
+                    const unsigned long long ai = qa(i), bi = tb(i);
+                    float m0, m1;
+                    f2_unpack(f2_sub(ai, bi), m0, m1);
+                    m0 = fabsf(m0);
+                    m1 = fabsf(m1);
+                    for (int jj = i - w > 0 ? i - w : 0; jj < i; ++jj) {
+                        float x0, x1, y0, y1;
+                        f2_unpack(f2_sub(ai, tb(jj)), x0, x1);  // a_i - b_jj
+                        f2_unpack(f2_sub(qa(jj), bi), y0, y1);  // a_jj - b_i
+                        m0 = fminf(m0, fminf(fabsf(x0), fabsf(y0)));
+                        m1 = fminf(m1, fminf(fabsf(x1), fabsf(y1)));
+                    }
+                    bands = fmaf(m0, m0, bands);  // left band, then right: the tile kernel's order
+                    bands = fmaf(m1, m1, bands);
                 }
                 const float kim = kim_sum(a0, al, t0, tl, qkim[myq], kb, L);
                 const float full = fmaxf(kim, bands + mybridge);
@@ -390,9 +405,9 @@ __global__ void __launch_bounds__(256) k_lb_sparse(const float *__restrict__ q,
                 if (lb) lb[(int64_t)myq * ldlb + n] = full;  // level counters only
                 atomicMin(minkey2 + myq, make_key(full, (unsigned)n));
             }
-            __syncwarp();  // the next batch's row copies overwrite hd
+            __syncwarp();  // the next batch's row copies overwrite the pair rows
         }
-        __syncwarp();  // the next series overwrites th / tt (and, NCH == 0, sU / sL)
+        __syncwarp();  // the next series overwrites th2 (and, NCH == 0, sU / sL)
     }
 }
 
