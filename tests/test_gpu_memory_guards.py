@@ -149,6 +149,26 @@ def test_classify_workspace_guards_and_poisoning(dev, monkeypatch, flags, stages
     assert np.array_equal(keys[0], keys[1]) and np.array_equal(keys[0], keys[2])
 
 
+@pytest.mark.parametrize("stages", ["1", "2"])
+def test_classify_ga_layout_guards_and_poisoning(dev, oracle_lib, monkeypatch, stages):
+    """Config 2's band layout (L = 512, w = 103: R = 26, full warp, half-packed), whose survivor
+    round reads the query rows from the padded copy in the workspace (GA variant, k_pad_rows):
+    guard zones intact, the same keys under zero / 0xFF / random workspace poisoning, and the
+    oracle's neighbours."""
+    monkeypatch.setenv("NNDTW_S2_STAGES", stages)
+    ds = datagen.make_dataset(2, n_train=400, n_test=48)
+    w = ds.cfg.windows()[0]
+    assert w == 103
+    runs = [_classify_raw(dev, ds.train, ds.train_labels, ds.test, w, 5, 1, f)
+            for f in (0, 0xFF, "random")]
+    keys = [r[0] for r in runs]
+    assert np.array_equal(keys[0], keys[1]) and np.array_equal(keys[0], keys[2])
+    assert runs[0][1]["dtw_calls"] > 0
+    idx = (keys[0] & 0xFFFFFFFF).astype(np.int64)
+    ridx, _ = oracle_lib.nn(ds.test, ds.train, w)[:2]
+    assert np.array_equal(idx, ridx)
+
+
 def test_loocv_workspace_guards_and_poisoning(dev):
     import torch
     from paper_1808_09617_b200 import nndtw
