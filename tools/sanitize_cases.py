@@ -35,6 +35,7 @@ def case(name, fn):
 
 
 def main():
+    print("library", nndtw.LIB_PATH, flush=True)
     rng = np.random.default_rng(5)
     # S0-S7 on config 0 (all of classify's kernels), with stats and level counts
     ds = datagen.make_dataset(0)
@@ -53,6 +54,10 @@ def main():
     m1 = nndtw.Model(T(d1.train), T(d1.train_labels), d1.cfg.windows()[0], 5)
     case("classify two-stage S2 L=256", lambda: nndtw.classify(m1, T(d1.test)))
     del os.environ["NNDTW_S2_STAGES"]
+    # config 2's band layout (R = 26, full warp): the survivor round's padded query copy (GA)
+    d2 = datagen.make_dataset(2, n_train=300, n_test=32)
+    m2 = nndtw.Model(T(d2.train), T(d2.train_labels), d2.cfg.windows()[0], 5)
+    case("classify L=512 w=103 (GA band variant)", lambda: nndtw.classify(m2, T(d2.test)))
     ms = nndtw.Model(T(ds.train), T(ds.train_labels), w0, 5, symmetric=True)
     case("classify symmetric", lambda: nndtw.classify(ms, T(ds.test[:24])))
 
