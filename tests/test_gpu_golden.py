@@ -41,10 +41,12 @@ def dataset(c):
     return _DS[c]
 
 
-def _classify(dev, ds, w, V, **kw):
+def _classify(dev, ds, w, V, stats_out=None, **kw):
     from paper_1808_09617_b200 import nndtw
     model = nndtw.Model(T(ds.train, dev), T(ds.train_labels, dev), w, V, **kw)
-    p = nndtw.classify(model, T(ds.test, dev))
+    p = nndtw.classify(model, T(ds.test, dev), stats=stats_out is not None)
+    if stats_out is not None:
+        stats_out.update(p.stats)
     return p.idx.cpu().numpy(), p.label.cpu().numpy(), p.dist.cpu().numpy()
 
 
@@ -62,9 +64,12 @@ def test_golden_classify_every_query(dev, c):
     w = int(g["w"])
     assert w == ds.cfg.windows()[0]
     V = int(g["V"]) if "V" in g else 5
-    idx, lab, dist = _classify(dev, ds, w, V)
+    st = {}
+    idx, lab, dist = _classify(dev, ds, w, V, stats_out=st)
     assert idx.shape[0] == ds.test.shape[0] == g["idx"].shape[0]
     _compare(idx, lab, dist, g["idx"], g["label"], g["dist"], f"config {c}")
+    if c == 2:  # the size gate runs the default cascade in two stages here
+        assert 0 < st["bridge_pairs"] < st["lb_pairs"], st
 
 
 @pytest.mark.parametrize("p", [1, 10, 20, 50, 100])
