@@ -53,8 +53,8 @@ __global__ void __launch_bounds__(256) k_col_compact(const float *__restrict__ l
         unsigned live[4] = {0u, 0u, 0u, 0u};  // bit qq: query q0+qq keeps series n0+e
         unsigned *mrow = colmask + tq * nt;
         if (PASS == 0) {
-#pragma unroll 4
-            for (int qq = 0; qq < CC_Q; ++qq) {
+#pragma unroll 16
+            for (int qq = 0; qq < CC_Q; ++qq) {  // (16 rows' loads in flight per thread)
                 const int64_t q = q0 + qq;
                 if (q >= nq) break;
                 const float thr = key_dist(key[q]) * (1.0f + eps_p);
