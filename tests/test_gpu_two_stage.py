@@ -112,3 +112,19 @@ def test_two_stage_sharded_phases(dev, two_stage):
     ks, ws, _ = nndtw.classify_keys(model, q, exact=False, phase="seed")
     k2, _, _ = nndtw.classify_keys(model, q, exact=False, phase="search", key=ks.clone(), ws=ws)
     assert torch.equal(k1, k2)
+
+
+@pytest.mark.parametrize("nq,nt,L,kind", [(1, 1, 64, "walk"), (1, 500, 128, "walk"),
+                                          (40, 1, 64, "walk"), (33, 70, 96, "int"),
+                                          (65, 3, 256, "const"), (100, 90, 512, "walk")])
+def test_two_stage_degenerate_sizes(dev, oracle_lib, two_stage, nq, nt, L, kind):
+    """One query, one train series, 32k+1 queries per list (a one-entry batch after full ones),
+    a list of every query on every series (constant series: every pair ties and survives)."""
+    rng = np.random.default_rng(nq * 1000 + nt)
+    Tr = datagen.random_series(rng, nt, L, kind)
+    Q = datagen.random_series(rng, nq, L, kind)
+    trl = rng.integers(0, 3, size=nt).astype(np.int32)
+    w = max(1, L // 10)
+    idx, lab, dist, st = _classify(dev, Tr, trl, Q, w, 5, stats=True)
+    _check_nn(oracle_lib, Tr, trl, Q, w, idx, lab, dist)
+    assert 0 <= st["bridge_pairs"] <= nq * nt
