@@ -5,26 +5,26 @@
 //   stage A  k_lb_tile in no-bridge mode (lb.cu): P = max(LB_Kim, boundary + bands) for every
 //            pair, and the per-query argmin of P -> first seed; the seed's DTW (S3 seed round)
 //            gives a best-so-far bsf1 per query.
-//   stage B  k_col_compact: the pairs with P <= bsf1*(1+eps_p) (the others are pruned: Algorithm
-//            1 returns "infinity" at line 12) as per-train-series lists of queries;
-//            k_lb_sparse: one warp per train series computes the full cascade value
-//            max(LB_Kim, boundary + bands + bridge) for its listed queries, overwriting P, and
-//            the per-query argmin of the full value -> second seed (another S3 seed round).
+//   lists    k_col_compact: the pairs with P <= bsf1*(1+eps_p) (the others are pruned: Algorithm
+//            1 returns "infinity" at line 12) as per-train-series lists of queries.
+//   stage B  k_lb_sparse: one warp per train series computes the full cascade value
+//            max(LB_Kim, boundary + bands + bridge) for its listed queries, stores it next to
+//            the list entry, and the per-query argmin of the full value -> second seed (another
+//            S3 seed round).
 // Afterwards every pair that can survive is listed with its full cascade value (the others have
 // P > bsf1 >= the final best-so-far), so S3's compaction (k_list_compact, search.cu) keeps the
-// pairs the one-stage path keeps, up to the rounding order of the bridge sum.  On config 2 the partial cascade prunes ~91 % of the pairs
-// (numpy simulation of the seeds: 91.2 % with the partial-argmin seed, the second seed recovers
-// the full-argmin seed's best-so-far), so the O(L) bridge runs on ~9 % of them.
+// pairs the one-stage path keeps, up to the rounding order of the bridge sum.  On config 2 the
+// partial cascade leaves 7.3 % of the pairs to the O(L) bridge.
 //
 // B200 design.  Column lists: tiles of 32 queries x 1024 train series read the bound matrix
 // coalesced (float4), count per (tile, series) in registers and reserve with one atomic per
 // (tile, series) -- two passes (count, scatter) around a one-block scan; the count pass stores
-// the 32-bit live mask per (tile, series), so the scatter pass reads 1/32 of the matrix's bytes.  Sparse bridge: the
-// warp stages its series' envelope (U, L) in shared memory with the band columns masked to
-// (+inf, -inf) (a zero term), then per listed query: lane l takes 4 consecutive columns per
-// 128 (float4 query loads from L2, where the 20 MB of queries stay), a - U, L - a, max with 0,
-// FFMA; lanes 0 .. 2nb-3 each compute one band minimum of Algorithm 1 (lines 4-10), lane 2nb-2
-// the boundary terms (line 1); one warp sum; lane 0 adds LB_Kim by max.
+// the 32-bit live mask per (tile, series), so the scatter pass reads 1/32 of the matrix's bytes.
+// Sparse bridge (k_lb_sparse below): the series' envelope over the bridge columns in registers,
+// the listed queries' rows streamed through a per-warp cp.async ring (the 20 MB of queries stay
+// in L2), column pairs in f32x2, groups of 8 queries reduced with one transposing shuffle tree;
+// then each lane finishes its own query of the 32-query batch: boundary terms and bands from the
+// query's head/tail values (staged once per batch), LB_Kim, max.
 #include "launchers.cuh"
 
 namespace nndtw {
