@@ -17,7 +17,9 @@
 // "kill" slot whose A value is scaled by +inf (NaN/inf results, ignored by fminf); slots
 // beyond it stay +inf.  Early abandoning (reading C14): after every period the registers hold
 // two consecutive anti-diagonals, a cut of every warping path; the group abandons when every
-// lane's minimum exceeds bsf*(1+eps_t) (one warp ballot).
+// lane's minimum exceeds bsf*(1+eps_t) (one warp ballot).  GA variant (config 2's layout): the
+// query rows come through L1 from a padded copy in the classify workspace (k_pad_rows) and only
+// the train row is staged, which halves the shared memory per group (16 warps/SM instead of 8).
 #include <cstdlib>
 
 #include "launchers.cuh"

@@ -4,8 +4,11 @@
 // (line 1), n_bands = min(floor(L/2), V) (line 2, reading C10), the left band L_i and the right
 // band R_{L-i+1} minima for i = 2..n_bands (lines 3-11; the right band is the left band of the
 // reversed series, reading C9), then the LB_Keogh bridge (lines 13-15) over columns
-// n_bands+1..L-n_bands.  The line-12 abort is not taken: every pair's bound is produced
-// (north_star "over all query x train pairs"); pruning happens against the best-so-far later.
+// n_bands+1..L-n_bands.  One stage: every pair's full bound is produced (north_star "over all
+// query x train pairs"); pruning happens against the best-so-far later.  Two stages (large
+// inputs, lb_sparse.cu): this kernel in no-bridge mode is stage A -- the line-12 abort is then
+// taken against the first seed's best-so-far by the column lists, and the bridge runs only for
+// the pairs they keep.
 // LB_Kim is the sum variant "without repetitions" (reading C7).
 //
 // B200 design: the bridge is the O(L) part.  A CTA computes a 64-query x
