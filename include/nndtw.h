@@ -135,6 +135,11 @@ NNDTW_API int nndtw_series_stats(const float *x, int64_t n, int32_t L, nndtw_kim
 /* flags & NNDTW_LB_KEOGH: LB_Keogh (m = L, reading C6) over all L columns in place of
  * LB_Enhanced -- the paper's comparison bound (Fig. 9 normalises by it). */
 #define NNDTW_LB_KEOGH 2u
+/* flags & NNDTW_LB_PARTIAL: Algorithm 1 up to its line-12 test only -- the boundary terms and the
+ * bands (lines 1-11), no LB_Keogh bridge (max with LB_Kim under WITH_KIM): the value
+ * the two-stage S2 compares with the best-so-far before it computes the bridge.  A lower bound of
+ * the full value (every bridge term is >= 0).  Not combinable with NNDTW_LB_KEOGH. */
+#define NNDTW_LB_PARTIAL 4u
 NNDTW_API int nndtw_lb_enhanced(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
                       const float *upper, const float *lower, const nndtw_kim *tkim,
                       int64_t nt, int32_t L, int32_t w, int32_t v, uint32_t flags, float *lb,

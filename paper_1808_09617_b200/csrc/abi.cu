@@ -587,8 +587,11 @@ int nndtw_lb_enhanced(const float *q, int64_t nq, const nndtw_kim *qkim, const f
     bool kim = (flags & NNDTW_LB_WITH_KIM) != 0;
     if (nq > 0 && nt > 0 && (!q || !t || !upper || !lower || !lb || (kim && (!qkim || !tkim))))
         return fail(NNDTW_E_ARG, "null pointer argument");
+    const int partial = (flags & NNDTW_LB_PARTIAL) ? 1 : 0;
+    if (partial && (flags & NNDTW_LB_KEOGH))
+        return fail(NNDTW_E_ARG, "NNDTW_LB_PARTIAL cannot be combined with NNDTW_LB_KEOGH");
     if (launch_lb(q, nq, qkim, t, upper, lower, tkim, nt, L, w, v, kim ? 1 : 0, -1, lb, ldlb,
-                  nullptr, (cudaStream_t)stream, (flags & NNDTW_LB_KEOGH) ? 1 : 0))
+                  nullptr, (cudaStream_t)stream, (flags & NNDTW_LB_KEOGH) ? 1 : 0, 0, partial))
         return fail(NNDTW_E_ARG, "too many train series for one launch");
     return cuda_fail("nndtw_lb_enhanced");
 }

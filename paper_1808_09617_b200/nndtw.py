@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("NNDTW_LIB") or os.path.join(
     _HERE, "libnndtw_debug.so" if os.environ.get("NNDTW_DEBUG") == "1" else "libnndtw.so")
 
 NNDTW_LB_WITH_KIM = 1
+NNDTW_LB_PARTIAL = 4
 NNDTW_LB_KEOGH = 2
 NNDTW_CLASSIFY_EXACT = 1
 NNDTW_CLASSIFY_BOUND_KEOGH = 2
@@ -177,8 +178,9 @@ def series_stats(x: torch.Tensor, stream=None) -> torch.Tensor:
 
 
 def lb_enhanced(q, t, U, Lo, w: int, v: int, with_kim: bool = False, qkim=None, tkim=None,
-                keogh: bool = False, stream=None) -> torch.Tensor:
-    """S2: cascade bound matrix [nq][nt] (Eq. 7 / Algorithm 1; max with LB_Kim if asked)."""
+                keogh: bool = False, stream=None, partial: bool = False) -> torch.Tensor:
+    """S2: cascade bound matrix [nq][nt] (Eq. 7 / Algorithm 1; max with LB_Kim if asked;
+    partial: Algorithm 1 up to its line-12 test -- boundary terms and bands, no bridge)."""
     _series(q, "q"); _series(t, "t"); _series(U, "U"); _series(Lo, "Lo")
     nq, L = q.shape
     nt = t.shape[0]
@@ -190,7 +192,8 @@ def lb_enhanced(q, t, U, Lo, w: int, v: int, with_kim: bool = False, qkim=None, 
     _check(load().nndtw_lb_enhanced(_ptr(q), nq, _ptr(qkim), _ptr(t), _ptr(U), _ptr(Lo),
                                     _ptr(tkim), nt, L, int(w), int(v),
                                     (NNDTW_LB_WITH_KIM if with_kim else 0) |
-                                    (NNDTW_LB_KEOGH if keogh else 0), _ptr(out), nt,
+                                    (NNDTW_LB_KEOGH if keogh else 0) |
+                                    (NNDTW_LB_PARTIAL if partial else 0), _ptr(out), nt,
                                     _stream(stream)), "nndtw_lb_enhanced")
     return out
 

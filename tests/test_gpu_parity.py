@@ -115,6 +115,33 @@ def test_lb_enhanced_parity(dev, oracle_lib, L, w, V):
             assert abs(lbk[i, j] - refk) <= REL * refk + 1e-30, (i, j, lbk[i, j], refk)
 
 
+@pytest.mark.parametrize("L,w,V", [(2, 1, 5), (9, 2, 3), (64, 6, 5), (300, 30, 16),
+                                   (512, 103, 5), (257, 0, 4), (128, 127, 40)])
+def test_lb_enhanced_partial_parity(dev, oracle_lib, L, w, V):
+    """NNDTW_LB_PARTIAL (stage A of the two-stage S2): Algorithm 1 up to its line-12 test.  The
+    oracle's value is its own Algorithm 1 with an envelope of (+inf, -inf) -- every LB_Keogh
+    bridge term (lines 13-15) is then zero -- and it must not exceed the full bound."""
+    from paper_1808_09617_b200 import nndtw
+    rng = np.random.default_rng(L * 11 + w)
+    Q = datagen.random_series(rng, 40, L, "walk")
+    Tn = datagen.random_series(rng, 90, L, "walk")
+    Tn[4] = Q[2]
+    qt, tt = T(Q, dev), T(Tn, dev)
+    U, Lo, kim = nndtw.envelopes(tt, w)
+    part = nndtw.lb_enhanced(qt, tt, U, Lo, w, V, partial=True).cpu().numpy()
+    partk = nndtw.lb_enhanced(qt, tt, U, Lo, w, V, with_kim=True, tkim=kim,
+                              partial=True).cpu().numpy()
+    full = nndtw.lb_enhanced(qt, tt, U, Lo, w, V).cpu().numpy()
+    inf_u = np.full(L, np.inf, dtype=np.float32)
+    for i in range(0, 40, 3):
+        for j in range(90):
+            ref, _ = oracle_lib.lb_enhanced(Q[i], Tn[j], inf_u, -inf_u, w, V)
+            refk = max(ref, oracle_lib.lb_kim_sum(Q[i], Tn[j]))
+            assert abs(part[i, j] - ref) <= REL * ref + 1e-30, (i, j, part[i, j], ref)
+            assert abs(partk[i, j] - refk) <= REL * refk + 1e-30, (i, j, partk[i, j], refk)
+    assert np.all(part <= full * (1 + REL) + 1e-30)
+
+
 # ---------------------------------------------------------------- S4 DTW
 @pytest.mark.parametrize("L", [2, 3, 5, 17, 64, 128, 256, 300, 512])
 def test_dtw_batch_parity(dev, oracle_lib, L):
