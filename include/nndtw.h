@@ -187,6 +187,19 @@ NNDTW_API int nndtw_lb_new(const float *q, int64_t nq, const float *t, int64_t n
                            int32_t w, float *lb, int64_t ldlb, void *stream);
 
 /*
+ * Euclidean-nearest candidate of every query (the paper's candidate order; the ED is
+ * DTW_0): key[i] = min over j of ((bits of f32 ED(q_i, t_j)) << 32 | j), ED squared,
+ * computed from bf16-rounded series with fp32 accumulation on the tensor cores (tcgen05), so the
+ * chosen j is nearest up to that rounding -- it serves as a seed (any candidate's exact DTW is a
+ * valid best-so-far), not as a distance.  key must hold 0xFFFF...FF on entry (it is min-ed into).
+ * q: [nq][L], t: [nt][L] device fp32; 1 <= L <= 512 (else NNDTW_E_LENGTH); ws: device scratch of
+ * nndtw_ed_seed_workspace_bytes(nq, nt, L) bytes.
+ */
+NNDTW_API size_t nndtw_ed_seed_workspace_bytes(int64_t nq, int64_t nt, int32_t L);
+NNDTW_API int nndtw_ed_seed(const float *q, int64_t nq, const float *t, int64_t nt, int32_t L,
+                            void *ws, size_t ws_bytes, uint64_t *key, void *stream);
+
+/*
  * Tightness (reading C20): over the n pairs with 0 < dtw[p] <
  * +inf, accumulate sum[0] += sum of sqrt(lb[p] / dtw[p]) (fp64), count[0] += #pairs and
  * max_bits[0] = max(max_bits[0], float bits of the largest ratio).  lb and dtw are squared

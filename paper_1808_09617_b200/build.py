@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 DEBUG = os.environ.get("NNDTW_DEBUG", "0") == "1"
 LIB = os.path.join(HERE, "libnndtw_debug.so" if DEBUG else "libnndtw.so")
 SOURCES = ["abi.cu", "envelopes.cu", "lb.cu", "dtw_band.cu", "dtw_strip.cu", "search.cu",
-           "bounds_next.cu", "bounds_improved.cu", "lb_sparse.cu"]
+           "bounds_next.cu", "bounds_improved.cu", "lb_sparse.cu", "ed_seed.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-cudart", "static",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",

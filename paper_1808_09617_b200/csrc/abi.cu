@@ -675,6 +675,25 @@ int nndtw_lb_new(const float *q, int64_t nq, const float *t, int64_t nt, int32_t
     return cuda_fail("nndtw_lb_new");
 }
 
+size_t nndtw_ed_seed_workspace_bytes(int64_t nq, int64_t nt, int32_t L) {
+    if (nq < 0 || nt < 0 || L < 1) return 0;
+    return ed_seed_scratch_bytes(nq, nt, L);
+}
+
+int nndtw_ed_seed(const float *q, int64_t nq, const float *t, int64_t nt, int32_t L, void *ws,
+                  size_t ws_bytes, uint64_t *key, void *stream) {
+    int sms, rc;
+    if ((rc = device_sms(&sms))) return rc;
+    if (nq < 0 || nt < 0) return fail(NNDTW_E_ARG, "negative count");
+    if (L < 1) return fail(NNDTW_E_LENGTH, "L must be >= 1");
+    if (!ed_seed_supported(L)) return fail(NNDTW_E_LENGTH, "nndtw_ed_seed supports L <= 512");
+    if (nq > 0 && nt > 0 && (!q || !t || !key || !ws)) return fail(NNDTW_E_ARG, "null pointer argument");
+    if (ws_bytes < ed_seed_scratch_bytes(nq, nt, L)) return fail(NNDTW_E_WORKSPACE, "ws too small");
+    if (launch_ed_seed(q, nq, t, nt, L, ws, (unsigned long long *)key, sms, (cudaStream_t)stream))
+        return fail(NNDTW_E_ARG, "ed seed launch failed");
+    return cuda_fail("nndtw_ed_seed");
+}
+
 int nndtw_tightness(const float *lb, const float *dtw, int64_t n, double *sum, uint64_t *count,
                     uint32_t *max_bits, void *stream) {
     int sms, rc;

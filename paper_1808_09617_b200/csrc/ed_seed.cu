@@ -1,0 +1,269 @@
+// ed_seed.cu -- a first seed for every query from the paper's own candidate order: the train
+// series nearest in Euclidean distance (P:567-570 -- the sequential search visits candidates in
+// ED order; DTW_0 = ED).  Any candidate's exact DTW is a valid best-so-far, so the seed
+// only has to be good, not exact: its DTW on config 2 is 1.34x the final NN distance on average,
+// against 2.73x for the argmin of the partial cascade value (tools/seed_study.py), which shortens
+// the two-stage S2's lists and starts the survivor round closer to its end point.
+//
+// All-pairs ED is a dense contraction: ED(q, t) = |q|^2 + |t|^2 - 2 q.t, so the work is the GEMM
+// Q T^T (nq x nt x L) on the 5th-generation tensor cores, in bf16 with fp32 accumulation, and
+// the per-query argmin is fused into the epilogue -- the nq x nt scores never reach memory.
+//
+// B200 design (k_ed_argmin).  A CTA owns 128 queries (UMMA M = 128): their bf16 rows, K-major, sit
+// in shared memory for the whole unit (L <= 512: 8 K-chunks x 16 KB, the 128-byte-swizzled
+// canonical layout), and it sweeps a range of train tiles of 256 series (UMMA N = 256): per tile
+// the K-chunks of the train rows stream through a two-stage shared-memory ring (cp.async), one
+// elected thread issues tcgen05.mma (kind::f16, 4 x K = 16 per chunk) into a 128 x 256 fp32
+// accumulator in TMEM and commits each chunk to the stage's mbarrier (which frees the stage),
+// and after the tile the four warps read their 32 TMEM lanes (tcgen05.ld 32x32b) and update a
+// per-row running argmin of |t|^2 - 2 q.t.  One atomicMin per query and unit at the end.
+#include "launchers.cuh"
+
+#include <cuda_bf16.h>
+
+namespace nndtw {
+
+constexpr int ED_M = 128, ED_N = 256, ED_KC = 64;  // bf16 per K-chunk row: 128 bytes
+constexpr int ED_A_CHUNK = ED_M * ED_KC * 2;       // 16 KB
+constexpr int ED_B_CHUNK = ED_N * ED_KC * 2;       // 32 KB
+constexpr int ED_MAX_L = 512;                      // A resident: L <= 512 (128 KB)
+
+// rows to bf16, zero-padded to Lk columns; |x|^2 in fp32 from the fp32 values
+__global__ void k_ed_prep(const float *__restrict__ x, int64_t n, int L, int Lk,
+                          __nv_bfloat16 *__restrict__ xb, float *__restrict__ norm) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = wid; r < n; r += nw) {
+        float s = 0.0f;
+        for (int c = lane; c < Lk; c += 32) {
+            const float v = c < L ? x[r * L + c] : 0.0f;
+            s = fmaf(v, v, s);
+            xb[r * Lk + c] = __float2bfloat16_rn(v);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) norm[r] = s;
+    }
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// K-major, 128-byte-swizzled canonical UMMA operand: rows of 128 bytes, 8-row groups 1024 bytes
+// apart (SBO), 16-byte chunk c of row r stored at chunk c ^ (r % 8)
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFFu);   // start address (16-byte units)
+    d |= (uint64_t)1 << 16;                   // leading byte offset (unused when swizzled)
+    d |= (uint64_t)(1024 >> 4) << 32;         // stride byte offset: 8-row groups
+    d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                   // layout: SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(128, 1)
+    k_ed_argmin(const __nv_bfloat16 *__restrict__ qb, const __nv_bfloat16 *__restrict__ tb,
+                const float *__restrict__ qn, const float *__restrict__ tn, int64_t nq,
+                int64_t nt, int Lk, int nsplit, unsigned long long *key) {
+    extern __shared__ __align__(1024) uint8_t ed_smem[];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+    const int nkc = Lk / ED_KC;
+    // 1024-byte aligned base (the 128-byte swizzle pattern repeats every 1024 bytes)
+    uint8_t *smA = ed_smem + ((1024u - (smem_u32(ed_smem) & 1023u)) & 1023u);
+    uint8_t *smB = smA + nkc * ED_A_CHUNK;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smB + 2 * ED_B_CHUNK);
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 2);
+    const uint32_t bar0 = smem_u32(&bars[0]), bar1 = smem_u32(&bars[1]);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tslot)),
+                     "n"(ED_N)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t taddr = *tslot;
+
+    // instruction descriptor: D f32, A/B bf16, both K-major, N = 256, M = 128
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(ED_N >> 3) << 17) |
+                           ((uint32_t)(ED_M >> 4) << 24);
+    const uint32_t aA = smem_u32(smA), aB = smem_u32(smB);
+    uint32_t phase[2] = {0u, 0u};
+    bool pending[2] = {false, false};
+    int stage = 0;
+    auto consume = [&](int s) {  // wait for the stage's outstanding MMA commit (all threads)
+        if (pending[s]) {
+            mbar_wait(s ? bar1 : bar0, phase[s]);
+            phase[s] ^= 1u;
+            pending[s] = false;
+        }
+    };
+
+    const int64_t nmb = (nq + ED_M - 1) / ED_M;
+    const int64_t ntile = (nt + ED_N - 1) / ED_N;
+    const int64_t units = nmb * nsplit;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int64_t m0 = (u / nsplit) * ED_M;
+        const int sp = (int)(u % nsplit);
+        const int64_t t_beg = ntile * sp / nsplit, t_end = ntile * (sp + 1) / nsplit;
+        if (t_beg >= t_end) continue;
+        // the unit's 128 query rows, all K-chunks (no MMA is in flight: the last tile waited)
+        for (int e = tid; e < ED_M * nkc * 8; e += 128) {
+            const int r = e / (nkc * 8), rem = e - r * (nkc * 8), kc = rem >> 3, c = rem & 7;
+            uint8_t *dst = smA + kc * ED_A_CHUNK + (r >> 3) * 1024 + (r & 7) * 128 +
+                           ((c ^ (r & 7)) << 4);
+            if (m0 + r < nq)
+                cp_async16(reinterpret_cast<float *>(dst),
+                           reinterpret_cast<const float *>(qb + (m0 + r) * Lk + kc * ED_KC + c * 8));
+            else
+                *reinterpret_cast<uint4 *>(dst) = make_uint4(0u, 0u, 0u, 0u);
+        }
+        cp_async_commit();
+        const int64_t row = m0 + 32 * warp + lane;  // this thread's query (its TMEM lane)
+        const float qrow = row < nq ? qn[row] : 0.0f;
+        float bestv = kInf;
+        int64_t besti = -1;
+        for (int64_t tt = t_beg; tt < t_end; ++tt) {
+            const int64_t n0 = tt * ED_N;
+            for (int kc = 0; kc < nkc; ++kc) {
+                const int s = stage;
+                consume(s);  // the MMA that last read this stage is done
+                uint8_t *sb = smB + s * ED_B_CHUNK;
+                for (int e = tid; e < ED_N * 8; e += 128) {
+                    const int r = e >> 3, c = e & 7;
+                    uint8_t *dst = sb + (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
+                    if (n0 + r < nt)
+                        cp_async16(reinterpret_cast<float *>(dst),
+                                   reinterpret_cast<const float *>(tb + (n0 + r) * Lk +
+                                                                   kc * ED_KC + c * 8));
+                    else
+                        *reinterpret_cast<uint4 *>(dst) = make_uint4(0u, 0u, 0u, 0u);
+                }
+                cp_async_commit();
+                cp_async_wait_all();
+                // generic-proxy writes (cp.async, st.shared) -> visible to the tensor cores
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncthreads();
+                if (tid == 0) {
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                    for (int k = 0; k < ED_KC / 16; ++k) {
+                        const uint64_t da = umma_desc_sw128(aA + kc * ED_A_CHUNK + k * 32);
+                        const uint64_t db = umma_desc_sw128(aB + s * ED_B_CHUNK + k * 32);
+                        const uint32_t acc = (kc | k) != 0 ? 1u : 0u;
+                        asm volatile(
+                            "{\n\t.reg .pred p;\n\t"
+                            "setp.ne.b32 p, %4, 0;\n\t"
+                            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(
+                                taddr),
+                            "l"(da), "l"(db), "r"(idesc), "r"(acc)
+                            : "memory");
+                    }
+                    asm volatile(
+                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 "
+                        "[%0];" ::"r"(s ? bar1 : bar0)
+                        : "memory");
+                }
+                pending[s] = true;
+                stage ^= 1;
+            }
+            // the tile's accumulator is complete once the last chunk's commit has arrived (MMAs
+            // complete in issue order)
+            consume(stage ^ 1);
+            consume(stage);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+            for (int cb = 0; cb < ED_N / 16; ++cb) {
+                uint32_t v[16];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, "
+                    "%9, %10, %11, %12, %13, %14, %15}, [%16];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                      "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                      "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                    : "r"(taddr + ((uint32_t)(32 * warp) << 16) + (uint32_t)(cb * 16)));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int64_t n = n0 + cb * 16 + j;
+                    if (n < nt) {
+                        const float sc = fmaf(-2.0f, __uint_as_float(v[j]), qrow + tn[n]);
+                        if (sc < bestv) {
+                            bestv = sc;
+                            besti = n;
+                        }
+                    }
+                }
+            }
+            // every warp's TMEM reads are done before the next tile's MMAs overwrite it
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncthreads();
+        }
+        if (row < nq && besti >= 0)
+            atomicMin(key + row, make_key(fmaxf(bestv, 0.0f), (unsigned)besti));
+    }
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr),
+                     "n"(ED_N)
+                     : "memory");
+}
+
+int ed_seed_supported(int L) { return L >= 1 && L <= ED_MAX_L; }
+
+size_t ed_seed_scratch_bytes(int64_t nq, int64_t nt, int L) {
+    const int64_t Lk = (L + ED_KC - 1) / ED_KC * ED_KC;
+    return (size_t)(nq + nt) * (size_t)Lk * 2 + (size_t)(nq + nt) * 4 + 1024;
+}
+
+// q [nq][L], t [nt][L] fp32 -> key[q] = min over n of ((ED(q, t_n) as f32 bits) << 32 | n),
+// computed in bf16 / fp32 on the tensor cores (key must hold kNone on entry).  scratch: bf16 copies
+// and norms, ed_seed_scratch_bytes.
+int launch_ed_seed(const float *q, int64_t nq, const float *t, int64_t nt, int L, void *scratch,
+                   unsigned long long *key, int num_sms, cudaStream_t st) {
+    if (nq == 0 || nt == 0) return 0;
+    if (!ed_seed_supported(L)) return -1;
+    const int Lk = (L + ED_KC - 1) / ED_KC * ED_KC;
+    __nv_bfloat16 *qb = reinterpret_cast<__nv_bfloat16 *>(scratch);
+    __nv_bfloat16 *tb = qb + nq * Lk;
+    float *qn = reinterpret_cast<float *>(tb + nt * Lk);
+    float *tn = qn + nq;
+    k_ed_prep<<<num_sms * 8, 256, 0, st>>>(q, nq, L, Lk, qb, qn);
+    k_ed_prep<<<num_sms * 8, 256, 0, st>>>(t, nt, L, Lk, tb, tn);
+    const int nkc = Lk / ED_KC;
+    const size_t smem = (size_t)nkc * ED_A_CHUNK + 2 * ED_B_CHUNK + 64 + 1024;
+    cudaFuncSetAttribute(k_ed_argmin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t nmb = (nq + ED_M - 1) / ED_M;
+    const int64_t ntile = (nt + ED_N - 1) / ED_N;
+    // about four units per SM (balance), each long enough to amortise its A load
+    int nsplit = (int)((4 * (int64_t)num_sms + nmb - 1) / nmb);
+    if (nsplit > ntile) nsplit = (int)ntile;
+    if (nsplit < 1) nsplit = 1;
+    const int64_t units = nmb * nsplit;
+    const int grid = (int)(units < num_sms ? units : num_sms);
+    k_ed_argmin<<<grid, 128, smem, st>>>(qb, tb, qn, tn, nq, nt, Lk, nsplit, key);
+    count_launch(3, __func__);
+    return 0;
+}
+
+}  // namespace nndtw

@@ -113,6 +113,12 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
 // seglen for any window: padl + L + padr <= L + w + R + 48)
 inline int64_t band_apad_row_floats(int L) { return 2 * (int64_t)L + 128; }
 
+// ed_seed.cu: per-query argmin of the Euclidean distance over all train series (tensor cores)
+int ed_seed_supported(int L);
+size_t ed_seed_scratch_bytes(int64_t nq, int64_t nt, int L);
+int launch_ed_seed(const float *q, int64_t nq, const float *t, int64_t nt, int L, void *scratch,
+                   unsigned long long *key, int num_sms, cudaStream_t st);
+
 int dtw_kernel_kind(int L, int w);  // 0 = k_dtw_w0, 1 = k_dtw_band, 2 = k_dtw_strip
 int strip_rows_per_lane(int L);
 int launch_dtw_strip(const float *A, const float *B, const Item *items,

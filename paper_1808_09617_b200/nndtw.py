@@ -93,6 +93,8 @@ _SIGS = {
     "nndtw_lb_enhanced_improved": (C.c_int, [_P, _I64, _P, _P, _P, _I64, _I32, _I32, _I32, _P,
                                              _I64, _P]),
     "nndtw_lb_new": (C.c_int, [_P, _I64, _P, _I64, _I32, _I32, _P, _I64, _P]),
+    "nndtw_ed_seed_workspace_bytes": (C.c_size_t, [_I64, _I64, _I32]),
+    "nndtw_ed_seed": (C.c_int, [_P, _I64, _P, _I64, _I32, _P, C.c_size_t, _P, _P]),
     "nndtw_tightness": (C.c_int, [_P, _P, _I64, _P, _P, _P, _P]),
     "nndtw_dtw_batch": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P]),
     "nndtw_classify_workspace_bytes": (C.c_size_t, [_I64, _I64, _I32, _I32]),
@@ -249,6 +251,24 @@ def lb_new(q, t, w: int, stream=None) -> torch.Tensor:
     _check(load().nndtw_lb_new(_ptr(q), nq, _ptr(t), nt, L, int(w), _ptr(out), nt,
                                _stream(stream)), "nndtw_lb_new")
     return out
+
+
+def ed_seed(q, t, stream=None):
+    """Euclidean-nearest train index of every query (int64 [nq]) and its squared ED as computed
+    (bf16 inputs, fp32 accumulation on the tensor cores) -- the paper's candidate order (P:569);
+    a seed, not a distance.  L <= 512."""
+    _series(q, "q"); _series(t, "t")
+    nq, L = q.shape
+    nt = t.shape[0]
+    lib = load()
+    ws = torch.empty(lib.nndtw_ed_seed_workspace_bytes(nq, nt, L), dtype=torch.uint8,
+                     device=q.device)
+    key = torch.full((nq,), -1, dtype=torch.int64, device=q.device)
+    _check(lib.nndtw_ed_seed(_ptr(q), nq, _ptr(t), nt, L, _ptr(ws), ws.numel(), _ptr(key),
+                             _stream(stream)), "nndtw_ed_seed")
+    idx = key & 0xFFFFFFFF
+    dist = (key >> 32).to(torch.int32).view(torch.float32)
+    return idx, dist
 
 
 def tightness(lb: torch.Tensor, d: torch.Tensor, stream=None):
