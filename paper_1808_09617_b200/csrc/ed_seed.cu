@@ -27,23 +27,38 @@ constexpr int ED_M = 128, ED_N = 256, ED_KC = 64;  // bf16 per K-chunk row: 128 
 constexpr int ED_A_CHUNK = ED_M * ED_KC * 2;       // 16 KB
 constexpr int ED_B_CHUNK = ED_N * ED_KC * 2;       // 32 KB
 constexpr int ED_MAX_L = 512;                      // A resident: L <= 512 (128 KB)
+constexpr int ED_STAGES = 3;                       // B ring: 3 x 32 KB (with A: 224 KB)
 
-// rows to bf16, zero-padded to Lk columns; |x|^2 in fp32 from the fp32 values
-__global__ void k_ed_prep(const float *__restrict__ x, int64_t n, int L, int Lk,
-                          __nv_bfloat16 *__restrict__ xb, float *__restrict__ norm) {
+__host__ __device__ inline int ed_lk(int L) { return (L + ED_KC - 1) / ED_KC * ED_KC; }
+
+// Rows to bf16 in the operand image the tensor cores read: per tile of `rows` rows and K-chunk of
+// 64 columns a contiguous block, row r at (r / 8) * 1024 + (r % 8) * 128 bytes, its 16-byte chunk c
+// at c ^ (r % 8) (the 128-byte swizzle), so every block is one bulk copy into shared memory.
+// Rows past n and columns past L are zero.  |x|^2 in fp32 from the fp32 values.
+__global__ void k_ed_prep(const float *__restrict__ x, int64_t n, int L, int Lk, int rows,
+                          __nv_bfloat16 *__restrict__ img, float *__restrict__ norm) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = wid; r < n; r += nw) {
+    const int nkc = Lk / ED_KC;
+    const int64_t nrows = (n + rows - 1) / rows * rows;
+    for (int64_t r = wid; r < nrows; r += nw) {
+        const int64_t tile = r / rows;
+        const int rr = (int)(r - tile * rows);
+        uint8_t *base = reinterpret_cast<uint8_t *>(img) + tile * (int64_t)nkc * rows * 128 +
+                        (rr >> 3) * 1024 + (rr & 7) * 128;
         float s = 0.0f;
         for (int c = lane; c < Lk; c += 32) {
-            const float v = c < L ? x[r * L + c] : 0.0f;
+            const float v = (r < n && c < L) ? x[r * L + c] : 0.0f;
             s = fmaf(v, v, s);
-            xb[r * Lk + c] = __float2bfloat16_rn(v);
+            const int kc = c / ED_KC, kk = c % ED_KC, ch = kk >> 3, e = kk & 7;
+            __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(
+                base + (int64_t)kc * rows * 128 + ((ch ^ (rr & 7)) << 4) + e * 2);
+            *dst = __float2bfloat16_rn(v);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) norm[r] = s;
+        if (lane == 0 && r < n) norm[r] = s;
     }
 }
 
@@ -63,6 +78,9 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t addr) {
     return d;
 }
 
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
@@ -72,9 +90,32 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// one bulk copy global -> shared, completing `bytes` on the mbarrier (armed by expect_tx)
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes,
+                                          uint32_t bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+        : "memory");
+}
 
-__global__ void __launch_bounds__(128, 1)
-    k_ed_argmin(const __nv_bfloat16 *__restrict__ qb, const __nv_bfloat16 *__restrict__ tb,
+// Warp-specialised: warp 4 (one elected lane) loads and issues the MMAs, warps 0-3 run the
+// epilogue on their TMEM lane quarters.  Two 256-column accumulators (all 512 TMEM columns): the
+// epilogue of one tile overlaps the MMAs of the next.  Work unit = (128-query block, range of
+// train tiles); the query block's operand image (nkc x 16 KB) is one bulk copy per unit.
+__global__ void __launch_bounds__(160, 1)
+    k_ed_argmin(const __nv_bfloat16 *__restrict__ qimg, const __nv_bfloat16 *__restrict__ timg,
                 const float *__restrict__ qn, const float *__restrict__ tn, int64_t nq,
                 int64_t nt, int Lk, int nsplit, unsigned long long *key) {
     extern __shared__ __align__(1024) uint8_t ed_smem[];
@@ -84,18 +125,28 @@ __global__ void __launch_bounds__(128, 1)
     // 1024-byte aligned base (the 128-byte swizzle pattern repeats every 1024 bytes)
     uint8_t *smA = ed_smem + ((1024u - (smem_u32(ed_smem) & 1023u)) & 1023u);
     uint8_t *smB = smA + nkc * ED_A_CHUNK;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smB + 2 * ED_B_CHUNK);
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 2);
-    const uint32_t bar0 = smem_u32(&bars[0]), bar1 = smem_u32(&bars[1]);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smB + ED_STAGES * ED_B_CHUNK);
+    // bars: full[3], empty[3], afull[2], aempty[2], abar
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 11);
+    const uint32_t b_full = smem_u32(bars), b_empty = b_full + 8 * ED_STAGES;
+    const uint32_t b_afull = b_empty + 8 * ED_STAGES, b_aempty = b_afull + 16;
+    const uint32_t b_a = b_aempty + 16;
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1) : "memory");
+        for (int i = 0; i < ED_STAGES; ++i) {
+            mbar_init(b_full + 8 * i, 1);
+            mbar_init(b_empty + 8 * i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(b_afull + 8 * i, 1);
+            mbar_init(b_aempty + 8 * i, 128);
+        }
+        mbar_init(b_a, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tslot)),
-                     "n"(ED_N)
+                     "n"(2 * ED_N)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -104,154 +155,176 @@ __global__ void __launch_bounds__(128, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t taddr = *tslot;
 
-    // instruction descriptor: D f32, A/B bf16, both K-major, N = 256, M = 128
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(ED_N >> 3) << 17) |
-                           ((uint32_t)(ED_M >> 4) << 24);
-    const uint32_t aA = smem_u32(smA), aB = smem_u32(smB);
-    uint32_t phase[2] = {0u, 0u};
-    bool pending[2] = {false, false};
-    int stage = 0;
-    auto consume = [&](int s) {  // wait for the stage's outstanding MMA commit (all threads)
-        if (pending[s]) {
-            mbar_wait(s ? bar1 : bar0, phase[s]);
-            phase[s] ^= 1u;
-            pending[s] = false;
-        }
-    };
-
     const int64_t nmb = (nq + ED_M - 1) / ED_M;
     const int64_t ntile = (nt + ED_N - 1) / ED_N;
     const int64_t units = nmb * nsplit;
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const int64_t m0 = (u / nsplit) * ED_M;
-        const int sp = (int)(u % nsplit);
-        const int64_t t_beg = ntile * sp / nsplit, t_end = ntile * (sp + 1) / nsplit;
-        if (t_beg >= t_end) continue;
-        // the unit's 128 query rows, all K-chunks (no MMA is in flight: the last tile waited)
-        for (int e = tid; e < ED_M * nkc * 8; e += 128) {
-            const int r = e / (nkc * 8), rem = e - r * (nkc * 8), kc = rem >> 3, c = rem & 7;
-            uint8_t *dst = smA + kc * ED_A_CHUNK + (r >> 3) * 1024 + (r & 7) * 128 +
-                           ((c ^ (r & 7)) << 4);
-            if (m0 + r < nq)
-                cp_async16(reinterpret_cast<float *>(dst),
-                           reinterpret_cast<const float *>(qb + (m0 + r) * Lk + kc * ED_KC + c * 8));
-            else
-                *reinterpret_cast<uint4 *>(dst) = make_uint4(0u, 0u, 0u, 0u);
-        }
-        cp_async_commit();
-        const int64_t row = m0 + 32 * warp + lane;  // this thread's query (its TMEM lane)
-        const float qrow = row < nq ? qn[row] : 0.0f;
-        float bestv = kInf;
-        int64_t besti = -1;
-        for (int64_t tt = t_beg; tt < t_end; ++tt) {
-            const int64_t n0 = tt * ED_N;
-            for (int kc = 0; kc < nkc; ++kc) {
-                const int s = stage;
-                consume(s);  // the MMA that last read this stage is done
-                uint8_t *sb = smB + s * ED_B_CHUNK;
-                for (int e = tid; e < ED_N * 8; e += 128) {
-                    const int r = e >> 3, c = e & 7;
-                    uint8_t *dst = sb + (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
-                    if (n0 + r < nt)
-                        cp_async16(reinterpret_cast<float *>(dst),
-                                   reinterpret_cast<const float *>(tb + (n0 + r) * Lk +
-                                                                   kc * ED_KC + c * 8));
-                    else
-                        *reinterpret_cast<uint4 *>(dst) = make_uint4(0u, 0u, 0u, 0u);
+
+    if (warp == 4) {
+        if (lane == 0) {
+            // ---- producer + MMA issuer -------------------------------------------------------
+            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
+                                   ((uint32_t)(ED_N >> 3) << 17) | ((uint32_t)(ED_M >> 4) << 24);
+            const uint32_t aA = smem_u32(smA), aB = smem_u32(smB);
+            uint32_t ph_full[ED_STAGES] = {0u, 0u, 0u}, ph_empty[ED_STAGES] = {0u, 0u, 0u};
+            bool used[ED_STAGES] = {false, false, false};
+            uint32_t ph_aempty[2] = {0u, 0u}, ph_a = 0u;
+            bool aused[2] = {false, false};
+            int buf = 0;
+            uint64_t gload = 0, gcons = 0;  // chunk counters (load / consume)
+            bool a_pending = false;
+            for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+                const int64_t mb = u / nsplit;
+                const int sp = (int)(u % nsplit);
+                const int64_t t_beg = ntile * sp / nsplit, t_end = ntile * (sp + 1) / nsplit;
+                if (t_beg >= t_end) continue;
+                // A: every MMA of the previous unit must be done reading it
+                if (a_pending) {
+                    for (int st = 0; st < ED_STAGES; ++st)
+                        if (used[st]) {
+                            mbar_wait(b_empty + 8 * st, ph_empty[st]);
+                            ph_empty[st] ^= 1u;
+                            used[st] = false;
+                        }
                 }
-                cp_async_commit();
-                cp_async_wait_all();
-                // generic-proxy writes (cp.async, st.shared) -> visible to the tensor cores
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncthreads();
-                if (tid == 0) {
+                bulk_load(aA, qimg + mb * (int64_t)nkc * ED_M * ED_KC,
+                          (uint32_t)(nkc * ED_A_CHUNK), b_a);
+                a_pending = true;
+                const int64_t nchunks = (t_end - t_beg) * nkc;
+                auto load_chunk = [&](int64_t c) {  // chunk c of this unit -> its ring stage
+                    const int st = (int)(gload % ED_STAGES);
+                    if (used[st]) {  // the MMAs that read this stage before are done
+                        mbar_wait(b_empty + 8 * st, ph_empty[st]);
+                        ph_empty[st] ^= 1u;
+                    }
+                    const int64_t tile = t_beg + c / nkc;
+                    const int kc = (int)(c % nkc);
+                    bulk_load(aB + st * ED_B_CHUNK,
+                              timg + (tile * nkc + kc) * (int64_t)ED_N * ED_KC,
+                              (uint32_t)ED_B_CHUNK, b_full + 8 * st);
+                    used[st] = true;
+                    ++gload;
+                };
+                const int64_t pre = nchunks < ED_STAGES - 1 ? nchunks : ED_STAGES - 1;
+                for (int64_t c = 0; c < pre; ++c) load_chunk(c);
+                mbar_wait(b_a, ph_a);
+                ph_a ^= 1u;
+                for (int64_t c = 0; c < nchunks; ++c) {
+                    const int st = (int)(gcons % ED_STAGES);
+                    const int kc = (int)(c % nkc);
+                    if (kc == 0 && aused[buf]) {  // the epilogue is done with this accumulator
+                        mbar_wait(b_aempty + 8 * buf, ph_aempty[buf]);
+                        ph_aempty[buf] ^= 1u;
+                    }
+                    mbar_wait(b_full + 8 * st, ph_full[st]);
+                    ph_full[st] ^= 1u;
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t dtm = taddr + (uint32_t)(buf * ED_N);
 #pragma unroll
                     for (int k = 0; k < ED_KC / 16; ++k) {
                         const uint64_t da = umma_desc_sw128(aA + kc * ED_A_CHUNK + k * 32);
-                        const uint64_t db = umma_desc_sw128(aB + s * ED_B_CHUNK + k * 32);
+                        const uint64_t db = umma_desc_sw128(aB + st * ED_B_CHUNK + k * 32);
                         const uint32_t acc = (kc | k) != 0 ? 1u : 0u;
                         asm volatile(
                             "{\n\t.reg .pred p;\n\t"
                             "setp.ne.b32 p, %4, 0;\n\t"
                             "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(
-                                taddr),
+                                dtm),
                             "l"(da), "l"(db), "r"(idesc), "r"(acc)
                             : "memory");
                     }
-                    asm volatile(
-                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 "
-                        "[%0];" ::"r"(s ? bar1 : bar0)
-                        : "memory");
+                    umma_commit(b_empty + 8 * st);  // frees the stage when these MMAs finish
+                    ++gcons;
+                    if (kc == nkc - 1) {            // tile complete -> its accumulator is ready
+                        umma_commit(b_afull + 8 * buf);
+                        aused[buf] = true;
+                        buf ^= 1;
+                    }
+                    if (c + ED_STAGES - 1 < nchunks) load_chunk(c + ED_STAGES - 1);
                 }
-                pending[s] = true;
-                stage ^= 1;
             }
-            // the tile's accumulator is complete once the last chunk's commit has arrived (MMAs
-            // complete in issue order)
-            consume(stage ^ 1);
-            consume(stage);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+    } else {
+        // ---- epilogue: warps 0-3, TMEM lanes 32w .. 32w+31 = this thread's query -------------
+        uint32_t ph_afull[2] = {0u, 0u};
+        int buf = 0;
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+            const int64_t mb = u / nsplit;
+            const int sp = (int)(u % nsplit);
+            const int64_t t_beg = ntile * sp / nsplit, t_end = ntile * (sp + 1) / nsplit;
+            if (t_beg >= t_end) continue;
+            const int64_t row = mb * ED_M + 32 * warp + lane;
+            const float qrow = row < nq ? qn[row] : 0.0f;
+            float bestv = kInf;
+            int64_t besti = -1;
+            for (int64_t tt = t_beg; tt < t_end; ++tt) {
+                mbar_wait(b_afull + 8 * buf, ph_afull[buf]);
+                ph_afull[buf] ^= 1u;
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const int64_t n0 = tt * ED_N;
 #pragma unroll 1
-            for (int cb = 0; cb < ED_N / 16; ++cb) {
-                uint32_t v[16];
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, "
-                    "%9, %10, %11, %12, %13, %14, %15}, [%16];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                      "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
-                      "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                    : "r"(taddr + ((uint32_t)(32 * warp) << 16) + (uint32_t)(cb * 16)));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                for (int cb = 0; cb < ED_N / 16; ++cb) {
+                    uint32_t v[16];
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, "
+                        "%8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                          "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]),
+                          "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                        : "r"(taddr + ((uint32_t)(32 * warp) << 16) +
+                              (uint32_t)(buf * ED_N + cb * 16)));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int64_t n = n0 + cb * 16 + j;
-                    if (n < nt) {
-                        const float sc = fmaf(-2.0f, __uint_as_float(v[j]), qrow + tn[n]);
-                        if (sc < bestv) {
-                            bestv = sc;
-                            besti = n;
+                    for (int j = 0; j < 16; ++j) {
+                        const int64_t n = n0 + cb * 16 + j;
+                        if (n < nt) {
+                            const float sc = fmaf(-2.0f, __uint_as_float(v[j]), qrow + tn[n]);
+                            if (sc < bestv) {
+                                bestv = sc;
+                                besti = n;
+                            }
                         }
                     }
                 }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(b_aempty + 8 * buf);  // this thread is done with the accumulator
+                buf ^= 1;
             }
-            // every warp's TMEM reads are done before the next tile's MMAs overwrite it
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncthreads();
+            if (row < nq && besti >= 0)
+                atomicMin(key + row, make_key(fmaxf(bestv, 0.0f), (unsigned)besti));
         }
-        if (row < nq && besti >= 0)
-            atomicMin(key + row, make_key(fmaxf(bestv, 0.0f), (unsigned)besti));
     }
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr),
-                     "n"(ED_N)
+                     "n"(2 * ED_N)
                      : "memory");
 }
 
 int ed_seed_supported(int L) { return L >= 1 && L <= ED_MAX_L; }
 
 size_t ed_seed_scratch_bytes(int64_t nq, int64_t nt, int L) {
-    const int64_t Lk = (L + ED_KC - 1) / ED_KC * ED_KC;
-    return (size_t)(nq + nt) * (size_t)Lk * 2 + (size_t)(nq + nt) * 4 + 1024;
+    const int64_t Lk = ed_lk(L);
+    const int64_t qrows = (nq + ED_M - 1) / ED_M * ED_M, trows = (nt + ED_N - 1) / ED_N * ED_N;
+    return (size_t)(qrows + trows) * (size_t)Lk * 2 + (size_t)(nq + nt) * 4 + 1024;
 }
 
 // q [nq][L], t [nt][L] fp32 -> key[q] = min over n of ((ED(q, t_n) as f32 bits) << 32 | n),
-// computed in bf16 / fp32 on the tensor cores (key must hold kNone on entry).  scratch: bf16 copies
-// and norms, ed_seed_scratch_bytes.
+// computed in bf16 / fp32 on the tensor cores (key must hold kNone on entry).  scratch: the bf16
+// operand images and norms, ed_seed_scratch_bytes.
 int launch_ed_seed(const float *q, int64_t nq, const float *t, int64_t nt, int L, void *scratch,
                    unsigned long long *key, int num_sms, cudaStream_t st) {
     if (nq == 0 || nt == 0) return 0;
     if (!ed_seed_supported(L)) return -1;
-    const int Lk = (L + ED_KC - 1) / ED_KC * ED_KC;
-    __nv_bfloat16 *qb = reinterpret_cast<__nv_bfloat16 *>(scratch);
-    __nv_bfloat16 *tb = qb + nq * Lk;
-    float *qn = reinterpret_cast<float *>(tb + nt * Lk);
+    const int Lk = ed_lk(L);
+    const int64_t qrows = (nq + ED_M - 1) / ED_M * ED_M, trows = (nt + ED_N - 1) / ED_N * ED_N;
+    __nv_bfloat16 *qimg = reinterpret_cast<__nv_bfloat16 *>(scratch);
+    __nv_bfloat16 *timg = qimg + qrows * Lk;
+    float *qn = reinterpret_cast<float *>(timg + trows * Lk);
     float *tn = qn + nq;
-    k_ed_prep<<<num_sms * 8, 256, 0, st>>>(q, nq, L, Lk, qb, qn);
-    k_ed_prep<<<num_sms * 8, 256, 0, st>>>(t, nt, L, Lk, tb, tn);
+    k_ed_prep<<<num_sms * 8, 256, 0, st>>>(q, nq, L, Lk, ED_M, qimg, qn);
+    k_ed_prep<<<num_sms * 8, 256, 0, st>>>(t, nt, L, Lk, ED_N, timg, tn);
     const int nkc = Lk / ED_KC;
-    const size_t smem = (size_t)nkc * ED_A_CHUNK + 2 * ED_B_CHUNK + 64 + 1024;
+    const size_t smem = (size_t)nkc * ED_A_CHUNK + ED_STAGES * ED_B_CHUNK + 128 + 1024;
     cudaFuncSetAttribute(k_ed_argmin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t nmb = (nq + ED_M - 1) / ED_M;
     const int64_t ntile = (nt + ED_N - 1) / ED_N;
@@ -261,7 +334,7 @@ int launch_ed_seed(const float *q, int64_t nq, const float *t, int64_t nt, int L
     if (nsplit < 1) nsplit = 1;
     const int64_t units = nmb * nsplit;
     const int grid = (int)(units < num_sms ? units : num_sms);
-    k_ed_argmin<<<grid, 128, smem, st>>>(qb, tb, qn, tn, nq, nt, Lk, nsplit, key);
+    k_ed_argmin<<<grid, 160, smem, st>>>(qimg, timg, qn, tn, nq, nt, Lk, nsplit, key);
     count_launch(3, __func__);
     return 0;
 }
