@@ -261,27 +261,40 @@ __global__ void __launch_bounds__(160, 1)
                 ph_afull[buf] ^= 1u;
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const int64_t n0 = tt * ED_N;
+                // 4 blocks of 64 columns: the block's |t|^2 (16 float4, the same addresses for
+                // every lane: L1 broadcasts) and accumulator columns (4 x tcgen05.ld x16) are all
+                // requested before the first compare -- one latency per block, not per column
 #pragma unroll 1
-                for (int cb = 0; cb < ED_N / 16; ++cb) {
-                    uint32_t v[16];
-                    asm volatile(
-                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, "
-                        "%8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                          "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]),
-                          "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                        : "r"(taddr + ((uint32_t)(32 * warp) << 16) +
-                              (uint32_t)(buf * ED_N + cb * 16)));
+                for (int blk = 0; blk < ED_N / 64; ++blk) {
+                    const int64_t nb0 = n0 + blk * 64;
+                    float tv[64];
+                    const float4 *tp = reinterpret_cast<const float4 *>(tn + nb0);
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float4 f = __ldg(tp + k);
+                        tv[4 * k] = f.x; tv[4 * k + 1] = f.y; tv[4 * k + 2] = f.z; tv[4 * k + 3] = f.w;
+                    }
+                    uint32_t v[64];
+#pragma unroll
+                    for (int cb = 0; cb < 4; ++cb)
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, "
+                            "%7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+                            : "=r"(v[16 * cb + 0]), "=r"(v[16 * cb + 1]), "=r"(v[16 * cb + 2]),
+                              "=r"(v[16 * cb + 3]), "=r"(v[16 * cb + 4]), "=r"(v[16 * cb + 5]),
+                              "=r"(v[16 * cb + 6]), "=r"(v[16 * cb + 7]), "=r"(v[16 * cb + 8]),
+                              "=r"(v[16 * cb + 9]), "=r"(v[16 * cb + 10]), "=r"(v[16 * cb + 11]),
+                              "=r"(v[16 * cb + 12]), "=r"(v[16 * cb + 13]), "=r"(v[16 * cb + 14]),
+                              "=r"(v[16 * cb + 15])
+                            : "r"(taddr + ((uint32_t)(32 * warp) << 16) +
+                                  (uint32_t)(buf * ED_N + blk * 64 + cb * 16)));
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int64_t n = n0 + cb * 16 + j;
-                        if (n < nt) {
-                            const float sc = fmaf(-2.0f, __uint_as_float(v[j]), qrow + tn[n]);
-                            if (sc < bestv) {
-                                bestv = sc;
-                                besti = n;
-                            }
+                    for (int j = 0; j < 64; ++j) {
+                        const float sc = fmaf(-2.0f, __uint_as_float(v[j]), qrow + tv[j]);
+                        if (sc < bestv && nb0 + j < nt) {
+                            bestv = sc;
+                            besti = nb0 + j;
                         }
                     }
                 }
@@ -305,7 +318,8 @@ int ed_seed_supported(int L) { return L >= 1 && L <= ED_MAX_L; }
 size_t ed_seed_scratch_bytes(int64_t nq, int64_t nt, int L) {
     const int64_t Lk = ed_lk(L);
     const int64_t qrows = (nq + ED_M - 1) / ED_M * ED_M, trows = (nt + ED_N - 1) / ED_N * ED_N;
-    return (size_t)(qrows + trows) * (size_t)Lk * 2 + (size_t)(nq + nt) * 4 + 1024;
+    return (size_t)(qrows + trows) * (size_t)Lk * 2 + (size_t)((nq + 3) / 4 * 4 + trows) * 4 +
+           1024;
 }
 
 // q [nq][L], t [nt][L] fp32 -> key[q] = min over n of ((ED(q, t_n) as f32 bits) << 32 | n),
@@ -320,7 +334,7 @@ int launch_ed_seed(const float *q, int64_t nq, const float *t, int64_t nt, int L
     __nv_bfloat16 *qimg = reinterpret_cast<__nv_bfloat16 *>(scratch);
     __nv_bfloat16 *timg = qimg + qrows * Lk;
     float *qn = reinterpret_cast<float *>(timg + trows * Lk);
-    float *tn = qn + nq;
+    float *tn = qn + (nq + 3) / 4 * 4;  // 16-byte aligned: the epilogue reads it as float4
     k_ed_prep<<<num_sms * 8, 256, 0, st>>>(q, nq, L, Lk, ED_M, qimg, qn);
     k_ed_prep<<<num_sms * 8, 256, 0, st>>>(t, nt, L, Lk, ED_N, timg, tn);
     const int nkc = Lk / ED_KC;
