@@ -114,6 +114,10 @@ struct ClassifyWs {
     float *apad;     // the band kernel's padded query rows (survivor round, GA variant)
     int64_t apad_cap;
     unsigned *colmask;  // two-stage lists: live bits per (32-query tile, train series)
+    void *ed_scratch;   // ED seed (ed_seed.cu): bf16 operand images and norms
+    size_t ed_bytes;
+    unsigned long long *edkey;  // [nq] the ED argmin as a packed key
+    int32_t *edseed;            // [nq] its train index (the first seed round's extra seed)
     int32_t *blist;  // the listed queries, train-series-major (col_off)
     float *bval;     // their full cascade values (S3 compacts from these lists)
     unsigned long long *minkey2;  // argmin of the full cascade value (second seed)
@@ -164,6 +168,10 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
     W.apad_cap = (int64_t)q1 * band_apad_row_floats(L);
     W.apad = (float *)take(sizeof(float) * (size_t)W.apad_cap);
     W.colmask = (unsigned *)take(sizeof(unsigned) * ((q1 + 31) / 32) * t1);
+    W.ed_bytes = ed_seed_supported(L) ? ed_seed_scratch_bytes((int64_t)q1, (int64_t)t1, L) : 0;
+    W.ed_scratch = take(W.ed_bytes);
+    W.edkey = (unsigned long long *)take(8 * q1);
+    W.edseed = (int32_t *)take(4 * q1);
     W.blist = (int32_t *)take(sizeof(int32_t) * (size_t)W.item_cap);
     W.bval = (float *)take(sizeof(float) * (size_t)W.item_cap);
     W.bytes = off;
@@ -227,7 +235,7 @@ static void exact_local(ClassifyWs &W, const float *q, int64_t nq, const float *
 static int classify_impl(const float *q, int64_t nq, const float *t, const float *U,
                          const float *Lo, const nndtw_kim *tkim, int64_t nt, int64_t index_base,
                          int64_t self_offset, int L, int w, int v, uint32_t flags,
-                         const int32_t *seed2, void *ws, size_t ws_bytes,
+                         const int32_t *seed2_in, void *ws, size_t ws_bytes,
                          unsigned long long *key, nndtw_stats *stats, cudaStream_t st,
                          StageTimer *outer_tm = nullptr) {
     int sms = 0;
@@ -297,6 +305,16 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         if (e[0] == '1') two_stage = false;
         if (e[0] == '2') two_stage = !alt && !sym && !keogh && nb_ >= 1 && nb_ <= 16;
     }
+    // Euclidean-nearest first seed (ed_seed.cu; the paper's candidate order): in the
+    // two-stage path, when the caller gives no seed of its own (LOOCV passes the previous
+    // window's neighbour), there is no leave-one-out self pair (the ED argmin would be the
+    // held-out series itself) and the rows fit the tensor-core kernel.  NNDTW_ED_SEED=0 disables
+    // it (experiments; read per call -- keep it fixed across the phases of one sharded classify).
+    bool ed_seed = two_stage && seed2_in == nullptr && self_offset < 0 && ed_seed_supported(L) &&
+                   nt > 0;
+    if (const char *e = getenv("NNDTW_ED_SEED"))
+        if (e[0] == '0') ed_seed = false;
+    const int32_t *seed2 = ed_seed ? W.edseed : seed2_in;
     TieLog log{W.log, W.log_count, W.log_cap, W.overflow};
     unsigned long long *cnt = stats ? W.counters : nullptr;
 
@@ -340,6 +358,12 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     StageTimer bridge_tm(stats != nullptr && outer_tm == nullptr && two_stage, st);
     long long bridge_pairs_h = 0;
     if (do_seed && two_stage && nt > 0) {
+        if (ed_seed) {  // the ED argmin joins the first seed round
+            cudaMemsetAsync(W.edkey, 0xff, 8 * (size_t)nq, st);
+            if (launch_ed_seed(q, nq, t, nt, L, W.ed_scratch, W.edkey, sms, st))
+                return fail(NNDTW_E_ARG, "ED seed launch failed");
+            launch_key_index(W.edkey, nq, nt, W.edseed, st);
+        }
         // stage A: max(LB_Kim, boundary + bands) for all pairs + its argmin (first seed)
         if (launch_lb(q, nq, W.qkim, t, U, Lo, tkim, nt, L, w, v, 1, self_offset, W.lb, W.ldlb,
                       W.minkey, st, 0, 0, 1))

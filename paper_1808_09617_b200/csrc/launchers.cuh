@@ -113,6 +113,8 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
 // seglen for any window: padl + L + padr <= L + w + R + 48)
 inline int64_t band_apad_row_floats(int L) { return 2 * (int64_t)L + 128; }
 
+int launch_key_index(const unsigned long long *key, int64_t nq, int64_t nt, int32_t *idx,
+                     cudaStream_t st);
 // ed_seed.cu: per-query argmin of the Euclidean distance over all train series (tensor cores)
 int ed_seed_supported(int L);
 size_t ed_seed_scratch_bytes(int64_t nq, int64_t nt, int L);

@@ -77,6 +77,23 @@ __global__ void k_seed_items(const unsigned long long *minkey, const int32_t *se
     }
 }
 
+// the train index of a packed key, or -1 (no candidate)
+__global__ void k_key_index(const unsigned long long *key, int64_t nq, int64_t nt, int32_t *idx) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const unsigned long long k = key[q];
+    const unsigned n = (unsigned)(k & 0xffffffffull);
+    idx[q] = (k != kNone && n < (unsigned)nt) ? (int32_t)n : -1;
+}
+
+int launch_key_index(const unsigned long long *key, int64_t nq, int64_t nt, int32_t *idx,
+                     cudaStream_t st) {
+    if (nq == 0) return 0;
+    k_key_index<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(key, nq, nt, idx);
+    count_launch(1, __func__);
+    return 0;
+}
+
 int launch_seed_items(const unsigned long long *minkey, const int32_t *seed2, int64_t nq,
                       int64_t nt, Item *items, unsigned long long *count, cudaStream_t st) {
     if (nq == 0) return 0;
