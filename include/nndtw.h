@@ -188,11 +188,13 @@ NNDTW_API int nndtw_lb_new(const float *q, int64_t nq, const float *t, int64_t n
 
 /*
  * Euclidean-nearest candidate of every query (the paper's candidate order; the ED is
- * DTW_0): key[i] = min over j of ((bits of f32 ED(q_i, t_j)) << 32 | j), ED squared,
- * computed from bf16-rounded series with fp32 accumulation on the tensor cores (tcgen05), so the
- * chosen j is nearest up to that rounding -- it serves as a seed (any candidate's exact DTW is a
- * valid best-so-far), not as a distance.  key must hold 0xFFFF...FF on entry (it is min-ed into).
- * q: [nq][L], t: [nt][L] device fp32; 1 <= L <= 512 (else NNDTW_E_LENGTH); ws: device scratch of
+ * DTW_0), on piecewise-aggregate approximations: x -> the means over f consecutive points
+ * (the last segment zero-padded), f the smallest power of two with ceil(L/f) <= 128.
+ * key[i] = min over j of ((bits of f32 ED(paa(q_i), paa(t_j))) << 32 | j), ED squared, computed
+ * from bf16-rounded PAAs with fp32 accumulation on the tensor cores (tcgen05), so the chosen j is
+ * nearest up to that approximation -- it serves as a seed (any candidate's exact DTW is a valid
+ * best-so-far), not as a distance.  key must hold 0xFFFF...FF on entry (it is min-ed into).
+ * q: [nq][L], t: [nt][L] device fp32, L >= 1; ws: device scratch of
  * nndtw_ed_seed_workspace_bytes(nq, nt, L) bytes.
  */
 NNDTW_API size_t nndtw_ed_seed_workspace_bytes(int64_t nq, int64_t nt, int32_t L);

@@ -710,7 +710,7 @@ int nndtw_ed_seed(const float *q, int64_t nq, const float *t, int64_t nt, int32_
     if ((rc = device_sms(&sms))) return rc;
     if (nq < 0 || nt < 0) return fail(NNDTW_E_ARG, "negative count");
     if (L < 1) return fail(NNDTW_E_LENGTH, "L must be >= 1");
-    if (!ed_seed_supported(L)) return fail(NNDTW_E_LENGTH, "nndtw_ed_seed supports L <= 512");
+    if (!ed_seed_supported(L)) return fail(NNDTW_E_LENGTH, "L must be >= 1");
     if (nq > 0 && nt > 0 && (!q || !t || !key || !ws)) return fail(NNDTW_E_ARG, "null pointer argument");
     if (ws_bytes < ed_seed_scratch_bytes(nq, nt, L)) return fail(NNDTW_E_WORKSPACE, "ws too small");
     if (launch_ed_seed(q, nq, t, nt, L, ws, (unsigned long long *)key, sms, (cudaStream_t)stream))

@@ -9,14 +9,15 @@
 // Q T^T (nq x nt x L) on the 5th-generation tensor cores, in bf16 with fp32 accumulation, and
 // the per-query argmin is fused into the epilogue -- the nq x nt scores never reach memory.
 //
-// B200 design (k_ed_argmin).  A CTA owns 128 queries (UMMA M = 128): their bf16 rows, K-major, sit
-// in shared memory for the whole unit (L <= 512: 8 K-chunks x 16 KB, the 128-byte-swizzled
-// canonical layout), and it sweeps a range of train tiles of 256 series (UMMA N = 256): per tile
-// the K-chunks of the train rows stream through a two-stage shared-memory ring (cp.async), one
-// elected thread issues tcgen05.mma (kind::f16, 4 x K = 16 per chunk) into a 128 x 256 fp32
-// accumulator in TMEM and commits each chunk to the stage's mbarrier (which frees the stage),
-// and after the tile the four warps read their 32 TMEM lanes (tcgen05.ld 32x32b) and update a
-// per-row running argmin of |t|^2 - 2 q.t.  One atomicMin per query and unit at the end.
+// B200 design (k_ed_argmin).  A CTA owns 128 queries (UMMA M = 128): their bf16 PAA rows, K-major,
+// sit in shared memory for the whole unit (<= 2 K-chunks x 16 KB, the 128-byte-swizzled canonical
+// layout), and it sweeps a range of train tiles of 256 series (UMMA N = 256): per tile the
+// K-chunks of the train rows arrive by bulk copies (pre-swizzled images, one cp.async.bulk per
+// 32 KB chunk on an mbarrier) into a six-stage ring; one elected thread issues tcgen05.mma
+// (kind::f16, 4 x K = 16 per chunk) into one of two 128 x 256 fp32 accumulators in TMEM and
+// commits each chunk to its stage's mbarrier (which frees the stage); four epilogue warps read
+// their 32 TMEM lanes (tcgen05.ld 32x32b) and update a per-row running argmin of |t|^2 - 2 q.t
+// while the next tile accumulates.  One atomicMin per query and unit at the end.
 #include "launchers.cuh"
 
 #include <cuda_bf16.h>
@@ -26,16 +27,29 @@ namespace nndtw {
 constexpr int ED_M = 128, ED_N = 256, ED_KC = 64;  // bf16 per K-chunk row: 128 bytes
 constexpr int ED_A_CHUNK = ED_M * ED_KC * 2;       // 16 KB
 constexpr int ED_B_CHUNK = ED_N * ED_KC * 2;       // 32 KB
-constexpr int ED_MAX_L = 512;                      // A resident: L <= 512 (128 KB)
-constexpr int ED_STAGES = 3;                       // B ring: 3 x 32 KB (with A: 224 KB)
+constexpr int ED_MAX_LK = 128;                     // PAA length cap: A resident in 32 KB
+constexpr int ED_STAGES = 6;                       // B ring: 6 x 32 KB (with A: 224 KB)
 
-__host__ __device__ inline int ed_lk(int L) { return (L + ED_KC - 1) / ED_KC * ED_KC; }
+// The seed is chosen on piecewise-aggregate approximations (means over f consecutive points,
+// f the smallest power of two with ceil(L / f) <= 128): on config 2 (f = 4) the PAA-ED argmin's
+// DTW is 1.336x the final distance, the full ED argmin's 1.341x (tools/seed_study.py) -- the
+// seed quality is the same at a quarter of the bytes and MMA work.
+__host__ __device__ inline int ed_f(int L) {
+    int f = 1;
+    while ((L + f - 1) / f > ED_MAX_LK) f <<= 1;
+    return f;
+}
+__host__ __device__ inline int ed_lk(int L) {
+    const int f = ed_f(L), Lr = (L + f - 1) / f;
+    return (Lr + ED_KC - 1) / ED_KC * ED_KC;
+}
 
-// Rows to bf16 in the operand image the tensor cores read: per tile of `rows` rows and K-chunk of
-// 64 columns a contiguous block, row r at (r / 8) * 1024 + (r % 8) * 128 bytes, its 16-byte chunk c
-// at c ^ (r % 8) (the 128-byte swizzle), so every block is one bulk copy into shared memory.
-// Rows past n and columns past L are zero.  |x|^2 in fp32 from the fp32 values.
-__global__ void k_ed_prep(const float *__restrict__ x, int64_t n, int L, int Lk, int rows,
+// Rows to their PAA (means over f points; the last segment zero-padded) in bf16, in the operand
+// image the tensor cores read: per tile of `rows` rows and K-chunk of 64 columns a contiguous
+// block, row r at (r / 8) * 1024 + (r % 8) * 128 bytes, its 16-byte chunk c at c ^ (r % 8) (the
+// 128-byte swizzle), so every block is one bulk copy into shared memory.  Rows past n and columns
+// past the PAA length are zero.  |PAA|^2 in fp32.
+__global__ void k_ed_prep(const float *__restrict__ x, int64_t n, int L, int f, int Lk, int rows,
                           __nv_bfloat16 *__restrict__ img, float *__restrict__ norm) {
     const int lane = threadIdx.x & 31;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -49,7 +63,10 @@ __global__ void k_ed_prep(const float *__restrict__ x, int64_t n, int L, int Lk,
                         (rr >> 3) * 1024 + (rr & 7) * 128;
         float s = 0.0f;
         for (int c = lane; c < Lk; c += 32) {
-            const float v = (r < n && c < L) ? x[r * L + c] : 0.0f;
+            float v = 0.0f;
+            if (r < n)
+                for (int e = 0; e < f; ++e) v += (c * f + e < L) ? x[r * L + c * f + e] : 0.0f;
+            v *= 1.0f / (float)f;
             s = fmaf(v, v, s);
             const int kc = c / ED_KC, kk = c % ED_KC, ch = kk >> 3, e = kk & 7;
             __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(
@@ -126,8 +143,8 @@ __global__ void __launch_bounds__(160, 1)
     uint8_t *smA = ed_smem + ((1024u - (smem_u32(ed_smem) & 1023u)) & 1023u);
     uint8_t *smB = smA + nkc * ED_A_CHUNK;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smB + ED_STAGES * ED_B_CHUNK);
-    // bars: full[3], empty[3], afull[2], aempty[2], abar
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 11);
+    // bars: full[S], empty[S], afull[2], aempty[2], abar
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 2 * ED_STAGES + 5);
     const uint32_t b_full = smem_u32(bars), b_empty = b_full + 8 * ED_STAGES;
     const uint32_t b_afull = b_empty + 8 * ED_STAGES, b_aempty = b_afull + 16;
     const uint32_t b_a = b_aempty + 16;
@@ -165,8 +182,12 @@ __global__ void __launch_bounds__(160, 1)
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
                                    ((uint32_t)(ED_N >> 3) << 17) | ((uint32_t)(ED_M >> 4) << 24);
             const uint32_t aA = smem_u32(smA), aB = smem_u32(smB);
-            uint32_t ph_full[ED_STAGES] = {0u, 0u, 0u}, ph_empty[ED_STAGES] = {0u, 0u, 0u};
-            bool used[ED_STAGES] = {false, false, false};
+            uint32_t ph_full[ED_STAGES], ph_empty[ED_STAGES];
+            bool used[ED_STAGES];
+            for (int i = 0; i < ED_STAGES; ++i) {
+                ph_full[i] = ph_empty[i] = 0u;
+                used[i] = false;
+            }
             uint32_t ph_aempty[2] = {0u, 0u}, ph_a = 0u;
             bool aused[2] = {false, false};
             int buf = 0;
@@ -289,13 +310,25 @@ __global__ void __launch_bounds__(160, 1)
                             : "r"(taddr + ((uint32_t)(32 * warp) << 16) +
                                   (uint32_t)(buf * ED_N + blk * 64 + cb * 16)));
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    // score' = |t|^2 - 2 q.t (|q|^2 is added once per row); the block minimum
+                    // by a min tree, the index only when the row's best improves (rare once a
+                    // few tiles are done)
+                    float sc[64];
 #pragma unroll
-                    for (int j = 0; j < 64; ++j) {
-                        const float sc = fmaf(-2.0f, __uint_as_float(v[j]), qrow + tv[j]);
-                        if (sc < bestv && nb0 + j < nt) {
-                            bestv = sc;
-                            besti = nb0 + j;
-                        }
+                    for (int j = 0; j < 64; ++j) sc[j] = fmaf(-2.0f, __uint_as_float(v[j]), tv[j]);
+                    if (nb0 + 64 > nt) {  // the last tile's columns past nt (warp-uniform)
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) sc[j] = nb0 + j < nt ? sc[j] : kInf;
+                    }
+                    float m = sc[0];
+#pragma unroll
+                    for (int j = 1; j < 64; j += 2) m = fminf(m, fminf(sc[j], j + 1 < 64 ? sc[j + 1] : kInf));
+                    if (m + qrow < bestv) {
+                        int jj = 0;
+#pragma unroll
+                        for (int j = 63; j >= 0; --j) jj = sc[j] == m ? j : jj;  // first minimum
+                        bestv = m + qrow;
+                        besti = nb0 + jj;
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -313,7 +346,7 @@ __global__ void __launch_bounds__(160, 1)
                      : "memory");
 }
 
-int ed_seed_supported(int L) { return L >= 1 && L <= ED_MAX_L; }
+int ed_seed_supported(int L) { return L >= 1; }
 
 size_t ed_seed_scratch_bytes(int64_t nq, int64_t nt, int L) {
     const int64_t Lk = ed_lk(L);
@@ -335,10 +368,11 @@ int launch_ed_seed(const float *q, int64_t nq, const float *t, int64_t nt, int L
     __nv_bfloat16 *timg = qimg + qrows * Lk;
     float *qn = reinterpret_cast<float *>(timg + trows * Lk);
     float *tn = qn + (nq + 3) / 4 * 4;  // 16-byte aligned: the epilogue reads it as float4
-    k_ed_prep<<<num_sms * 8, 256, 0, st>>>(q, nq, L, Lk, ED_M, qimg, qn);
-    k_ed_prep<<<num_sms * 8, 256, 0, st>>>(t, nt, L, Lk, ED_N, timg, tn);
+    const int f = ed_f(L);
+    k_ed_prep<<<num_sms * 8, 256, 0, st>>>(q, nq, L, f, Lk, ED_M, qimg, qn);
+    k_ed_prep<<<num_sms * 8, 256, 0, st>>>(t, nt, L, f, Lk, ED_N, timg, tn);
     const int nkc = Lk / ED_KC;
-    const size_t smem = (size_t)nkc * ED_A_CHUNK + ED_STAGES * ED_B_CHUNK + 128 + 1024;
+    const size_t smem = (size_t)nkc * ED_A_CHUNK + ED_STAGES * ED_B_CHUNK + 256 + 1024;
     cudaFuncSetAttribute(k_ed_argmin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t nmb = (nq + ED_M - 1) / ED_M;
     const int64_t ntile = (nt + ED_N - 1) / ED_N;

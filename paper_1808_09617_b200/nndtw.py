@@ -255,8 +255,9 @@ def lb_new(q, t, w: int, stream=None) -> torch.Tensor:
 
 def ed_seed(q, t, stream=None):
     """Euclidean-nearest train index of every query (int64 [nq]) and its squared ED as computed
-    (bf16 inputs, fp32 accumulation on the tensor cores) -- the paper's candidate order (P:569);
-    a seed, not a distance.  L <= 512."""
+    on piecewise-aggregate approximations (means over f points, ceil(L/f) <= 128; bf16 inputs,
+    fp32 accumulation on the tensor cores) -- the paper's candidate order; a seed, not a
+    distance."""
     _series(q, "q"); _series(t, "t")
     nq, L = q.shape
     nt = t.shape[0]
