@@ -64,6 +64,26 @@ def main():
     print(f"ED-argmin seed: NN found for {(de <= final * (1 + 1e-6)).double().mean().item() * 100:.1f} % "
           f"of queries, mean bsf / final = {(de / final.clamp_min(1e-30)).mean().item():.3f}, "
           f"listed at its bsf: {(part <= de.float().unsqueeze(1)).double().mean().item() * 100:.2f} %")
+    for f in (2, 4):  # the same on series averaged over f consecutive points (PAA)
+        qp = q.reshape(nq, -1, f).mean(2)
+        tp = t.reshape(t.shape[0], -1, f).mean(2)
+        edp = (qp * qp).sum(1, keepdim=True) + (tp * tp).sum(1).unsqueeze(0) - 2.0 * (qp @ tp.T)
+        ep = edp.argmin(dim=1).to(torch.int32)
+        if f == 4:  # the k Euclidean-nearest (PAA) candidates as seeds
+            eo = torch.argsort(edp, dim=1)[:, :8]
+            de8 = nndtw.dtw_batch(q, t, w, torch.arange(nq, device=dev, dtype=torch.int32)
+                                  .repeat_interleave(8), eo.reshape(-1).to(torch.int32)).double()
+            de8 = de8.reshape(nq, 8)
+            for k in (1, 2, 4, 8):
+                bk = de8[:, :k].min(dim=1).values
+                print(f"top-{k} ED (PAA/4) candidates: mean bsf / final = "
+                      f"{(bk / final.clamp_min(1e-30)).mean().item():.3f}, listed at its bsf: "
+                      f"{(part <= bk.float().unsqueeze(1)).double().mean().item() * 100:.2f} %")
+        del edp
+        dpa = nndtw.dtw_batch(q, t, w, torch.arange(nq, device=dev, dtype=torch.int32), ep).double()
+        print(f"ED argmin on PAA/{f}: mean bsf / final = "
+              f"{(dpa / final.clamp_min(1e-30)).mean().item():.3f}, listed at its bsf: "
+              f"{(part <= dpa.float().unsqueeze(1)).double().mean().item() * 100:.2f} %")
     for k in (1, 2, 4, 8, 16):
         best = d[:, :k].min(dim=1).values
         hit = (best <= final * (1 + 1e-6)).double().mean().item()
