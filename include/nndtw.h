@@ -285,7 +285,21 @@ NNDTW_API int nndtw_dtw_batch(const float *a, const float *b, const int32_t *ia,
 #define NNDTW_CLASSIFY_BOUND_NEW 512u
 #define NNDTW_CLASSIFY_BOUND_ENHANCED_IMPROVED 1024u
 #define NNDTW_CLASSIFY_BOUND_NONE 2048u
+/* Workspace.  nndtw_classify_workspace_bytes: the full layout, room for every (query, train)
+ * pair as a survivor and as a two-stage list entry (24 bytes per pair with the 4-byte bound
+ * matrix).  nndtw_classify_workspace_bytes_capped: room for at most max_pairs survivors and
+ * max_pairs list entries (4 + 20*max_pairs/(nq*nt) bytes per pair; >= 2*nq + 2); classify
+ * infers the capacity from ws_bytes (the full layout whenever ws_bytes holds it).  A call whose
+ * survivors or listed pairs exceed the capacity stores only what fits and sets an overflow word
+ * in ws: its keys are then NOT valid.  nndtw_classify_overflowed synchronises `stream`, and sets
+ * *overflowed = 1 if the last classify on ws overflowed (else 0); the caller reruns that call
+ * with a larger (e.g. the full) workspace.  The answer of a call that did not overflow is the
+ * full layout's. */
 NNDTW_API size_t nndtw_classify_workspace_bytes(int64_t nq, int64_t nt, int32_t L, int32_t w);
+NNDTW_API size_t nndtw_classify_workspace_bytes_capped(int64_t nq, int64_t nt, int32_t L,
+                                                       int32_t w, int64_t max_pairs);
+NNDTW_API int nndtw_classify_overflowed(const void *ws, size_t ws_bytes, int64_t nq, int64_t nt,
+                                        int32_t L, int32_t *overflowed, void *stream);
 NNDTW_API int nndtw_classify(const float *q, int64_t nq, const float *t, const float *upper,
                    const float *lower, const nndtw_kim *tkim, int64_t nt, int64_t index_base,
                    int64_t self_offset, int32_t L, int32_t w, int32_t v, uint32_t flags,

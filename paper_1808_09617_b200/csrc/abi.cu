@@ -92,8 +92,9 @@ static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // ---- classify workspace layout -----------------------------------------------------------
 struct ClassifyWs {
-    unsigned long long *counters;  // CNT_N + 3 (seed count, item count, log count)
+    unsigned long long *counters;  // CNT_N + 4 (seed count, item count, log count, overflow)
     unsigned long long *seed_count, *main_count, *log_count;
+    unsigned long long *cap_overflow;  // set when a survivor or list count exceeded item_cap
     nndtw_kim *qkim;
     unsigned long long *minkey, *f64key, *resolve_out;
     unsigned *overflow;
@@ -124,7 +125,13 @@ struct ClassifyWs {
     size_t bytes;
 };
 
-static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
+static unsigned long long full_pair_cap(int64_t nq, int64_t nt) {
+    return (unsigned long long)nq * (unsigned long long)nt + 1;
+}
+
+// pair_cap: entries of the survivor list and of the two-stage pair lists (full = nq*nt + 1)
+static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L,
+                                  unsigned long long pair_cap) {
     ClassifyWs W;
     size_t off = 0;
     char *b = (char *)base;
@@ -134,10 +141,11 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
         return p;
     };
     const size_t q1 = (size_t)(nq > 0 ? nq : 1);
-    W.counters = (unsigned long long *)take(sizeof(unsigned long long) * (CNT_N + 3));
+    W.counters = (unsigned long long *)take(sizeof(unsigned long long) * (CNT_N + 4));
     W.seed_count = W.counters ? W.counters + CNT_N : nullptr;
     W.main_count = W.counters ? W.counters + CNT_N + 1 : nullptr;
     W.log_count = W.counters ? W.counters + CNT_N + 2 : nullptr;
+    W.cap_overflow = W.counters ? W.counters + CNT_N + 3 : nullptr;
     W.qkim = (nndtw_kim *)take(sizeof(nndtw_kim) * q1);
     W.minkey = (unsigned long long *)take(8 * q1);
     W.f64key = (unsigned long long *)take(8 * q1);
@@ -149,7 +157,7 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
     W.buckets = (unsigned long long *)take(sizeof(unsigned long long) * 3 * NBUCKET);
     W.split_count = (unsigned long long *)take(sizeof(unsigned long long));
     W.seed_items = (Item *)take(sizeof(Item) * (2 * q1 + 1));
-    W.item_cap = (unsigned long long)nq * (unsigned long long)nt + 1;
+    W.item_cap = pair_cap;
     W.items = (Item *)take(sizeof(Item) * (size_t)W.item_cap);
     W.log_cap = (unsigned long long)(64 * nq > 65536 ? 64 * nq : 65536);
     if (const char *cap = getenv("NNDTW_TIE_LOG_CAP")) {  // tests: force the overflow path
@@ -176,6 +184,30 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
     W.bval = (float *)take(sizeof(float) * (size_t)W.item_cap);
     W.bytes = off;
     return W;
+}
+
+static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L) {
+    return classify_layout(base, nq, nt, L, full_pair_cap(nq, nt));
+}
+
+// The layout a workspace of ws_bytes holds: the full one (every pair can be a survivor) when it
+// fits, else the largest pair capacity that does (nndtw_classify_workspace_bytes_capped).  A
+// call whose survivors or listed pairs exceed the capacity sets the overflow word
+// (nndtw_classify_overflowed); its keys are then not valid and the caller reruns it with more.
+static ClassifyWs classify_layout_for(void *base, int64_t nq, int64_t nt, int L, size_t ws_bytes) {
+    const unsigned long long full = full_pair_cap(nq, nt);
+    ClassifyWs W = classify_layout(base, nq, nt, L, full);
+    if (ws_bytes >= W.bytes) return W;
+    const size_t fixed = classify_layout(nullptr, nq, nt, L, 0).bytes;
+    const size_t per_pair = sizeof(Item) + sizeof(int32_t) + sizeof(float);
+    if (ws_bytes <= fixed) return W;  // too small for any capacity: reported by the caller
+    // the largest capacity that fits (alignment: each of the three arrays rounds up to 256 B,
+    // so this starts at most a few dozen above it; the layout size grows with the capacity)
+    unsigned long long cap = (unsigned long long)((ws_bytes - fixed) / per_pair);
+    if (cap >= full) cap = full - 1;
+    while (cap > 0 && classify_layout(nullptr, nq, nt, L, cap).bytes > ws_bytes) --cap;
+    if (cap < 2ull * (unsigned long long)nq + 2ull) return W;  // (not even the seed rounds)
+    return classify_layout(base, nq, nt, L, cap);
 }
 
 static int check_common(int64_t n, int L, int w) {
@@ -250,7 +282,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     if (index_base < 0 || index_base + nt > 0x7fffffffll)
         return fail(NNDTW_E_INDEX, "global train indices must be < 2^31 (signed int64 shard "
                                    "combine of (index << 32) keys)");
-    ClassifyWs W = classify_layout(ws, nq, nt, L);
+    ClassifyWs W = classify_layout_for(ws, nq, nt, L, ws_bytes);
     if (ws_bytes < W.bytes) return fail(NNDTW_E_WORKSPACE, "workspace too small");
     if (nq == 0) return NNDTW_OK;
     const int64_t launches0 = launches_total();
@@ -321,7 +353,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     tm.mark();  // 0
     if (do_seed) {
         launch_classify_init(nq, key, W.minkey, W.f64key, W.resolve_out, W.overflow, W.tiecnt,
-                             W.counters, CNT_N + 3, W.buckets, st);
+                             W.counters, CNT_N + 4, W.buckets, st);
         launch_cells_prefix(L, w, W.cells_prefix, st);
     }
     tm.mark();  // 1
@@ -377,7 +409,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         // stage B: the pairs Algorithm 1's line-12 test keeps (P <= bsf1*(1+eps_p)), per train
         // series, and the full cascade value for them (+ its argmin: the second seed)
         launch_col_compact(W.lb, W.ldlb, nq, nt, key, eps_p, W.col_count, W.col_off, W.col_fill,
-                           W.blist, W.item_cap, W.colmask, sms, st);
+                           W.blist, W.item_cap, W.colmask, W.cap_overflow, sms, st);
         cudaMemsetAsync(W.minkey2, 0xff, 8 * (size_t)nq, st);
         if (bridge_tm.on) cudaEventRecord(bridge_tm.ev[0], st);
         if (launch_lb_sparse(q, W.qkim, nq, t, U, Lo, tkim, nt, L, w, v, W.col_off,
@@ -431,11 +463,11 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     if (nt > 0 && do_compact && two_stage) {
         // S3 from the two-stage lists (every possible survivor is listed, with its full value)
         launch_list_compact(W.col_off, W.blist, W.bval, nt, key, W.minkey, seed2, eps_p, W.items,
-                            W.main_count, W.buckets, W.item_cap, sms, st);
+                            W.main_count, W.buckets, W.item_cap, W.cap_overflow, sms, st);
     } else if (nt > 0 && do_compact) {
         // S3: prune + compact the survivors against the seeded best-so-far
         launch_compact(W.lb, W.ldlb, nq, nt, key, W.minkey, seed2, eps_p, W.items,
-                       W.main_count, W.buckets, W.item_cap, sms, st);
+                       W.main_count, W.buckets, W.item_cap, W.cap_overflow, sms, st);
     }
     tm.mark();  // 4
     if (nt > 0 && whole) {
@@ -751,6 +783,33 @@ size_t nndtw_classify_workspace_bytes(int64_t nq, int64_t nt, int32_t L, int32_t
     return classify_layout(nullptr, nq, nt, L).bytes;
 }
 
+size_t nndtw_classify_workspace_bytes_capped(int64_t nq, int64_t nt, int32_t L, int32_t w,
+                                             int64_t max_pairs) {
+    (void)w;
+    const unsigned long long full = full_pair_cap(nq, nt);
+    const unsigned long long lo = 2ull * (unsigned long long)(nq > 0 ? nq : 0) + 2ull;
+    unsigned long long cap = max_pairs < 0 ? full : (unsigned long long)max_pairs;
+    if (cap < lo) cap = lo;
+    if (cap >= full) return classify_layout(nullptr, nq, nt, L).bytes;
+    return classify_layout(nullptr, nq, nt, L, cap).bytes;
+}
+
+int nndtw_classify_overflowed(const void *ws, size_t ws_bytes, int64_t nq, int64_t nt, int32_t L,
+                              int32_t *overflowed, void *stream) {
+    if (!ws || !overflowed) return fail(NNDTW_E_ARG, "null pointer argument");
+    if (nq < 0 || nt < 0 || L < 2) return fail(NNDTW_E_ARG, "bad shape");
+    ClassifyWs W = classify_layout_for(const_cast<void *>(ws), nq, nt, L, ws_bytes);
+    if (ws_bytes < W.bytes) return fail(NNDTW_E_WORKSPACE, "workspace too small");
+    *overflowed = 0;
+    if (nq == 0) return NNDTW_OK;
+    unsigned long long h = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemcpyAsync(&h, W.cap_overflow, sizeof h, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_fail("overflow check");
+    *overflowed = h != 0ull ? 1 : 0;
+    return NNDTW_OK;
+}
+
 int nndtw_classify(const float *q, int64_t nq, const float *t, const float *upper,
                    const float *lower, const nndtw_kim *tkim, int64_t nt, int64_t index_base,
                    int64_t self_offset, int32_t L, int32_t w, int32_t v, uint32_t flags,
@@ -771,7 +830,7 @@ int nndtw_classify_refine(void *ws, size_t ws_bytes, const float *q, int64_t nq,
     if ((rc = device_sms(&sms))) return rc;
     if ((rc = check_common(nq, L, w))) return rc;
     if (w > L - 1) w = L - 1;
-    ClassifyWs W = classify_layout(ws, nq, nt, L);
+    ClassifyWs W = classify_layout_for(ws, nq, nt, L, ws_bytes);
     if (!ws || ws_bytes < W.bytes) return fail(NNDTW_E_WORKSPACE, "workspace too small");
     if (nq == 0) return NNDTW_OK;
     cudaStream_t st = (cudaStream_t)stream;
@@ -795,7 +854,7 @@ int nndtw_classify_resolve(void *ws, size_t ws_bytes, const float *q, int64_t nq
     if ((rc = device_sms(&sms))) return rc;
     if ((rc = check_common(nq, L, w))) return rc;
     if (w > L - 1) w = L - 1;
-    ClassifyWs W = classify_layout(ws, nq, nt, L);
+    ClassifyWs W = classify_layout_for(ws, nq, nt, L, ws_bytes);
     if (!ws || ws_bytes < W.bytes) return fail(NNDTW_E_WORKSPACE, "workspace too small");
     if (nq == 0) return NNDTW_OK;
     cudaStream_t st = (cudaStream_t)stream;

@@ -18,8 +18,8 @@ int launch_lb(const float *q, int64_t nq, const nndtw_kim *qkim, const float *t,
 int launch_col_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
                        const unsigned long long *key, float eps_p, long long *col_count,
                        long long *col_off, long long *col_fill, int32_t *qlist,
-                       unsigned long long qlist_cap, unsigned *colmask, int num_sms,
-                       cudaStream_t st);
+                       unsigned long long qlist_cap, unsigned *colmask,
+                       unsigned long long *cap_overflow, int num_sms, cudaStream_t st);
 int launch_lb_sparse(const float *q, const nndtw_kim *qkim, int64_t nq, const float *t,
                      const float *U, const float *Lo, const nndtw_kim *tkim, int64_t nt, int L,
                      int w, int v, const long long *col_off, const int32_t *qlist, float *bval,
@@ -65,12 +65,13 @@ int launch_list_compact(const long long *col_off, const int32_t *blist, const fl
                         int64_t nt, const unsigned long long *key,
                         const unsigned long long *minkey, const int32_t *seed2, float eps_p,
                         Item *items, unsigned long long *count, unsigned long long *buckets,
-                        unsigned long long capacity, int num_sms, cudaStream_t st);
+                        unsigned long long capacity, unsigned long long *cap_overflow,
+                        int num_sms, cudaStream_t st);
 int launch_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
                    const unsigned long long *key, const unsigned long long *minkey,
                    const int32_t *seed2, float eps_p, Item *items, unsigned long long *count,
-                   unsigned long long *buckets, unsigned long long capacity, int num_sms,
-                   cudaStream_t st);
+                   unsigned long long *buckets, unsigned long long capacity,
+                   unsigned long long *cap_overflow, int num_sms, cudaStream_t st);
 int launch_cells_prefix(int L, int w, long long *prefix, cudaStream_t st);
 int launch_refine(TieEntry *e, const unsigned long long *count, unsigned long long cap,
                   const float *A, const float *B, int L, int w, const unsigned long long *gkey,

@@ -101,9 +101,14 @@ __global__ void __launch_bounds__(256) k_col_compact(const float *__restrict__ l
     }
 }
 
-// counts -> offsets (col_off[n] = sum of counts before n; col_off[nt] = total), fill = 0
+// counts -> offsets (col_off[n] = sum of counts before n; col_off[nt] = total), fill = 0.
+// A capped workspace (total > cap): the offsets are clamped to cap -- the lists past it are
+// empty, so every reader stays inside the arrays -- and the overflow word is set (the call's
+// answer is invalid; nndtw_classify_overflowed reports it).
 __global__ void __launch_bounds__(1024) k_col_scan(const long long *count, long long *off,
-                                                   long long *fill, int64_t nt) {
+                                                   long long *fill, int64_t nt,
+                                                   long long cap,
+                                                   unsigned long long *cap_overflow) {
     __shared__ long long part[1024];
     const int64_t per = (nt + blockDim.x - 1) / blockDim.x;
     const int64_t b = threadIdx.x * per, e = b + per < nt ? b + per : nt;
@@ -118,12 +123,13 @@ __global__ void __launch_bounds__(1024) k_col_scan(const long long *count, long 
             part[i] = run;
             run += v;
         }
-        off[nt] = run;
+        off[nt] = run < cap ? run : cap;
+        if (run > cap && cap_overflow) *cap_overflow = 1ull;
     }
     __syncthreads();
     long long run = part[threadIdx.x];
     for (int64_t i = b; i < e; ++i) {
-        off[i] = run;
+        off[i] = run < cap ? run : cap;
         run += count[i];
         fill[i] = 0;
     }
@@ -132,8 +138,8 @@ __global__ void __launch_bounds__(1024) k_col_scan(const long long *count, long 
 int launch_col_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
                        const unsigned long long *key, float eps_p, long long *col_count,
                        long long *col_off, long long *col_fill, int32_t *qlist,
-                       unsigned long long qlist_cap, unsigned *colmask, int num_sms,
-                       cudaStream_t st) {
+                       unsigned long long qlist_cap, unsigned *colmask,
+                       unsigned long long *cap_overflow, int num_sms, cudaStream_t st) {
     if (nq == 0 || nt == 0) return 0;
     cudaMemsetAsync(col_count, 0, sizeof(long long) * (size_t)nt, st);
     const int64_t ntiles = ((nq + CC_Q - 1) / CC_Q) * ((nt + CC_N - 1) / CC_N);
@@ -141,7 +147,8 @@ int launch_col_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
     k_col_compact<0><<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, eps_p, col_count,
                                                      col_off, col_fill, qlist, qlist_cap,
                                                      colmask);
-    k_col_scan<<<1, 1024, 0, st>>>(col_count, col_off, col_fill, nt);
+    k_col_scan<<<1, 1024, 0, st>>>(col_count, col_off, col_fill, nt, (long long)qlist_cap,
+                                    cap_overflow);
     k_col_compact<1><<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, eps_p, col_count,
                                                      col_off, col_fill, qlist, qlist_cap,
                                                      colmask);

@@ -196,8 +196,11 @@ __global__ void __launch_bounds__(256) k_compact(const float *__restrict__ lb, i
 }
 
 // bucket counts -> offsets; the total is the survivor count the DTW kernel reads
+// (a capped workspace: survivors beyond `capacity` are not stored -- the overflow word is set
+// and the call's answer is invalid; nndtw_classify_overflowed reports it to the caller)
 __global__ void k_bucket_scan(const unsigned long long *count, unsigned long long *base,
-                              unsigned long long *fill, unsigned long long *total) {
+                              unsigned long long *fill, unsigned long long *total,
+                              unsigned long long capacity, unsigned long long *cap_overflow) {
     if (threadIdx.x == 0) {
         unsigned long long run = 0;
         for (int b = 0; b < NBUCKET; ++b) {
@@ -206,14 +209,15 @@ __global__ void k_bucket_scan(const unsigned long long *count, unsigned long lon
             run += count[b];
         }
         *total = run;
+        if (run > capacity && cap_overflow) *cap_overflow = 1ull;
     }
 }
 
 int launch_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
                    const unsigned long long *key, const unsigned long long *minkey,
                    const int32_t *seed2, float eps_p, Item *items, unsigned long long *count,
-                   unsigned long long *buckets, unsigned long long capacity, int num_sms,
-                   cudaStream_t st) {
+                   unsigned long long *buckets, unsigned long long capacity,
+                   unsigned long long *cap_overflow, int num_sms, cudaStream_t st) {
     if (nq == 0 || nt == 0) return 0;
     // buckets: [count | base | fill] x NBUCKET; the counts were zeroed by k_classify_init
     unsigned long long *bcount = buckets, *bbase = buckets + NBUCKET, *bfill = buckets + 2 * NBUCKET;
@@ -223,7 +227,7 @@ int launch_compact(const float *lb, int64_t ldlb, int64_t nq, int64_t nt,
     const int one = ob && ob[0] == '1';
     k_compact<0><<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, minkey, seed2, eps_p,
                                                   items, bcount, bbase, bfill, capacity, one);
-    k_bucket_scan<<<1, 32, 0, st>>>(bcount, bbase, bfill, count);
+    k_bucket_scan<<<1, 32, 0, st>>>(bcount, bbase, bfill, count, capacity, cap_overflow);
     k_compact<1><<<(unsigned)grid, 256, 0, st>>>(lb, ldlb, nq, nt, key, minkey, seed2, eps_p,
                                                   items, bcount, bbase, bfill, capacity, one);
     count_launch(3, __func__);
@@ -303,7 +307,8 @@ int launch_list_compact(const long long *col_off, const int32_t *blist, const fl
                         int64_t nt, const unsigned long long *key,
                         const unsigned long long *minkey, const int32_t *seed2, float eps_p,
                         Item *items, unsigned long long *count, unsigned long long *buckets,
-                        unsigned long long capacity, int num_sms, cudaStream_t st) {
+                        unsigned long long capacity, unsigned long long *cap_overflow,
+                        int num_sms, cudaStream_t st) {
     if (nt == 0) return 0;
     unsigned long long *bcount = buckets, *bbase = buckets + NBUCKET, *bfill = buckets + 2 * NBUCKET;
     const int64_t ntiles = (nt + LC_W - 1) / LC_W;
@@ -313,7 +318,7 @@ int launch_list_compact(const long long *col_off, const int32_t *blist, const fl
     k_list_compact<0><<<(unsigned)grid, 32 * LC_W, 0, st>>>(col_off, blist, bval, nt, key, minkey,
                                                             seed2, eps_p, items, bcount, bbase,
                                                             bfill, capacity, one);
-    k_bucket_scan<<<1, 32, 0, st>>>(bcount, bbase, bfill, count);
+    k_bucket_scan<<<1, 32, 0, st>>>(bcount, bbase, bfill, count, capacity, cap_overflow);
     k_list_compact<1><<<(unsigned)grid, 32 * LC_W, 0, st>>>(col_off, blist, bval, nt, key, minkey,
                                                             seed2, eps_p, items, bcount, bbase,
                                                             bfill, capacity, one);

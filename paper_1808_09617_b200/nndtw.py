@@ -98,6 +98,9 @@ _SIGS = {
     "nndtw_tightness": (C.c_int, [_P, _P, _I64, _P, _P, _P, _P]),
     "nndtw_dtw_batch": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P]),
     "nndtw_classify_workspace_bytes": (C.c_size_t, [_I64, _I64, _I32, _I32]),
+    "nndtw_classify_workspace_bytes_capped": (C.c_size_t, [_I64, _I64, _I32, _I32, _I64]),
+    "nndtw_classify_overflowed": (C.c_int, [_P, C.c_size_t, _I64, _I64, _I32,
+                                            C.POINTER(C.c_int32), _P]),
     "nndtw_classify": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32,
                                  C.c_uint32, _P, C.c_size_t, _P, C.POINTER(Stats), _P]),
     "nndtw_classify_refine": (C.c_int, [_P, C.c_size_t, _P, _I64, _P, _I64, _I32, _I32, _P,
@@ -311,6 +314,7 @@ class Prediction:
     label: torch.Tensor   # int32 [nq]
     dist: torch.Tensor    # float32 [nq] squared DTW (sqrt for Eq. 2's DTW)
     stats: dict | None
+    key: torch.Tensor | None = None  # int64 [nq] the packed keys (nndtw.classify)
 
 
 class Model:
@@ -337,8 +341,15 @@ class Model:
         self.U, self.Lo, self.kim = envelopes(train, self.w, True, stream)
         self._ws = None
 
-    def workspace(self, nq: int) -> torch.Tensor:
-        need = load().nndtw_classify_workspace_bytes(nq, self.t.shape[0], self.L, self.w)
+    def workspace(self, nq: int, max_pairs: int | None = None) -> torch.Tensor:
+        """Classify workspace for nq queries: the full layout, or (max_pairs) room for at most
+        that many survivors / listed pairs (nndtw_classify_workspace_bytes_capped)."""
+        lib = load()
+        if max_pairs is None:
+            need = lib.nndtw_classify_workspace_bytes(nq, self.t.shape[0], self.L, self.w)
+        else:
+            need = lib.nndtw_classify_workspace_bytes_capped(nq, self.t.shape[0], self.L, self.w,
+                                                             int(max_pairs))
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.t.device)
         return self._ws
@@ -346,7 +357,7 @@ class Model:
 
 def classify_keys(model: Model, q: torch.Tensor, exact: bool = True, self_offset: int = -1,
                   stats: bool = False, stream=None, phase: str | None = None, key=None, ws=None,
-                  level_stats: bool = False):
+                  level_stats: bool = False, max_pairs: int | None = None):
     """S2-S7 on one shard: returns (key int64 [nq], workspace, stats dict | None).
 
     phase None runs everything; "seed" stops after the S3 seed round (keys = seed keys);
@@ -362,7 +373,7 @@ def classify_keys(model: Model, q: torch.Tensor, exact: bool = True, self_offset
         if ws is None or key is None:
             raise NNDTWError(f"phase {phase!r} needs the seed call's ws and the combined key")
     else:
-        ws = model.workspace(nq)
+        ws = model.workspace(nq, max_pairs)
         key = torch.empty(nq, dtype=torch.int64, device=q.device)
     flags = ((NNDTW_CLASSIFY_EXACT if exact else 0) |
              BOUND_FLAGS[model.bound] |
@@ -380,6 +391,16 @@ def classify_keys(model: Model, q: torch.Tensor, exact: bool = True, self_offset
                                  _ptr(key), C.byref(st) if stats else None, _stream(stream)),
            "nndtw_classify")
     return key, ws, (st.as_dict() if stats else None)
+
+
+def classify_overflowed(model: Model, nq: int, ws: torch.Tensor, stream=None) -> bool:
+    """Whether the last classify on ws stored fewer survivors / listed pairs than it had (a
+    capped workspace): its keys are then not valid.  Synchronises the stream."""
+    out = C.c_int32(0)
+    _check(load().nndtw_classify_overflowed(_ptr(ws), ws.numel(), nq, model.t.shape[0], model.L,
+                                            C.byref(out), _stream(stream)),
+           "nndtw_classify_overflowed")
+    return bool(out.value)
 
 
 def merge_stats(a: dict | None, b: dict | None) -> dict | None:
@@ -420,39 +441,60 @@ def finalize(key, labels, key_format: int = 0, stream=None):
 
 
 WORKSPACE_BUDGET = 48 << 30  # bytes of classify workspace per call before queries are blocked
+SURVIVOR_CAP = 0.125  # nndtw.classify: survivors / listed pairs reserved, as a fraction of pairs
+CAP_MIN_PAIRS = 1 << 24  # calls with fewer (query, train) pairs keep the full layout by default
 
 
 def classify(model: Model, q: torch.Tensor, stats: bool = False, check: bool = True,
              stream=None, workspace_budget: int | None = None,
-             level_stats: bool = False) -> Prediction:
+             level_stats: bool = False, survivor_cap: float | None = None) -> Prediction:
     """Exact 1-NN of every query (single GPU / single shard, fp64-exact tie resolution).
 
-    The workspace holds the bound matrix, the two-stage S2's pair lists and a worst-case
-    survivor list (24 bytes per (query, train) pair: 4 + 8 + 12); when that exceeds
-    `workspace_budget` (default 48 GB of the B200's 180 GB) the queries are processed in
-    blocks -- queries are independent, the answer is the same."""
+    The workspace holds the 4-byte bound matrix per (query, train) pair and room for
+    survivor_cap (default SURVIVOR_CAP) of the pairs as survivors and as two-stage list entries
+    (20 bytes each; config 2 uses 3.6 % and 5.7 %) -- by default for calls above CAP_MIN_PAIRS
+    pairs; smaller ones keep the full layout.  A call that needs more is detected
+    (nndtw_classify_overflowed, one stream synchronisation per call) and rerun with the full
+    layout (every pair: 24 bytes per pair); survivor_cap >= 1 uses the full layout directly.
+    When the workspace exceeds `workspace_budget` (default 48 GB of the B200's 180 GB) the
+    queries are processed in blocks -- queries are independent, the answer is the same."""
     if check and not check_finite(q, stream):
         raise NNDTWError("queries contain NaN or infinity")
     budget = WORKSPACE_BUDGET if workspace_budget is None else int(workspace_budget)
+    frac = SURVIVOR_CAP if survivor_cap is None else float(survivor_cap)
     nq = q.shape[0]
     nt = model.t.shape[0]
-    blk = nq
+    # (by default only large calls are capped: below 2^24 pairs the full layout is <= 400 MB and
+    # a capped call would add a host synchronisation for nothing)
+    capped = frac < 1.0 and (survivor_cap is not None or nq * nt > CAP_MIN_PAIRS)
     lib = load()
-    while blk > 1 and lib.nndtw_classify_workspace_bytes(blk, nt, model.L, model.w) > budget:
+
+    def max_pairs(b: int) -> int | None:
+        return int(frac * b * nt) + 1 if capped else None
+
+    def ws_bytes(b: int) -> int:
+        if capped:
+            return lib.nndtw_classify_workspace_bytes_capped(b, nt, model.L, model.w, max_pairs(b))
+        return lib.nndtw_classify_workspace_bytes(b, nt, model.L, model.w)
+
+    blk = nq
+    while blk > 1 and ws_bytes(blk) > budget:
         blk = (blk + 1) // 2
-    if blk >= nq:
-        key, _, st = classify_keys(model, q, exact=True, stats=stats, stream=stream,
-                                   level_stats=level_stats)
-    else:
-        keys, st = [], None
-        for i in range(0, nq, blk):
-            k, _, s = classify_keys(model, q[i:i + blk], exact=True, stats=stats, stream=stream,
-                                    level_stats=level_stats)
-            keys.append(k)
-            st = merge_stats(st, s) if stats else None
-        key = torch.cat(keys)
+    keys, st = [], None
+    for i in range(0, max(nq, 1), max(blk, 1)):
+        qb = q[i:i + blk]
+        k, ws, s = classify_keys(model, qb, exact=True, stats=stats, stream=stream,
+                                 level_stats=level_stats, max_pairs=max_pairs(qb.shape[0]))
+        if capped and qb.shape[0] > 0 and classify_overflowed(model, qb.shape[0], ws, stream):
+            # more survivors than reserved: rerun this block with room for every pair
+            pred = classify(model, qb, stats=stats, check=False, stream=stream,
+                            workspace_budget=budget, level_stats=level_stats, survivor_cap=1.0)
+            k, s = pred.key, pred.stats
+        keys.append(k)
+        st = merge_stats(st, s) if stats else None
+    key = keys[0] if len(keys) == 1 else torch.cat(keys)
     idx, lab, dist = finalize(key, model.labels, 0, stream)
-    return Prediction(idx, lab, dist, st)
+    return Prediction(idx, lab, dist, st, key)
 
 
 def loocv_window(x: torch.Tensor, labels: torch.Tensor, windows, v: int = 5, q_begin: int = 0,
@@ -493,13 +535,15 @@ class GraphedClassifier:
         self.q = torch.zeros((nq, model.L), dtype=torch.float32, device=dev)
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))
+        # the full workspace layout: a capped one needs a host check of its overflow word after
+        # every call, which a graph cannot contain
         with torch.cuda.stream(side):  # warm-up: workspace, kernel attributes
-            classify(model, self.q, check=False)
+            classify(model, self.q, check=False, survivor_cap=1.0)
         torch.cuda.current_stream(dev).wait_stream(side)
         torch.cuda.synchronize(dev)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self.pred = classify(model, self.q, check=False)
+            self.pred = classify(model, self.q, check=False, survivor_cap=1.0)
 
     def __call__(self, q: torch.Tensor) -> Prediction:
         self.q.copy_(q, non_blocking=True)

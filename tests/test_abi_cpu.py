@@ -59,6 +59,26 @@ def test_host_only_calls(lib):
     assert lib.nndtw_loocv_workspace_bytes(300, 64, 0, 300) > 300 * 64 * 8
 
 
+def test_capped_workspace_sizes(lib):
+    """nndtw_classify_workspace_bytes_capped: 20 bytes per reserved pair on top of the bound
+    matrix and the fixed part, never more than the full layout, at least the seed rounds."""
+    import ctypes as C
+    f = lib.nndtw_classify_workspace_bytes_capped
+    f.restype = C.c_size_t
+    f.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int64]
+    full = lib.nndtw_classify_workspace_bytes(10000, 100000, 512, 103)
+    a = f(10000, 100000, 512, 103, 10 ** 8)
+    b = f(10000, 100000, 512, 103, 2 * 10 ** 8)
+    assert a < b < full
+    assert abs((b - a) - 20 * 10 ** 8) <= 4 * 256
+    assert f(10000, 100000, 512, 103, 10 ** 12) == full      # capacity >= every pair: full
+    assert f(10000, 100000, 512, 103, -1) == full
+    assert f(10000, 100000, 512, 103, 0) == f(10000, 100000, 512, 103, 2 * 10000 + 2)
+    # config 2 at the default 1/8: about a quarter of the full layout's 24 bytes per pair
+    c = f(10000, 100000, 512, 103, 10 ** 9 // 8 + 1)
+    assert c < 0.3 * full
+
+
 def test_binding_rejects_bad_tensors():
     import torch
     from paper_1808_09617_b200 import nndtw
