@@ -87,6 +87,9 @@ typedef struct {
     float ms_envelopes, ms_lb, ms_dtw, ms_other;
     /* the part of ms_lb spent in the sparse bridge kernel (two-stage S2; 0 otherwise) */
     float ms_lb_bridge;
+    /* S4 band-limited pass (wide windows): survivors whose
+     * band-edge cells came within the threshold and were rerun with the full window */
+    int64_t dtw_fallback;
 } nndtw_stats;
 
 /* Library identity and introspection. */

@@ -95,6 +95,7 @@ struct ClassifyWs {
     unsigned long long *counters;  // CNT_N + 4 (seed count, item count, log count, overflow)
     unsigned long long *seed_count, *main_count, *log_count;
     unsigned long long *cap_overflow;  // set when a survivor or list count exceeded item_cap
+    unsigned long long *fb_count;      // S4 band-limited pass: items left for the full window
     nndtw_kim *qkim;
     unsigned long long *minkey, *f64key, *resolve_out;
     unsigned *overflow;
@@ -109,6 +110,7 @@ struct ClassifyWs {
     TieEntry *log;
     unsigned long long log_cap;
     long long *cells_prefix;
+    long long *cells_prefix2;  // in-band cells of the band-limited pass's window
     float *qU, *qL;  // query envelopes (symmetric bound)
     // two-stage S2 (lb_sparse.cu): per-train-series lists of the queries left after stage A
     long long *col_count, *col_off, *col_fill;
@@ -141,11 +143,12 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L,
         return p;
     };
     const size_t q1 = (size_t)(nq > 0 ? nq : 1);
-    W.counters = (unsigned long long *)take(sizeof(unsigned long long) * (CNT_N + 4));
+    W.counters = (unsigned long long *)take(sizeof(unsigned long long) * (CNT_N + 5));
     W.seed_count = W.counters ? W.counters + CNT_N : nullptr;
     W.main_count = W.counters ? W.counters + CNT_N + 1 : nullptr;
     W.log_count = W.counters ? W.counters + CNT_N + 2 : nullptr;
     W.cap_overflow = W.counters ? W.counters + CNT_N + 3 : nullptr;
+    W.fb_count = W.counters ? W.counters + CNT_N + 4 : nullptr;
     W.qkim = (nndtw_kim *)take(sizeof(nndtw_kim) * q1);
     W.minkey = (unsigned long long *)take(8 * q1);
     W.f64key = (unsigned long long *)take(8 * q1);
@@ -166,6 +169,7 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L,
     }
     W.log = (TieEntry *)take(sizeof(TieEntry) * (size_t)W.log_cap);
     W.cells_prefix = (long long *)take(sizeof(long long) * (size_t)(2 * L));
+    W.cells_prefix2 = (long long *)take(sizeof(long long) * (size_t)(2 * L));
     W.qU = (float *)take(sizeof(float) * q1 * (size_t)L);  // symmetric bound: query envelopes
     W.qL = (float *)take(sizeof(float) * q1 * (size_t)L);
     const size_t t1 = (size_t)(nt > 0 ? nt : 1);
@@ -353,7 +357,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     tm.mark();  // 0
     if (do_seed) {
         launch_classify_init(nq, key, W.minkey, W.f64key, W.resolve_out, W.overflow, W.tiecnt,
-                             W.counters, CNT_N + 4, W.buckets, st);
+                             W.counters, CNT_N + 5, W.buckets, st);
         launch_cells_prefix(L, w, W.cells_prefix, st);
     }
     tm.mark();  // 1
@@ -471,10 +475,24 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     }
     tm.mark();  // 4
     if (nt > 0 && whole) {
-        // S4/S5: DTW with early abandoning on the survivors
+        // S4/S5: DTW with early abandoning on the survivors.  Wide windows first run the
+        // band-limited pass (window wb < w): exact for every
+        // item whose band edges stay above the threshold; the others are appended after the
+        // survivors and rerun with the full window below.
+        const int wb = dtw_kernel_kind(L, w) == 1 ? band_adapt_window(L, w) : -1;
+        bool adapted = false;
+        if (wb >= 0) {
+            launch_cells_prefix(L, wb, W.cells_prefix2, st);
+            cudaMemsetAsync(W.fb_count, 0, sizeof(unsigned long long), st);
+            adapted = dispatch_dtw(q, t, nq, nt, W.items, W.main_count, W.item_cap, nullptr,
+                                   nullptr, 0, L, w, 0, key, index_base, eps_t, log, cnt,
+                                   W.cells_prefix2, nullptr, nullptr, st, sms, W.apad,
+                                   W.apad_cap, wb, W.items, W.fb_count, 0) == 0;
+        }
         rc = dispatch_dtw(q, t, nq, nt, W.items, W.main_count, W.item_cap, nullptr, nullptr, 0, L, w, 0,
                           key, index_base, eps_t, log, cnt, W.cells_prefix, nullptr, nullptr,
-                          st, sms, W.apad, W.apad_cap);
+                          st, sms, W.apad, W.apad_cap, -1, nullptr,
+                          adapted ? W.fb_count : nullptr, adapted ? 1 : 0);
         if ((rc = dtw_fail(rc, L, w))) return rc;
     } else if (nt > 0 && dtw_a) {
         // the survivors of buckets < split_b: items [0, base[split_b]) (the bucket-major list)
@@ -537,6 +555,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
             stats->dtw_abandoned += (int64_t)h[CNT_ABANDONED];
             stats->cells += (int64_t)h[CNT_CELLS];
             stats->near_tie_pairs += (int64_t)h[CNT_TIES];
+            stats->dtw_fallback += (int64_t)h[CNT_FALLBACK];
             stats->rounds += 1;
         }
         stats->launches += (int32_t)(launches_total() - launches0);

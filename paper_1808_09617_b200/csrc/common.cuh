@@ -210,6 +210,6 @@ struct TieLog {
 // Per-call device counters (stats); index meaning below.
 enum { CNT_ITEMS = 0, CNT_ABANDONED = 1, CNT_CELLS = 2, CNT_SURVIVORS = 3, CNT_TIES = 4,
        CNT_SKIPPED = 5, CNT_PRUNED_KIM = 8, CNT_PRUNED_BANDS = 9, CNT_PRUNED_KEOGH = 10,
-       CNT_SEED2 = 11, CNT_N = 12 };
+       CNT_SEED2 = 11, CNT_FALLBACK = 12, CNT_N = 13 };
 
 }  // namespace nndtw

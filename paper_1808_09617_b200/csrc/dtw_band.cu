@@ -48,6 +48,14 @@ struct BandParams {
     const float *Apad;                    // GA variant: A rows with their pads, [na][seglen]
     float *apad_ws;                       // search mode, nullable: room for Apad
     int64_t apad_cap;                     // floats available at apad_ws
+    // Band-limited pass (ADAPT, search mode): the layout's window w is narrower than the
+    // distance's; an item whose band-edge cells come within the threshold is appended to the
+    // item array after the survivors (fb_items[*nitems_dev + k], k = atomicAdd(fb_count)) for
+    // the full-window pass.  fbsel (full-window pass): run those appended items -- or, if they
+    // did not all fit below item_cap, every survivor again.
+    Item *fb_items;
+    unsigned long long *fb_count;
+    int fbsel;
 };
 
 // An opaque copy: the compiler cannot rematerialise the value (it would otherwise recompute
@@ -71,7 +79,7 @@ constexpr int band_min_blocks() {
     return (R <= 24 || (R == 26 && KM >= 1)) ? 2 : 1;
 }
 
-template <int R, int KM, bool PACK, bool GA = false>
+template <int R, int KM, bool PACK, bool GA = false, bool ADAPT = false>
 __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(BandParams p) {
     constexpr bool ALIGNED = KM >= 1;
     constexpr bool NOMASK = KM == 2;
@@ -125,9 +133,17 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
     const float nbmask_hi = (g == G - 1) ? kInf : 0.0f;
 
     int64_t nitems = p.nitems_host;
+    int64_t ioff = 0;  // fbsel: the appended items start after the survivors
     if (p.mode == 0) {
         unsigned long long c = *p.nitems_dev;
         nitems = (int64_t)(c < p.item_cap ? c : p.item_cap);
+        if (p.fbsel) {
+            const unsigned long long f = *p.fb_count;
+            if (c + f <= p.item_cap) {
+                ioff = (int64_t)c;
+                nitems = (int64_t)f;
+            }  // else: not all were stored -- every survivor again (exact, slower)
+        }
     }
     int64_t it = gid;
     bool active = valid_lane && it < nitems;
@@ -148,6 +164,7 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
     // the hot loop).
     bool skipping = false;
     long long my_skipped = 0;
+    float e0 = kInf, e1 = kInf;             // ADAPT: band-edge minima over the period
     unsigned long long kstart = 0;
 #ifdef NNDTW_PROFILE_SETUP
     // instrumentation build only (tools/setup_share.sh): cycles spent waiting for item setups
@@ -161,7 +178,7 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
         unsigned a_idx, b_idx;
         float ilb = 0.0f;
         if (p.mode == 0) {
-            Item itm = p.items[it];
+            Item itm = p.items[ioff + it];
             a_idx = itm.q;
             b_idx = itm.n;
             ilb = itm.lb;
@@ -196,7 +213,7 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
         if (p.mode == 0 && g == 0 && p.vec4) {
             const int64_t nx = it + ngroups;
             if (nx < nitems) {
-                const unsigned nb = p.items[nx].n;
+                const unsigned nb = p.items[ioff + nx].n;
                 bulk_prefetch_l2(p.B + (int64_t)nb * L, (unsigned)L * 4u);
             }
         }
@@ -275,6 +292,10 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
                         const float lo = (r == 0) ? nlo : D[r - 1];
                         D[r] = fmaf(t0, t0, fminf(fminf(D[r], lo), D[r + 1]));
                     }
+                    if (ADAPT) {  // band edges d = -w (lane 0, slot 0) and d = +w (top lane, R-2)
+                        e0 = fminf(e0, D[0]);
+                        e1 = fminf(e1, D[R - 2]);
+                    }
                 }
                 {  // diagonal t+1 (odd offsets r = 2m+1); r = R-1 carries the kill scale
                     float nhi;
@@ -328,13 +349,38 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
         unsigned ballot = __ballot_sync(0xffffffffu, vote);
         bool done = active && per == p.nper;
         bool abandon = active && !done && ((ballot & gbits) == gbits);
+        bool fired = false;
+        if (ADAPT) {
+            // an edge cell within the threshold: a path leaving the band might be cheaper than
+            // the band's value, so the item goes to the full-
+            // window pass; otherwise every out-of-band cell exceeds the threshold and the
+            // band's values, abandon and result are the full window's
+            const bool near = (g == 0 && e0 <= thr) || (g == G - 1 && e1 <= thr);
+            const unsigned fb = __ballot_sync(0xffffffffu, near);
+            fired = active && !skipping && (fb & gbits) != 0u;
+            done = done && !fired;
+            abandon = abandon && !fired;
+            e0 = kInf;
+            e1 = kInf;
+        }
 #ifdef NNDTW_TRACE
         if (active && p.mode == 0 && blockIdx.x == 0 && warp == 0 && lane < 2)
             printf("TRACE lane=%d it=%lld q=%u n=%u per=%d/%d lmin=%g thr=%g D0=%g done=%d ab=%d\n",
                    lane, (long long)it, qcur, ncur, per, p.nper, lmin, thr, D[0], (int)done,
                    (int)abandon);
 #endif
-        if (__any_sync(0xffffffffu, done || abandon)) {  // rare: once per item per group
+        if (__any_sync(0xffffffffu, done || abandon || fired)) {  // rare: once per item per group
+            if (ADAPT && fired && g == 0) {
+                const unsigned long long k = atomicAdd(p.fb_count, 1ull);
+                const unsigned long long pos = (unsigned long long)nitems + k;
+                if (pos < p.item_cap) p.fb_items[pos] = Item{qcur, ncur, p.items[ioff + it].lb};
+                if (p.counters != nullptr) {
+                    atomicAdd(p.counters + CNT_FALLBACK, 1ull);
+                    int klast = p.k0 + per * R - 1;
+                    if (klast > 2 * L - 2) klast = 2 * L - 2;
+                    my_cells += klast >= 0 ? p.cells_prefix[klast] : 0;
+                }
+            }
             if (done && g == g0) {  // (most items end abandoned: the result slot only here)
                 float res = D[0];
 #pragma unroll
@@ -363,8 +409,8 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
                 }
             }
             if (abandon && p.mode == 1 && g == 0) p.out[it] = kInf;
-            if (done || abandon) {
-                if (g == 0 && p.counters != nullptr) {
+            if (done || abandon || fired) {
+                if (!fired && g == 0 && p.counters != nullptr) {
                     if (skipping) {
                         my_skipped += 1;
                     } else {
@@ -399,7 +445,7 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
 #endif
     if (p.counters != nullptr && valid_lane && g == 0 && my_skipped > 0)
         atomicAdd(p.counters + CNT_SKIPPED, (unsigned long long)my_skipped);
-    if (p.counters != nullptr && valid_lane && g == 0 && my_items > 0) {
+    if (p.counters != nullptr && valid_lane && g == 0 && (my_items > 0 || my_cells > 0)) {
         atomicAdd(p.counters + CNT_ITEMS, (unsigned long long)my_items);
         atomicAdd(p.counters + CNT_ABANDONED, (unsigned long long)my_aband);
         atomicAdd(p.counters + CNT_CELLS, (unsigned long long)my_cells);
@@ -532,9 +578,9 @@ __global__ void k_pad_rows(const float *__restrict__ A, int64_t na, int L, int p
     }
 }
 
-template <int R, int KM, bool PACK, bool GA = false>
+template <int R, int KM, bool PACK, bool GA = false, bool ADAPT = false>
 static int launch_band_t(BandParams &p, const BandChoice &c, cudaStream_t st, int num_sms) {
-    auto kern = k_dtw_band<R, KM, PACK, GA>;
+    auto kern = k_dtw_band<R, KM, PACK, GA, ADAPT>;
     const int block = 32 * c.warps;
     size_t smem = (size_t)c.warps * p.gpw * (GA ? 1 : 2) * p.seglen * sizeof(float);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -628,6 +674,63 @@ int launch_dtw_band(BandParams p, cudaStream_t st, int num_sms) {
         default:
             return -1;
     }
+}
+
+// ---- band-limited pass ------------------------------------
+// The window wb of the band-limited pass for a distance window w, or -1: the R = 26 full-warp
+// layout (the GA variant, 2wb + 2 = 26 G with G * gpw = 32) with the largest wb <= w / 2.
+int band_adapt_window(int L, int w) {
+    const char *ee = getenv("NNDTW_ADAPT");  // 0 = off; an integer > 1 forces that wb
+    const int env = ee ? atoi(ee) : -1;
+    if (w > L - 1) w = L - 1;
+    if (env == 0 || L % 4 != 0) return -1;
+    int best = -1;
+    for (int G = 1; G <= 32; G <<= 1) {
+        const int wb = 13 * G - 1;
+        if (env > 1 ? wb == env : 2 * wb <= w) best = wb > best ? wb : best;
+    }
+    if (best < 0 || best >= w) return -1;
+    if (env < 0 && w < 64) return -1;  // default: wide windows only
+    return best;
+}
+
+// Launch the band-limited pass: p.w = wb (band_adapt_window), search mode, p.fb_items /
+// p.fb_count set.  -1 if the layout cannot run (the caller then runs the full window only).
+int launch_dtw_band_adapt(BandParams p, cudaStream_t st, int num_sms) {
+    if (p.mode != 0 || p.apad_ws == nullptr || p.fb_count == nullptr || p.fb_items == nullptr)
+        return -1;
+    const int G = (2 * p.w + 2) / 26;
+    if (G * 26 != 2 * p.w + 2 || G < 1 || G > 32 || (32 % G) != 0) return -1;
+    BandChoice c{};
+    c.R = 26;
+    c.G = G;
+    c.gpw = 32 / G;
+    c.km = 2;
+    c.pack = true;
+    band_geometry(26, G, p.L, p.w, c);
+    // GA rows must be 16-byte aligned (cp.async16, the padded query copy); one staged row per
+    // group, so consecutive groups sit seglen words apart: seglen = 4 (mod 32) staggers up to 8
+    // groups of a warp over distinct bank quads
+    while (c.seglen % 32 != 4) ++c.seglen;
+    const double warp_smem = (double)c.gpw * 2 * c.seglen * sizeof(float);
+    int warps = (int)((226.0 * 1024) / warp_smem);
+    if (warps < 1) return -1;
+    c.warps = warps > 8 ? 8 : warps;
+    p.G = c.G;
+    p.gpw = c.gpw;
+    p.k0 = c.k0;
+    p.nper = c.nper;
+    p.padl = c.padl;
+    p.seglen = c.seglen;
+    p.vec4 = (p.L % 4 == 0 && c.seglen % 4 == 0 && c.padl % 4 == 0 &&
+              ((uintptr_t)p.A % 16) == 0 && ((uintptr_t)p.B % 16) == 0) ? 1 : 0;
+    if (!p.vec4 || p.dbg_na <= 0 || p.dbg_na * (int64_t)c.seglen > p.apad_cap) return -1;
+    const int64_t n = p.dbg_na * (int64_t)c.seglen;
+    const int64_t blocks = (n + 255) / 256 < 4 * num_sms ? (n + 255) / 256 : 4 * num_sms;
+    k_pad_rows<<<(unsigned)blocks, 256, 0, st>>>(p.A, p.dbg_na, p.L, p.padl, p.seglen, p.apad_ws);
+    count_launch(1, "k_pad_rows");
+    p.Apad = p.apad_ws;
+    return launch_band_t<26, 2, true, true, true>(p, c, st, num_sms);
 }
 
 // ---- w = 0: DTW_0 is the squared Euclidean distance; one warp per item -------------
@@ -733,9 +836,13 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
                  int mode, unsigned long long *key, int64_t index_base, float eps_t, TieLog log,
                  unsigned long long *counters, const long long *cells_prefix,
                  const float *cutoff, float *out, cudaStream_t st, int num_sms,
-                 float *apad_ws, int64_t apad_cap) {
+                 float *apad_ws, int64_t apad_cap, int adapt_w, Item *fb_items,
+                 unsigned long long *fb_count, int fbsel) {
     if (w > L - 1) w = L - 1;
     BandParams p;
+    p.fb_items = fb_items;
+    p.fb_count = fb_count;
+    p.fbsel = fbsel;
     p.A = A;
     p.B = B;
     p.items = items;
@@ -765,6 +872,10 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
     p.Apad = nullptr;
     p.apad_ws = apad_ws;
     p.apad_cap = apad_cap;
+    if (adapt_w >= 0) {  // the band-limited pass (its caller checked band_adapt_window)
+        p.w = adapt_w;
+        return launch_dtw_band_adapt(p, st, num_sms);
+    }
     const int kind = dtw_kernel_kind(L, w);
     if (kind == 0) return launch_dtw_w0(p, st, num_sms);
     if (kind == 1) {

@@ -103,13 +103,17 @@ int launch_count_errors(const unsigned long long *key, int64_t nq, const int32_t
 // S4 dispatch: picks the band-wavefront kernel (2w+2 <= 32*32 slots) or the row-strip kernel
 // (long windows).  mode 0 = search (items + device count, atomicMin into key, tie log),
 // mode 1 = batch (ia/ib/cutoff/out, nitems_host pairs).  Returns 0 or an NNDTW_E_* code.
+// S4 band-limited pass (dtw_band.cu): its window for a distance window w, or -1
+int band_adapt_window(int L, int w);
 int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const Item *items,
                  const unsigned long long *nitems_dev, unsigned long long item_cap,
                  const int32_t *ia, const int32_t *ib, int64_t nitems_host, int L, int w,
                  int mode, unsigned long long *key, int64_t index_base, float eps_t, TieLog log,
                  unsigned long long *counters, const long long *cells_prefix,
                  const float *cutoff, float *out, cudaStream_t st, int num_sms,
-                 float *apad_ws = nullptr, int64_t apad_cap = 0);
+                 float *apad_ws = nullptr, int64_t apad_cap = 0, int adapt_w = -1,
+                 Item *fb_items = nullptr, unsigned long long *fb_count = nullptr,
+                 int fbsel = 0);
 // floats per query row of the band kernel's padded A copy (an upper bound of its row length
 // seglen for any window: padl + L + padr <= L + w + R + 48)
 inline int64_t band_apad_row_floats(int L) { return 2 * (int64_t)L + 128; }

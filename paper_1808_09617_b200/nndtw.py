@@ -53,7 +53,8 @@ class Stats(C.Structure):
                 ("dtw_abandoned", C.c_int64), ("cells", C.c_int64),
                 ("near_tie_pairs", C.c_int64), ("rounds", C.c_int32), ("launches", C.c_int32),
                 ("ms_envelopes", C.c_float), ("ms_lb", C.c_float), ("ms_dtw", C.c_float),
-                ("ms_other", C.c_float), ("ms_lb_bridge", C.c_float)]
+                ("ms_other", C.c_float), ("ms_lb_bridge", C.c_float),
+                ("dtw_fallback", C.c_int64)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
