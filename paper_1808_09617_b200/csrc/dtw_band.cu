@@ -335,6 +335,10 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
                     const float hi = (r == R - 1) ? nhi : D[r + 1];
                     D[r] = fmaf(tt, tt, fminf(fminf(D[r], lo), hi));
                 }
+                if (ADAPT && phi == 0) {  // band edges d = -w (lane 0, slot 0), +w (top, R-2)
+                    e0 = fminf(e0, D[0]);
+                    e1 = fminf(e1, D[R - 2]);
+                }
             }
         }
         per = active ? per + 1 : 0;  // idle groups replay period 0 (stay in bounds)
@@ -678,15 +682,19 @@ int launch_dtw_band(BandParams p, cudaStream_t st, int num_sms) {
 
 // ---- band-limited pass ------------------------------------
 // The window wb of the band-limited pass for a distance window w, or -1: the R = 26 full-warp
-// layout (the GA variant, 2wb + 2 = 26 G with G * gpw = 32) with the largest wb <= w / 2.
+// aligned layout (the GA variant, 2wb + 2 = 26 G with G * gpw = 32) with the largest
+// wb <= w / 2.  (Measured on config 2 against R = 12, 14, 20, 22 layouts of wb 39-55, by
+// NNDTW_ADAPT_R builds: 57.6 k queries/s for R = 26, wb = 51; 53.2 k for R = 14, wb = 55;
+// 48.9 k, 50.9 k, 45.7 k for the others.)
 int band_adapt_window(int L, int w) {
     const char *ee = getenv("NNDTW_ADAPT");  // 0 = off; an integer > 1 forces that wb
     const int env = ee ? atoi(ee) : -1;
     if (w > L - 1) w = L - 1;
     if (env == 0 || L % 4 != 0) return -1;
+    constexpr int R = 26;
     int best = -1;
     for (int G = 1; G <= 32; G <<= 1) {
-        const int wb = 13 * G - 1;
+        const int wb = (R / 2) * G - 1;
         if (env > 1 ? wb == env : 2 * wb <= w) best = wb > best ? wb : best;
     }
     if (best < 0 || best >= w) return -1;
@@ -699,23 +707,34 @@ int band_adapt_window(int L, int w) {
 int launch_dtw_band_adapt(BandParams p, cudaStream_t st, int num_sms) {
     if (p.mode != 0 || p.apad_ws == nullptr || p.fb_count == nullptr || p.fb_items == nullptr)
         return -1;
-    const int G = (2 * p.w + 2) / 26;
-    if (G * 26 != 2 * p.w + 2 || G < 1 || G > 32 || (32 % G) != 0) return -1;
+    constexpr int R = 26;
+    const int G = (2 * p.w + 2) / R;
+    if (G * R != 2 * p.w + 2 || G < 1 || G > 32 || (32 % G) != 0) return -1;
     BandChoice c{};
-    c.R = 26;
+    c.R = R;
     c.G = G;
     c.gpw = 32 / G;
     c.km = 2;
     c.pack = true;
-    band_geometry(26, G, p.L, p.w, c);
+    band_geometry(R, G, p.L, p.w, c);
     // GA rows must be 16-byte aligned (cp.async16, the padded query copy); one staged row per
     // group, so consecutive groups sit seglen words apart: seglen = 4 (mod 32) staggers up to 8
     // groups of a warp over distinct bank quads
     while (c.seglen % 32 != 4) ++c.seglen;
-    const double warp_smem = (double)c.gpw * 2 * c.seglen * sizeof(float);
-    int warps = (int)((226.0 * 1024) / warp_smem);
-    if (warps < 1) return -1;
-    c.warps = warps > 8 ? 8 : warps;
+    // CTA size: the most resident warps (one staged row per group; at most 16 warps per SM
+    // at the 128-register cap)
+    const double warp_smem = (double)c.gpw * c.seglen * sizeof(float);
+    int bestw = 0, best_res = 0;
+    for (int wv = 1; wv <= 8; ++wv) {
+        int ctas = (int)((227.0 * 1024) / (wv * warp_smem));
+        if (ctas > 16 / wv) ctas = 16 / wv;
+        if (ctas * wv >= best_res && ctas > 0) {
+            best_res = ctas * wv;
+            bestw = wv;
+        }
+    }
+    if (bestw < 1) return -1;
+    c.warps = bestw;
     p.G = c.G;
     p.gpw = c.gpw;
     p.k0 = c.k0;
