@@ -403,11 +403,23 @@ def main():
 
     # ---- per-level prune counters (one untimed call; the level pass is not in the step) ----
     levels = None
+    adapt_env = os.environ.get("NNDTW_ADAPT")
     if not sharded:
         model_l = nndtw.Model(train_d, labels_d[lo:hi], w, V, index_base=lo, check=False)
         st_l = nndtw.classify(model_l, test_d, stats=True, check=False, level_stats=True).stats
         levels = {k: st_l[k] for k in ("pruned_kim", "pruned_bands", "pruned_keogh",
-                                       "survivors")}
+                                       "survivors", "dtw_fallback")}
+        # the survivor round's cells without the band-limited S4 pass (DESIGN.md "S4 band-limited
+        # pass"): the full-window work the same answer takes, for the full-window-equivalent rate
+        os.environ["NNDTW_ADAPT"] = "0"
+        try:
+            st_f = nndtw.classify(model_l, test_d, stats=True, check=False).stats
+        finally:
+            if adapt_env is None:
+                del os.environ["NNDTW_ADAPT"]
+            else:
+                os.environ["NNDTW_ADAPT"] = adapt_env
+        levels["cells_full_window"] = st_f["cells"]
         del model_l
 
     # ---- e2e through the public API with host buffers ---------------------------------
@@ -473,6 +485,16 @@ def main():
                 "peak_source": f"{num_sms} SMs x 64 cells/clk (FMNMX3 at 16 lanes/clk/SMSP, "
                                f"tools/pipebench.cu) x {sm_mhz:.0f} MHz ({src})",
                 "ms_per_step": acc_tot["ms_dtw"] / args.steps}
+    if levels and levels.get("cells_full_window") and acc_tot["ms_dtw"] > 0 and \
+            levels["cells_full_window"] > 1.01 * acc_tot["cells"] / args.steps:
+        # band-limited pass on: the cells it computes are fewer than the full window's; the
+        # same answer over the full window takes cells_full_window (untimed run, pass off)
+        eq = levels["cells_full_window"] / (acc_tot["ms_dtw"] / args.steps * 1e-3) / 1e9 / world
+        roof_dtw["full_window_equivalent"] = {
+            "cells_per_step": levels["cells_full_window"], "achieved": eq,
+            "frac": eq / peak_cells if peak_cells else None,
+            "note": "full-window survivor-round cells (NNDTW_ADAPT=0, untimed) / the timed "
+                    "survivor round; achieved/frac above count the cells actually computed"}
     lb_bytes = (Q * L + (hi - lo) * (2 * L + 2 * min(L // 2, V)) + Q * (hi - lo)) * 4.0
     two_stage = acc_tot["ms_lb_bridge"] > 0 and acc_tot["bridge_pairs"] < acc_tot["lb_pairs"]
     if two_stage:

@@ -683,19 +683,29 @@ int launch_dtw_band(BandParams p, cudaStream_t st, int num_sms) {
 // ---- band-limited pass ------------------------------------
 // The window wb of the band-limited pass for a distance window w, or -1: the R = 26 full-warp
 // aligned layout (the GA variant, 2wb + 2 = 26 G with G * gpw = 32) with the largest
-// wb <= w / 2.  (Measured on config 2 against R = 12, 14, 20, 22 layouts of wb 39-55, by
-// NNDTW_ADAPT_R builds: 57.6 k queries/s for R = 26, wb = 51; 53.2 k for R = 14, wb = 55;
-// 48.9 k, 50.9 k, 45.7 k for the others.)
+// wb <= w / 2.  Measured on config 2 (queries/s): R = 26, wb = 51 (G = 4): 57.6 k (13 % of the
+// survivors fall back); R = 20, wb = 79 and R = 22, wb = 87 (G = 8, four groups per warp,
+// hardly any fall back): 49.7 k / 50.1 k; R = 26, wb = 25: 41.1 k; unpacked R = 14, wb = 55:
+// 53.2 k; R = 12, wb = 47: 48.9 k; no pass: 47.9 k.  NNDTW_ADAPT_R (20 / 22 / 26) and
+// NNDTW_ADAPT_FRAC (wb <= frac * w) select others for experiments.
+static int band_adapt_r() {  // experiments: NNDTW_ADAPT_R = 20 / 22 / 26 (default)
+    const char *e = getenv("NNDTW_ADAPT_R");
+    const int r = e ? atoi(e) : 26;
+    return (r == 20 || r == 22) ? r : 26;
+}
+
 int band_adapt_window(int L, int w) {
     const char *ee = getenv("NNDTW_ADAPT");  // 0 = off; an integer > 1 forces that wb
     const int env = ee ? atoi(ee) : -1;
     if (w > L - 1) w = L - 1;
     if (env == 0 || L % 4 != 0) return -1;
-    constexpr int R = 26;
+    const int R = band_adapt_r();
+    const char *ef = getenv("NNDTW_ADAPT_FRAC");  // experiments: wb <= w * frac (default 0.5)
+    const double frac = ef ? atof(ef) : 0.5;
     int best = -1;
     for (int G = 1; G <= 32; G <<= 1) {
         const int wb = (R / 2) * G - 1;
-        if (env > 1 ? wb == env : 2 * wb <= w) best = wb > best ? wb : best;
+        if (env > 1 ? wb == env : wb <= frac * w) best = wb > best ? wb : best;
     }
     if (best < 0 || best >= w) return -1;
     if (env < 0 && w < 64) return -1;  // default: wide windows only
@@ -707,7 +717,7 @@ int band_adapt_window(int L, int w) {
 int launch_dtw_band_adapt(BandParams p, cudaStream_t st, int num_sms) {
     if (p.mode != 0 || p.apad_ws == nullptr || p.fb_count == nullptr || p.fb_items == nullptr)
         return -1;
-    constexpr int R = 26;
+    const int R = band_adapt_r();
     const int G = (2 * p.w + 2) / R;
     if (G * R != 2 * p.w + 2 || G < 1 || G > 32 || (32 % G) != 0) return -1;
     BandChoice c{};
@@ -749,6 +759,8 @@ int launch_dtw_band_adapt(BandParams p, cudaStream_t st, int num_sms) {
     k_pad_rows<<<(unsigned)blocks, 256, 0, st>>>(p.A, p.dbg_na, p.L, p.padl, p.seglen, p.apad_ws);
     count_launch(1, "k_pad_rows");
     p.Apad = p.apad_ws;
+    if (R == 20) return launch_band_t<20, 2, true, true, true>(p, c, st, num_sms);
+    if (R == 22) return launch_band_t<22, 2, true, true, true>(p, c, st, num_sms);
     return launch_band_t<26, 2, true, true, true>(p, c, st, num_sms);
 }
 
