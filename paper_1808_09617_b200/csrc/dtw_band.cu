@@ -164,11 +164,6 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
     // the hot loop).
     bool skipping = false;
     long long my_skipped = 0;
-    // ASYNC (the band-limited pass: eight groups per warp, so an item ends every couple of
-    // periods per warp): a group that moves on issues its row copies and runs one inert period
-    // (all-+inf state, no events) while they land, instead of stalling the warp on the wait
-    constexpr bool ASYNC = ADAPT;
-    bool pending = false;
     float e0 = kInf, e1 = kInf;             // ADAPT: band-edge minima over the period
     unsigned long long kstart = 0;
 #ifdef NNDTW_PROFILE_SETUP
@@ -176,7 +171,7 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
     long long prof_setup = 0;
     const long long prof_t0 = clock64();
 #endif
-    auto setup = [&](bool wait) {
+    auto setup = [&]() {
 #ifdef NNDTW_PROFILE_SETUP
         const long long ps0 = clock64();
 #endif
@@ -223,13 +218,6 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
             }
         }
         if (p.mode == 0) kstart = ld_relaxed_u64(p.key + a_idx);
-        if (ASYNC && !wait) {  // inert until the iteration after next: D all +inf, no events
-#pragma unroll
-            for (int r = 0; r < R; ++r) D[r] = kInf;
-            per = 0;
-            pending = true;
-            return;
-        }
         cp_async_wait_all();
 #ifdef NNDTW_PROFILE_SETUP
         prof_setup += clock64() - ps0;  // (no __syncwarp here: setup runs in divergent code)
@@ -244,23 +232,13 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
         per = 0;
     };
 
-    auto setup_finish = [&]() {  // ASYNC: the wait and state setup of a pending item
-        cp_async_wait_all();
-        skipping = p.items[ioff + it].lb > key_dist(kstart) * (1.0f + p.eps_p);
-#pragma unroll
-        for (int r = 0; r < R; ++r) D[r] = (!skipping && g == g0 && r == r0) ? 0.0f : kInf;
-        per = 0;
-        pending = false;
-    };
-
-    if (active) setup(true);
+    if (active) setup();
     __syncwarp();
 
     // live best-so-far of the group's query, read one period ahead (the abandon test uses the
     // value loaded during the previous period: never tighter than the true live value)
     unsigned long long kprev = kstart;
     while (__any_sync(0xffffffffu, active)) {
-        bool issued_now = false;
         unsigned long long knext = 0;
         if (p.mode == 0 && active) knext = ld_relaxed_u64(p.key + qcur);
 
@@ -363,7 +341,7 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
                 }
             }
         }
-        per = (active && !(ASYNC && pending)) ? per + 1 : 0;  // idle / inert groups replay period 0
+        per = active ? per + 1 : 0;  // idle groups replay period 0 (stay in bounds)
 
         // ---- events: completion / early abandon --------------------------------------
         float lmin = D[0];
@@ -373,9 +351,8 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
         kprev = knext;
         bool vote = !(lmin <= thr);
         unsigned ballot = __ballot_sync(0xffffffffu, vote);
-        const bool live = active && !(ASYNC && pending);
-        bool done = live && per == p.nper;
-        bool abandon = live && !done && ((ballot & gbits) == gbits);
+        bool done = active && per == p.nper;
+        bool abandon = active && !done && ((ballot & gbits) == gbits);
         bool fired = false;
         if (ADAPT) {
             // an edge cell within the threshold: a path leaving the band might be cheaper than
@@ -384,7 +361,7 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
             // band's values, abandon and result are the full window's
             const bool near = (g == 0 && e0 <= thr) || (g == G - 1 && e1 <= thr);
             const unsigned fb = __ballot_sync(0xffffffffu, near);
-            fired = live && !skipping && (fb & gbits) != 0u;
+            fired = active && !skipping && (fb & gbits) != 0u;
             done = done && !fired;
             abandon = abandon && !fired;
             e0 = kInf;
@@ -451,17 +428,12 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
                 it += ngroups;
                 active = it < nitems;
                 if (active) {
-                    setup(false);
-                    issued_now = true;
+                    setup();
                     kprev = kstart;
                 } else {
                     per = 0;  // idle groups replay period 0 (stay in bounds)
                 }
             }
-        }
-        if (ASYNC && pending && !issued_now) {  // issued last iteration: its copies have landed
-            setup_finish();
-            kprev = kstart;
         }
         __syncwarp();
     }
