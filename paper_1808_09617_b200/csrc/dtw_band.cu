@@ -708,7 +708,8 @@ int band_adapt_window(int L, int w) {
         if (env > 1 ? wb == env : wb <= frac * w) best = wb > best ? wb : best;
     }
     if (best < 0 || best >= w) return -1;
-    if (env < 0 && w < 64) return -1;  // default: wide windows only
+    const char *em = getenv("NNDTW_ADAPT_MINW");  // experiments: the smallest w (default 64)
+    if (env < 0 && w < (em ? atoi(em) : 64)) return -1;  // default: wide windows only
     return best;
 }
 
