@@ -70,3 +70,35 @@ def test_adapt_fallback_items_do_not_fit(dev, monkeypatch):
     idx, lab, dist, st2 = _run(dev, ds, w, max_pairs=st["survivors"] + 16)
     _compare(idx, lab, dist, g[f"idx_w{w}"], g[f"label_w{w}"], g[f"dist_w{w}"], "no room")
     assert st2["dtw_fallback"] > 64, st2
+
+
+@pytest.mark.parametrize("shift", [30, 70, 100])
+def test_adapt_warped_neighbours_fall_back_exactly(dev, oracle_lib, shift):
+    """Adversarial for the band edge: every query is a train series shifted by `shift` samples
+    (w = 103, band-limited pass wb = 51), so for shift > 51 its nearest neighbour's warping path
+    leaves the band -- the edge check must send those items to the full window, and every
+    answer must be the fp64 oracle's (exhaustive)."""
+    from paper_1808_09617_b200 import nndtw
+    rng = np.random.default_rng(shift)
+    L, w, ns, nq = 512, 103, 32, 24
+    walk = np.cumsum(rng.standard_normal((ns, L + 2 * shift + 4)), axis=1)
+    # three noisy variants of every source (offsets 0, 1, 2): near-ties the survivor round must
+    # evaluate in full, all of them warped by about `shift` against their query
+    T_ = np.concatenate([walk[:, shift + o:shift + o + L] + 0.05 * rng.standard_normal((ns, L))
+                         for o in (0, 1, 2)])
+    nt = T_.shape[0]
+    src = rng.choice(ns, nq, replace=False)
+    Q_ = walk[src, 2 * shift + 1:2 * shift + 1 + L] + 0.05 * rng.standard_normal((nq, L))
+    z = lambda x: ((x - x.mean(1, keepdims=True)) / x.std(1, keepdims=True)).astype(np.float32)
+    T_, Q_ = z(T_), z(Q_)
+    labels = (np.arange(nt) % 5).astype(np.int32)
+    model = nndtw.Model(T(T_, dev), T(labels, dev), w, 5)
+    key, ws, st = nndtw.classify_keys(model, T(Q_, dev), stats=True)
+    idx, lab, dist = nndtw.finalize(key, model.labels)
+    ridx, rdist = oracle_lib.nn(Q_, T_, w, mode="exhaustive")
+    idx = idx.cpu().numpy()
+    assert np.array_equal(idx, ridx), (shift, np.nonzero(idx != ridx)[0][:8])
+    d = dist.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(d - rdist) <= 1e-5 * rdist + 1e-30)
+    if shift > 51:
+        assert st["dtw_fallback"] > 0, st
