@@ -477,7 +477,11 @@ def main():
     dominant = "dtw" if acc_tot["ms_dtw"] >= acc_tot["ms_lb"] else "lb"
     traffic = ncu_traffic()
     dtw_kernel = lib.nndtw_dtw_kernel_name(L, w).decode()  # the kernel dispatch_dtw runs
-    roof_dtw = {"kernel": f"{dtw_kernel} (S4 survivor round)", "bound": "alu",
+    wb = int(lib.nndtw_band_limited_window(L, w))
+    dtw_label = (f"{dtw_kernel} (S4 survivor round: band-limited pass wb={wb} + full-window "
+                 f"pass for the survivors it sends back)" if wb >= 0 else
+                 f"{dtw_kernel} (S4 survivor round)")
+    roof_dtw = {"kernel": dtw_label, "bound": "alu",
                 "achieved": dtw_gcups, "peak": peak_cells, "unit": "Gcells/s",
                 "frac": dtw_gcups / peak_cells if peak_cells else None,
                 "traffic": traffic.get(dtw_kernel, {}).get("bytes_per_launch")

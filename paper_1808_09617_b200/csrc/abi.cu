@@ -614,6 +614,11 @@ const char *nndtw_dtw_kernel_name(int32_t L, int32_t w) {
     static const char *names[3] = {"k_dtw_w0", "k_dtw_band", "k_dtw_strip"};
     return names[dtw_kernel_kind(L, w)];
 }
+int32_t nndtw_band_limited_window(int32_t L, int32_t w) {
+    if (L < 2 || w < 0) return -1;
+    if (w > L - 1) w = L - 1;
+    return dtw_kernel_kind(L, w) == 1 ? band_adapt_window(L, w) : -1;
+}
 int64_t nndtw_launch_count(void) { return launches_total(); }
 
 int nndtw_check_device(void) {

@@ -83,6 +83,7 @@ _SIGS = {
     "nndtw_launch_count": (_I64, []),
     "nndtw_check_device": (C.c_int, []),
     "nndtw_dtw_kernel_name": (C.c_char_p, [_I32, _I32]),
+    "nndtw_band_limited_window": (_I32, [_I32, _I32]),
     "nndtw_check_finite": (C.c_int, [_P, _I64, _P, _P]),
     "nndtw_envelopes": (C.c_int, [_P, _I64, _I32, _I32, _P, _P, _P, _P]),
     "nndtw_series_stats": (C.c_int, [_P, _I64, _I32, _P, _P]),

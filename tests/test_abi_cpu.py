@@ -129,3 +129,25 @@ def test_dtw_kernel_name_rule(lib):
     assert name(2048, 5000) == "k_dtw_strip"      # clamped to L-1
     assert name(1024, 511) == "k_dtw_band"        # R = 32 is the only band layout (2w+2 = 1024)
     assert name(1, 0) == "" and name(16, -1) == ""
+
+
+def test_band_limited_window_rule(lib, monkeypatch):
+    """nndtw_band_limited_window (host-only): the band of the S4 band-limited pass -- the
+    R = 26 full-warp layout's wb = 13 G - 1 <= w / 2 for band-kernel windows w >= 64, else -1."""
+    wb = lib.nndtw_band_limited_window
+    monkeypatch.delenv("NNDTW_ADAPT", raising=False)
+    assert wb(512, 103) == 51          # config 2
+    assert wb(256, 128) == 51          # config 1, p = 50
+    assert wb(300, 210) == 103
+    assert wb(256, 52) == -1           # w < 64
+    assert wb(256, 255) == -1          # full window: the row-strip kernel
+    assert wb(2048, 2047) == -1        # config 4
+    assert wb(510, 103) == -1          # L % 4 != 0 (the layout's 16-byte rows)
+    assert wb(512, 0) == -1 and wb(1, 5) == -1 and wb(16, -1) == -1
+    for w in range(64, 400, 7):
+        b = wb(1024, w)
+        assert b in (-1, 12, 25, 51, 103, 207) and (b == -1 or 2 * b <= w), (w, b)
+    monkeypatch.setenv("NNDTW_ADAPT", "0")
+    assert wb(512, 103) == -1
+    monkeypatch.setenv("NNDTW_ADAPT", "25")
+    assert wb(512, 103) == 25
