@@ -102,8 +102,9 @@ NNDTW_API int64_t nndtw_launch_count(void);
  * windows); "" for invalid arguments.  Host-only (bench / profiling bookkeeping). */
 NNDTW_API const char *nndtw_dtw_kernel_name(int32_t L, int32_t w);
 /* The band window wb of the band-limited S4 pass nndtw_classify's survivor round runs first for
- * (L, w), or -1 when it runs the full window directly (the
- * kernel for w is not the band kernel, w < 64, L % 4 != 0, or NNDTW_ADAPT=0).  Host-only. */
+ * (L, w), or -1 when it runs the full window directly.
+ * Band-kernel windows: wb = 13G - 1 <= w/2 for w >= 64; full windows (the row-strip kernel):
+ * wb <= w/8 where that is >= 103; -1 for L % 4 != 0 or NNDTW_ADAPT=0.  Host-only. */
 NNDTW_API int32_t nndtw_band_limited_window(int32_t L, int32_t w);
 /* NNDTW_OK if the current device is sm_100 (B200); NNDTW_E_ARCH otherwise. */
 NNDTW_API int nndtw_check_device(void);

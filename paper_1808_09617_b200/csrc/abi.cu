@@ -267,6 +267,17 @@ static void exact_local(ClassifyWs &W, const float *q, int64_t nq, const float *
     launch_swap_key(W.resolve_out, nq, key, st);
 }
 
+// The band-limited S4 pass in front of the row-strip kernel (full windows, band wb <= w / 8):
+// on where that band is at least 103 offsets wide (long series: config 4, L = 2048, wb = 207:
+// 11.7 k -> 14.0 k queries/s); at L = 256 (config 1, wb = 25) it was slower (1.03 -> 0.94 M
+// queries/s at w = 255).  NNDTW_ADAPT_FULL=0/1 forces it off/on.
+static int full_window_band(int L, int w) {
+    const int wb = band_adapt_window(L, w, true);
+    const char *e = getenv("NNDTW_ADAPT_FULL");
+    if (e) return e[0] == '1' ? wb : -1;
+    return wb >= 103 ? wb : -1;
+}
+
 // Core of nndtw_classify (also used per window by nndtw_loocv_window).
 static int classify_impl(const float *q, int64_t nq, const float *t, const float *U,
                          const float *Lo, const nndtw_kim *tkim, int64_t nt, int64_t index_base,
@@ -481,7 +492,10 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         // survivors and rerun with the full window below.
         // (not for the no-bound baseline: every pair is a survivor there, against a loose
         // early best-so-far, and a tenth of them fell back -- 96 -> 195 ms on config 2)
-        const int wb = (dtw_kernel_kind(L, w) == 1 && !alt_none) ? band_adapt_window(L, w) : -1;
+        const int kind = dtw_kernel_kind(L, w);
+        const int wb = alt_none ? -1
+                                : kind == 1 ? band_adapt_window(L, w)
+                                            : kind == 2 ? full_window_band(L, w) : -1;
         bool adapted = false;
         if (wb >= 0) {
             launch_cells_prefix(L, wb, W.cells_prefix2, st);
@@ -617,7 +631,8 @@ const char *nndtw_dtw_kernel_name(int32_t L, int32_t w) {
 int32_t nndtw_band_limited_window(int32_t L, int32_t w) {
     if (L < 2 || w < 0) return -1;
     if (w > L - 1) w = L - 1;
-    return dtw_kernel_kind(L, w) == 1 ? band_adapt_window(L, w) : -1;
+    const int kind = dtw_kernel_kind(L, w);
+    return kind == 1 ? band_adapt_window(L, w) : kind == 2 ? full_window_band(L, w) : -1;
 }
 int64_t nndtw_launch_count(void) { return launches_total(); }
 

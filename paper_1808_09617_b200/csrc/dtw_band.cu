@@ -694,14 +694,16 @@ static int band_adapt_r() {  // experiments: NNDTW_ADAPT_R = 20 / 22 / 26 (defau
     return (r == 20 || r == 22) ? r : 26;
 }
 
-int band_adapt_window(int L, int w) {
+int band_adapt_window(int L, int w, bool full_window) {
     const char *ee = getenv("NNDTW_ADAPT");  // 0 = off; an integer > 1 forces that wb
     const int env = ee ? atoi(ee) : -1;
     if (w > L - 1) w = L - 1;
     if (env == 0 || L % 4 != 0) return -1;
     const int R = band_adapt_r();
-    const char *ef = getenv("NNDTW_ADAPT_FRAC");  // experiments: wb <= w * frac (default 0.5)
-    const double frac = ef ? atof(ef) : 0.5;
+    // experiments: wb <= w * frac (default 0.5; 1/8 in front of the row-strip kernel: config 4
+    // at wb = 207 / 415 / 103: 14.0 k / 12.6 k / 11.3 k queries/s, 11.7 k without the pass)
+    const char *ef = getenv("NNDTW_ADAPT_FRAC");
+    const double frac = ef ? atof(ef) : (full_window ? 0.125 : 0.5);
     int best = -1;
     for (int G = 1; G <= 32; G <<= 1) {
         const int wb = (R / 2) * G - 1;
@@ -916,7 +918,7 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
     }
     return launch_dtw_strip(A, B, items, nitems_dev, item_cap, ia, ib, nitems_host, L, w, mode,
                             key, index_base, eps_t, log, counters, cells_prefix, cutoff, out, st,
-                            num_sms);
+                            num_sms, fbsel ? fb_count : nullptr);
 }
 
 }  // namespace nndtw

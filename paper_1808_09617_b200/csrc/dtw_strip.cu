@@ -45,6 +45,9 @@ struct StripParams {
     int rowlen;  // floats per warp region: (L + 2*PAD) for B, L + 32*KS + 1 for the row
                  // buffer, then ceil(L/32) block suffix minima of the row buffer
     int ks;      // sub-blocks per lane (the template KS; sizes rowlen)
+    // full-window pass after the band-limited one (dtw_band.cu): run the items appended after
+    // the survivors (fb_count of them), or every survivor again if they did not all fit
+    const unsigned long long *fb_count;  // nullable
 };
 
 template <int RR, int KS, bool MASK>
@@ -64,9 +67,17 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     int64_t nitems = p.nitems_host;
+    int64_t ioff = 0;
     if (p.mode == 0) {
         unsigned long long c = *p.nitems_dev;
         nitems = (int64_t)(c < p.item_cap ? c : p.item_cap);
+        if (p.fb_count != nullptr) {
+            const unsigned long long f = *p.fb_count;
+            if (c + f <= p.item_cap) {
+                ioff = (int64_t)c;
+                nitems = (int64_t)f;
+            }
+        }
     }
     // B pads: -2^64*(k+1) before, +2^64*(k+1) after (distinct from the A pad below)
     for (int x = lane; x < STRIP_PAD; x += 32) {
@@ -82,7 +93,7 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
         unsigned a_idx, b_idx;
         float thr_batch = kInf;
         if (p.mode == 0) {
-            Item itm = p.items[it];
+            Item itm = p.items[ioff + it];
             a_idx = itm.q;
             b_idx = itm.n;
             float live = key_dist(ld_relaxed_u64(p.key + a_idx));
@@ -422,8 +433,10 @@ int launch_dtw_strip(const float *A, const float *B, const Item *items,
                      const int32_t *ia, const int32_t *ib, int64_t nitems_host, int L, int w,
                      int mode, unsigned long long *key, int64_t index_base, float eps_t,
                      TieLog log, unsigned long long *counters, const long long *cells_prefix,
-                     const float *cutoff, float *out, cudaStream_t st, int num_sms) {
+                     const float *cutoff, float *out, cudaStream_t st, int num_sms,
+                     const unsigned long long *fb_count) {
     StripParams p;
+    p.fb_count = fb_count;
     p.A = A;
     p.B = B;
     p.items = items;

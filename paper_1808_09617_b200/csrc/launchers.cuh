@@ -104,7 +104,7 @@ int launch_count_errors(const unsigned long long *key, int64_t nq, const int32_t
 // (long windows).  mode 0 = search (items + device count, atomicMin into key, tie log),
 // mode 1 = batch (ia/ib/cutoff/out, nitems_host pairs).  Returns 0 or an NNDTW_E_* code.
 // S4 band-limited pass (dtw_band.cu): its window for a distance window w, or -1
-int band_adapt_window(int L, int w);
+int band_adapt_window(int L, int w, bool full_window = false);
 int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const Item *items,
                  const unsigned long long *nitems_dev, unsigned long long item_cap,
                  const int32_t *ia, const int32_t *ib, int64_t nitems_host, int L, int w,
@@ -133,6 +133,7 @@ int launch_dtw_strip(const float *A, const float *B, const Item *items,
                      const int32_t *ia, const int32_t *ib, int64_t nitems_host, int L, int w,
                      int mode, unsigned long long *key, int64_t index_base, float eps_t,
                      TieLog log, unsigned long long *counters, const long long *cells_prefix,
-                     const float *cutoff, float *out, cudaStream_t st, int num_sms);
+                     const float *cutoff, float *out, cudaStream_t st, int num_sms,
+                     const unsigned long long *fb_count = nullptr);
 
 }  // namespace nndtw

@@ -133,15 +133,24 @@ def test_dtw_kernel_name_rule(lib):
 
 def test_band_limited_window_rule(lib, monkeypatch):
     """nndtw_band_limited_window (host-only): the band of the S4 band-limited pass -- the
-    R = 26 full-warp layout's wb = 13 G - 1 <= w / 2 for band-kernel windows w >= 64, else -1."""
+    R = 26 full-warp layout's wb = 13 G - 1 <= w / 2 for band-kernel windows w >= 64, <= w / 8
+    in front of the row-strip kernel where that is >= 103, else -1."""
     wb = lib.nndtw_band_limited_window
     monkeypatch.delenv("NNDTW_ADAPT", raising=False)
+    monkeypatch.delenv("NNDTW_ADAPT_FULL", raising=False)
     assert wb(512, 103) == 51          # config 2
     assert wb(256, 128) == 51          # config 1, p = 50
     assert wb(300, 210) == 103
     assert wb(256, 52) == -1           # w < 64
-    assert wb(256, 255) == -1          # full window: the row-strip kernel
-    assert wb(2048, 2047) == -1        # config 4
+    # full windows (the row-strip kernel): a band of <= w / 8 offsets, where that is >= 103
+    assert wb(256, 255) == -1          # config 1, p = 100: 25 would be too narrow
+    assert wb(2048, 2047) == 207       # config 4
+    assert wb(1024, 1023) == 103
+    monkeypatch.setenv("NNDTW_ADAPT_FULL", "0")
+    assert wb(2048, 2047) == -1 and wb(512, 103) == 51
+    monkeypatch.setenv("NNDTW_ADAPT_FULL", "1")
+    assert wb(256, 255) == 25
+    monkeypatch.delenv("NNDTW_ADAPT_FULL")
     assert wb(510, 103) == -1          # L % 4 != 0 (the layout's 16-byte rows)
     assert wb(512, 0) == -1 and wb(1, 5) == -1 and wb(16, -1) == -1
     for w in range(64, 400, 7):

@@ -72,15 +72,19 @@ def test_adapt_fallback_items_do_not_fit(dev, monkeypatch):
     assert st2["dtw_fallback"] > 64, st2
 
 
-@pytest.mark.parametrize("shift", [30, 70, 100])
-def test_adapt_warped_neighbours_fall_back_exactly(dev, oracle_lib, shift):
-    """Adversarial for the band edge: every query is a train series shifted by `shift` samples
-    (w = 103, band-limited pass wb = 51), so for shift > 51 its nearest neighbour's warping path
-    leaves the band -- the edge check must send those items to the full window, and every
-    answer must be the fp64 oracle's (exhaustive)."""
+@pytest.mark.parametrize("L,w,shift", [(512, 103, 30), (512, 103, 70), (512, 103, 100),
+                                         (1024, 1023, 60), (1024, 1023, 160), (1024, 1023, 300)])
+def test_adapt_warped_neighbours_fall_back_exactly(dev, oracle_lib, L, w, shift):
+    """Adversarial for the band edge: every query is a train series shifted by `shift` samples,
+    so for shift > wb (w = 103: wb = 51, the band kernel's fallback; the full window at L = 1024:
+    wb = 103, the row-strip kernel's fallback) its nearest neighbour's warping path leaves the
+    band -- the edge check must send those items to the full window, and every answer must be
+    the fp64 oracle's (exhaustive)."""
     from paper_1808_09617_b200 import nndtw
     rng = np.random.default_rng(shift)
-    L, w, ns, nq = 512, 103, 32, 24
+    ns, nq = 32, 24
+    wb_ = nndtw.load().nndtw_band_limited_window(L, w)
+    assert wb_ == (51 if w == 103 else 103)
     walk = np.cumsum(rng.standard_normal((ns, L + 2 * shift + 4)), axis=1)
     # three noisy variants of every source (offsets 0, 1, 2): near-ties the survivor round must
     # evaluate in full, all of them warped by about `shift` against their query
@@ -100,5 +104,5 @@ def test_adapt_warped_neighbours_fall_back_exactly(dev, oracle_lib, shift):
     assert np.array_equal(idx, ridx), (shift, np.nonzero(idx != ridx)[0][:8])
     d = dist.cpu().numpy().astype(np.float64)
     assert np.all(np.abs(d - rdist) <= 1e-5 * rdist + 1e-30)
-    if shift > 51:
+    if shift > wb_:
         assert st["dtw_fallback"] > 0, st
