@@ -478,8 +478,8 @@ def main():
     traffic = ncu_traffic()
     dtw_kernel = lib.nndtw_dtw_kernel_name(L, w).decode()  # the kernel dispatch_dtw runs
     wb = int(lib.nndtw_band_limited_window(L, w))
-    dtw_label = (f"{dtw_kernel} (S4 survivor round: band-limited pass wb={wb} + full-window "
-                 f"pass for the survivors it sends back)" if wb >= 0 else
+    dtw_label = (f"k_dtw_band band-limited pass (wb={wb}) + {dtw_kernel} full-window pass for "
+                 f"the survivors it sends back (S4 survivor round)" if wb >= 0 else
                  f"{dtw_kernel} (S4 survivor round)")
     roof_dtw = {"kernel": dtw_label, "bound": "alu",
                 "achieved": dtw_gcups, "peak": peak_cells, "unit": "Gcells/s",
