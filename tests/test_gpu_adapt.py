@@ -106,3 +106,13 @@ def test_adapt_warped_neighbours_fall_back_exactly(dev, oracle_lib, L, w, shift)
     assert np.all(np.abs(d - rdist) <= 1e-5 * rdist + 1e-30)
     if shift > wb_:
         assert st["dtw_fallback"] > 0, st
+    if shift > wb_ and st["dtw_fallback"] > 1:
+        # no room for the appended items (a capped workspace one pair above the survivors):
+        # the full-window pass (band or row-strip kernel) reruns every survivor -- same answer
+        key2, ws2, st2 = nndtw.classify_keys(model, T(Q_, dev), stats=True,
+                                             max_pairs=st["survivors"] + 1)
+        assert not nndtw.classify_overflowed(model, nq, ws2)
+        idx2, _, dist2 = nndtw.finalize(key2, model.labels)
+        assert np.array_equal(idx2.cpu().numpy(), ridx)
+        assert np.all(np.abs(dist2.cpu().numpy().astype(np.float64) - rdist) <=
+                      1e-5 * rdist + 1e-30)
