@@ -95,7 +95,7 @@ struct ClassifyWs {
     unsigned long long *counters;  // CNT_N + 4 (seed count, item count, log count, overflow)
     unsigned long long *seed_count, *main_count, *log_count;
     unsigned long long *cap_overflow;  // set when a survivor or list count exceeded item_cap
-    unsigned long long *fb_count;      // S4 band-limited pass: items left for the full window
+    unsigned long long *fb_count;      // S4 band-limited passes: items appended per level [2]
     nndtw_kim *qkim;
     unsigned long long *minkey, *f64key, *resolve_out;
     unsigned *overflow;
@@ -111,6 +111,7 @@ struct ClassifyWs {
     unsigned long long log_cap;
     long long *cells_prefix;
     long long *cells_prefix2;  // in-band cells of the band-limited pass's window
+    long long *cells_prefix3;  // ... of the second band-limited pass (full windows)
     float *qU, *qL;  // query envelopes (symmetric bound)
     // two-stage S2 (lb_sparse.cu): per-train-series lists of the queries left after stage A
     long long *col_count, *col_off, *col_fill;
@@ -143,7 +144,7 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L,
         return p;
     };
     const size_t q1 = (size_t)(nq > 0 ? nq : 1);
-    W.counters = (unsigned long long *)take(sizeof(unsigned long long) * (CNT_N + 5));
+    W.counters = (unsigned long long *)take(sizeof(unsigned long long) * (CNT_N + 6));
     W.seed_count = W.counters ? W.counters + CNT_N : nullptr;
     W.main_count = W.counters ? W.counters + CNT_N + 1 : nullptr;
     W.log_count = W.counters ? W.counters + CNT_N + 2 : nullptr;
@@ -170,6 +171,7 @@ static ClassifyWs classify_layout(void *base, int64_t nq, int64_t nt, int L,
     W.log = (TieEntry *)take(sizeof(TieEntry) * (size_t)W.log_cap);
     W.cells_prefix = (long long *)take(sizeof(long long) * (size_t)(2 * L));
     W.cells_prefix2 = (long long *)take(sizeof(long long) * (size_t)(2 * L));
+    W.cells_prefix3 = (long long *)take(sizeof(long long) * (size_t)(2 * L));
     W.qU = (float *)take(sizeof(float) * q1 * (size_t)L);  // symmetric bound: query envelopes
     W.qL = (float *)take(sizeof(float) * q1 * (size_t)L);
     const size_t t1 = (size_t)(nt > 0 ? nt : 1);
@@ -271,6 +273,11 @@ static void exact_local(ClassifyWs &W, const float *q, int64_t nq, const float *
 // on where that band is at least 103 offsets wide (long series: config 4, L = 2048, wb = 207:
 // 11.7 k -> 14.0 k queries/s); at L = 256 (config 1, wb = 25) it was slower (1.03 -> 0.94 M
 // queries/s at w = 255).  NNDTW_ADAPT_FULL=0/1 forces it off/on.
+static bool second_band_level() {  // experiments: NNDTW_ADAPT_LEVELS=2
+    const char *e = getenv("NNDTW_ADAPT_LEVELS");
+    return e && e[0] == '2';
+}
+
 static int full_window_band(int L, int w) {
     const int wb = band_adapt_window(L, w, true);
     const char *e = getenv("NNDTW_ADAPT_FULL");
@@ -368,7 +375,7 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
     tm.mark();  // 0
     if (do_seed) {
         launch_classify_init(nq, key, W.minkey, W.f64key, W.resolve_out, W.overflow, W.tiecnt,
-                             W.counters, CNT_N + 5, W.buckets, st);
+                             W.counters, CNT_N + 6, W.buckets, st);
         launch_cells_prefix(L, w, W.cells_prefix, st);
     }
     tm.mark();  // 1
@@ -496,19 +503,30 @@ static int classify_impl(const float *q, int64_t nq, const float *t, const float
         const int wb = alt_none ? -1
                                 : kind == 1 ? band_adapt_window(L, w)
                                             : kind == 2 ? full_window_band(L, w) : -1;
-        bool adapted = false;
+        int levels = 0;
         if (wb >= 0) {
             launch_cells_prefix(L, wb, W.cells_prefix2, st);
-            cudaMemsetAsync(W.fb_count, 0, sizeof(unsigned long long), st);
-            adapted = dispatch_dtw(q, t, nq, nt, W.items, W.main_count, W.item_cap, nullptr,
-                                   nullptr, 0, L, w, 0, key, index_base, eps_t, log, cnt,
-                                   W.cells_prefix2, nullptr, nullptr, st, sms, W.apad,
-                                   W.apad_cap, wb, W.items, W.fb_count, 0) == 0;
+            cudaMemsetAsync(W.fb_count, 0, 2 * sizeof(unsigned long long), st);
+            if (dispatch_dtw(q, t, nq, nt, W.items, W.main_count, W.item_cap, nullptr, nullptr, 0,
+                             L, w, 0, key, index_base, eps_t, log, cnt, W.cells_prefix2, nullptr,
+                             nullptr, st, sms, W.apad, W.apad_cap, wb, W.items, W.fb_count,
+                             0) == 0)
+                levels = 1;
+            // full windows: a second band, twice as wide, for the items the first sends back
+            const int wb2 = 2 * wb + 1;
+            if (levels == 1 && kind == 2 && second_band_level() && wb2 < w) {
+                launch_cells_prefix(L, wb2, W.cells_prefix3, st);
+                if (dispatch_dtw(q, t, nq, nt, W.items, W.main_count, W.item_cap, nullptr,
+                                 nullptr, 0, L, w, 0, key, index_base, eps_t, log, cnt,
+                                 W.cells_prefix3, nullptr, nullptr, st, sms, W.apad, W.apad_cap,
+                                 wb2, W.items, W.fb_count, 1) == 0)
+                    levels = 2;
+            }
         }
         rc = dispatch_dtw(q, t, nq, nt, W.items, W.main_count, W.item_cap, nullptr, nullptr, 0, L, w, 0,
                           key, index_base, eps_t, log, cnt, W.cells_prefix, nullptr, nullptr,
                           st, sms, W.apad, W.apad_cap, -1, nullptr,
-                          adapted ? W.fb_count : nullptr, adapted ? 1 : 0);
+                          levels ? W.fb_count : nullptr, levels);
         if ((rc = dtw_fail(rc, L, w))) return rc;
     } else if (nt > 0 && dtw_a) {
         // the survivors of buckets < split_b: items [0, base[split_b]) (the bucket-major list)

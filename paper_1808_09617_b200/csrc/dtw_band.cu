@@ -50,8 +50,8 @@ struct BandParams {
     int64_t apad_cap;                     // floats available at apad_ws
     // Band-limited pass (ADAPT, search mode): the layout's window w is narrower than the
     // distance's; an item whose band-edge cells come within the threshold is appended to the
-    // item array after the survivors (fb_items[*nitems_dev + k], k = atomicAdd(fb_count)) for
-    // the full-window pass.  fbsel (full-window pass): run those appended items -- or, if they
+    // item array after the items it reads (level fbsel appends at fb_count[fbsel]) for the next
+    // pass.  fbsel >= 1: run the items level fbsel - 1 appended -- or, if they
     // did not all fit below item_cap, every survivor again.
     Item *fb_items;
     unsigned long long *fb_count;
@@ -137,12 +137,16 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
     if (p.mode == 0) {
         unsigned long long c = *p.nitems_dev;
         nitems = (int64_t)(c < p.item_cap ? c : p.item_cap);
-        if (p.fbsel) {
-            const unsigned long long f = *p.fb_count;
-            if (c + f <= p.item_cap) {
-                ioff = (int64_t)c;
-                nitems = (int64_t)f;
-            }  // else: not all were stored -- every survivor again (exact, slower)
+        if (p.fbsel) {  // level fbsel: the items level fbsel - 1 appended
+            const unsigned long long f0 = p.fb_count[0];
+            const unsigned long long off = c + (p.fbsel >= 2 ? f0 : 0ull);
+            const unsigned long long n = p.fb_count[p.fbsel - 1];
+            if (off + n <= p.item_cap) {
+                ioff = (int64_t)off;
+                nitems = (int64_t)n;
+            } else if (ADAPT) {
+                nitems = 0;  // not all were stored: the last, full-window pass reruns everything
+            }  // else: every survivor again (exact, slower)
         }
     }
     int64_t it = gid;
@@ -375,8 +379,8 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
 #endif
         if (__any_sync(0xffffffffu, done || abandon || fired)) {  // rare: once per item per group
             if (ADAPT && fired && g == 0) {
-                const unsigned long long k = atomicAdd(p.fb_count, 1ull);
-                const unsigned long long pos = (unsigned long long)nitems + k;
+                const unsigned long long k = atomicAdd(p.fb_count + p.fbsel, 1ull);
+                const unsigned long long pos = (unsigned long long)(ioff + nitems) + k;
                 if (pos < p.item_cap) p.fb_items[pos] = Item{qcur, ncur, p.items[ioff + it].lb};
                 if (p.counters != nullptr) {
                     atomicAdd(p.counters + CNT_FALLBACK, 1ull);
@@ -918,7 +922,7 @@ int dispatch_dtw(const float *A, const float *B, int64_t na, int64_t nb, const I
     }
     return launch_dtw_strip(A, B, items, nitems_dev, item_cap, ia, ib, nitems_host, L, w, mode,
                             key, index_base, eps_t, log, counters, cells_prefix, cutoff, out, st,
-                            num_sms, fbsel ? fb_count : nullptr);
+                            num_sms, fbsel ? fb_count : nullptr, fbsel);
 }
 
 }  // namespace nndtw

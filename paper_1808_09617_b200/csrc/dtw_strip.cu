@@ -47,7 +47,8 @@ struct StripParams {
     int ks;      // sub-blocks per lane (the template KS; sizes rowlen)
     // full-window pass after the band-limited one (dtw_band.cu): run the items appended after
     // the survivors (fb_count of them), or every survivor again if they did not all fit
-    const unsigned long long *fb_count;  // nullable
+    const unsigned long long *fb_count;  // nullable: the band-limited passes' append counts
+    int fbsel;                           // which level's appended items to run (>= 1)
 };
 
 template <int RR, int KS, bool MASK>
@@ -71,12 +72,14 @@ __global__ void __launch_bounds__(128) k_dtw_strip(StripParams p) {
     if (p.mode == 0) {
         unsigned long long c = *p.nitems_dev;
         nitems = (int64_t)(c < p.item_cap ? c : p.item_cap);
-        if (p.fb_count != nullptr) {
-            const unsigned long long f = *p.fb_count;
-            if (c + f <= p.item_cap) {
-                ioff = (int64_t)c;
-                nitems = (int64_t)f;
-            }
+        if (p.fb_count != nullptr && p.fbsel >= 1) {  // the items level fbsel - 1 appended
+            const unsigned long long f0 = p.fb_count[0];
+            const unsigned long long off = c + (p.fbsel >= 2 ? f0 : 0ull);
+            const unsigned long long n = p.fb_count[p.fbsel - 1];
+            if (off + n <= p.item_cap) {
+                ioff = (int64_t)off;
+                nitems = (int64_t)n;
+            }  // else: every survivor again
         }
     }
     // B pads: -2^64*(k+1) before, +2^64*(k+1) after (distinct from the A pad below)
@@ -434,9 +437,10 @@ int launch_dtw_strip(const float *A, const float *B, const Item *items,
                      int mode, unsigned long long *key, int64_t index_base, float eps_t,
                      TieLog log, unsigned long long *counters, const long long *cells_prefix,
                      const float *cutoff, float *out, cudaStream_t st, int num_sms,
-                     const unsigned long long *fb_count) {
+                     const unsigned long long *fb_count, int fbsel) {
     StripParams p;
     p.fb_count = fb_count;
+    p.fbsel = fbsel;
     p.A = A;
     p.B = B;
     p.items = items;

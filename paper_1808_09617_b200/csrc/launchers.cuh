@@ -134,6 +134,6 @@ int launch_dtw_strip(const float *A, const float *B, const Item *items,
                      int mode, unsigned long long *key, int64_t index_base, float eps_t,
                      TieLog log, unsigned long long *counters, const long long *cells_prefix,
                      const float *cutoff, float *out, cudaStream_t st, int num_sms,
-                     const unsigned long long *fb_count = nullptr);
+                     const unsigned long long *fb_count = nullptr, int fbsel = 0);
 
 }  // namespace nndtw
