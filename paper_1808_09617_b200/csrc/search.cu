@@ -442,6 +442,98 @@ __device__ double dtw64_warp(const float *__restrict__ a, const float *__restric
     return __shfl_sync(0xffffffffu, result, owner);
 }
 
+// The same fp64 DTW by a CTA of nstrips = ceil(L / (32 RR64)) warps, warp k on strip k (rows
+// 256k .. 256k+255), pipelined: warp k reads the row above its strip from rows[k] as warp k-1
+// writes it (lane 31, column by column; published every 32 columns through prog[k], a
+// shared-memory counter behind a block fence), and writes its own bottom row to rows[k+1].
+// The cells and their operations are dtw64_warp's (bit-identical results); long series no
+// longer run on one warp alone: config 4's 16 near-tie pairs (L = 2048) took 8 ms on 16 warps.
+// rows: (nstrips + 1) x (L + 1) doubles; prog: nstrips ints; every thread gets the result.
+__device__ double dtw64_cta(const float *__restrict__ a, const float *__restrict__ b, int L,
+                            int w, double *rows, volatile int *prog, double *res) {
+    const int lane = threadIdx.x & 31;
+    const int k = threadIdx.x >> 5;           // strip
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    const int H = 32 * RR64;
+    const int nstrips = (L + H - 1) / H;
+    const int ld = L + 1;
+    if (k == 0) {  // rows[0]: D(-1, j) = +inf, D(-1, -1) = 0
+        for (int j = lane; j < L; j += 32) rows[1 + j] = INF;
+        if (lane == 0) rows[0] = 0.0;
+    }
+    if (lane == 0) {
+        prog[k] = (k == 0) ? L : 0;            // strip 0's row above is complete
+        rows[(size_t)(k + 1) * ld] = INF;      // D(row above, -1) of strip k+1
+    }
+    __syncthreads();
+    const double *above = rows + (size_t)k * ld;
+    double *below = rows + (size_t)(k + 1) * ld;
+    const int i0 = k * H + lane * RR64;
+    double av[RR64], Dl[RR64];
+#pragma unroll
+    for (int r = 0; r < RR64; ++r) {
+        av[r] = (i0 + r < L) ? (double)a[i0 + r] : 0.0;
+        Dl[r] = INF;
+    }
+    double up_prev = (lane == 0) ? above[0] : INF;
+    double bot = INF;
+    double result = INF;
+    int ready = 0;  // lane 0: columns of the row above known to be written
+    for (int s = 0; s < L + 31; ++s) {
+        const int j = s - lane;
+        if (lane == 0 && j < L && j >= ready) {  // wait for warp k-1's next 32 columns
+            const int need = (j + 32 < L) ? j + 32 : L;
+            while (prog[k] < need) {
+            }
+            ready = need;
+            __threadfence_block();
+        }
+        __syncwarp();
+        const double from_up = __shfl_up_sync(0xffffffffu, bot, 1);
+        const bool jin = j >= 0 && j < L;
+        const double bj = jin ? (double)b[j] : 0.0;
+        const double rbv = (lane == 0 && jin) ? above[1 + j] : INF;
+        const double up = (lane == 0) ? rbv : from_up;
+        double dgv = up_prev, upv = up;
+#pragma unroll
+        for (int r = 0; r < RR64; ++r) {
+            const int i = i0 + r;
+            const double old = Dl[r];
+            double nv = INF;
+            if (jin && i < L && i - j <= w && j - i <= w) {
+                const double dd = __dsub_rn(av[r], bj);
+                const double delta = __dmul_rn(dd, dd);
+                const double m = (i == 0 && j == 0) ? 0.0 : fmin(fmin(dgv, old), upv);
+                nv = __dadd_rn(delta, m);
+            }
+            if (jin) Dl[r] = nv;
+            dgv = old;
+            upv = jin ? nv : INF;
+        }
+        up_prev = up;
+        bot = jin ? Dl[RR64 - 1] : INF;
+        if (lane == 31 && jin) {
+            below[1 + j] = bot;
+            if (k + 1 < nstrips && ((j & 31) == 31 || j == L - 1)) {
+                __threadfence_block();
+                prog[k + 1] = j + 1;
+            }
+        }
+        if (j == L - 1 && L - 1 >= i0 && L - 1 < i0 + RR64) {
+#pragma unroll
+            for (int r = 0; r < RR64; ++r)
+                if (i0 + r == L - 1) result = Dl[r];
+        }
+    }
+    const int owner = (L - 1) / H;  // the strip holding row L-1
+    const int olane = ((L - 1) % H) / RR64;
+    if (k == owner && lane == olane) *res = result;
+    __syncthreads();
+    const double out = *res;
+    __syncthreads();  // (rows / prog / res are reused by the next pair)
+    return out;
+}
+
 // Near-tie set sizes (single-shard EXACT mode): a query whose band holds one candidate needs no
 // fp64 re-rank -- that candidate is the unique minimum.
 __global__ void k_tie_count(const TieEntry *e, const unsigned long long *count,
@@ -501,6 +593,43 @@ __global__ void k_refine(TieEntry *e, const unsigned long long *count, unsigned 
     }
 }
 
+// k_refine with one CTA per entry (dtw64_cta): blockDim = 32 * nstrips
+__global__ void k_refine_cta(TieEntry *e, const unsigned long long *count, unsigned long long cap,
+                             const float *__restrict__ A, const float *__restrict__ B, int L,
+                             int w, const unsigned long long *__restrict__ gkey, float eps_t,
+                             unsigned long long *f64key, unsigned long long *counters,
+                             const unsigned *tiecnt, const unsigned *overflow) {
+    extern __shared__ double dsh[];
+    const int nstrips = blockDim.x >> 5;
+    double *rows = dsh;
+    double *res = dsh + (size_t)(nstrips + 1) * (L + 1);
+    volatile int *prog = (volatile int *)(res + 1);
+    unsigned long long n = *count;
+    if (n > cap) n = cap;
+    for (unsigned long long x = blockIdx.x; x < n; x += gridDim.x) {
+        TieEntry t = e[x];
+        const float gb = key_dist(gkey[t.q]);
+        if (t.d32 <= gb * (1.0f + eps_t)) {
+            if (tiecnt != nullptr && tiecnt[t.q] == 1u && !overflow[t.q]) {
+                if (threadIdx.x == 0) {  // singleton band: the candidate is the answer
+                    e[x].d64 = 0.0;
+                    atomicMin(f64key + t.q, 0ull);
+                }
+                continue;
+            }
+            const double d = dtw64_cta(A + (int64_t)t.q * L, B + (int64_t)t.n * L, L, w, rows,
+                                       prog, res);
+            if (threadIdx.x == 0) {
+                e[x].d64 = d;
+                atomicMin(f64key + t.q, (unsigned long long)__double_as_longlong(d));
+                if (counters) atomicAdd(counters + CNT_TIES, 1ull);
+            }
+        } else if (threadIdx.x == 0) {
+            e[x].d64 = -1.0;
+        }
+    }
+}
+
 // Overflowed queries (the tie log dropped an entry): every pair that survived the cascade at
 // the global best is re-ranked in fp64 (rare, slow, exact).  pass 0: min fp64 -> f64key;
 // pass 1: lowest index with fp64 == gf64 -> out.
@@ -550,6 +679,24 @@ int launch_refine(TieEntry *e, const unsigned long long *count, unsigned long lo
                   const unsigned *tiecnt, const unsigned *overflow, int num_sms,
                   cudaStream_t st) {
     if (w > L - 1) w = L - 1;
+    // a CTA of one warp per 256-row strip per entry where its row buffers fit (L <= 2048-ish):
+    // long series in parallel over their strips; else (or NNDTW_REFINE_CTA=0) one warp per entry
+    const int nstrips = (L + 32 * RR64 - 1) / (32 * RR64);
+    const size_t csmem = (size_t)(nstrips + 1) * (L + 1) * sizeof(double) + sizeof(double) +
+                         (size_t)nstrips * sizeof(int);
+    static const bool cta_on = [] {
+        const char *e = getenv("NNDTW_REFINE_CTA");
+        return !(e && e[0] == '0');
+    }();
+    if (cta_on && nstrips >= 2 && nstrips <= 16 && csmem <= 200 * 1024) {
+        cudaFuncSetAttribute(k_refine_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)csmem);
+        k_refine_cta<<<num_sms * 2, 32 * nstrips, csmem, st>>>(e, count, cap, A, B, L, w, gkey,
+                                                                eps_t, f64key, counters, tiecnt,
+                                                                overflow);
+        count_launch(1, __func__);
+        return 0;
+    }
     size_t smem;
     int block = refine_block(L, &smem);
     cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -216,9 +216,13 @@ def test_classify_config1_grid(dev, oracle_lib, p):
 
 @pytest.mark.parametrize("kind,L,w,V", [("int", 8, 2, 3), ("int", 16, 0, 5), ("int", 33, 32, 4),
                                         ("walk", 2, 0, 1), ("walk", 3, 1, 5), ("const", 12, 3, 2),
-                                        ("walk", 130, 129, 70), ("int", 64, 5, 1)])
+                                        ("walk", 130, 129, 70), ("int", 64, 5, 1),
+                                        ("int", 300, 40, 5), ("walk", 600, 599, 5),
+                                        ("walk", 1024, 200, 5)])
 def test_classify_ties_and_edges(dev, oracle_lib, kind, L, w, V):
-    """Exact ties (integer grids, duplicates, constants): the lowest train index must win."""
+    """Exact ties (integer grids, duplicates, constants): the lowest train index must win.
+    (L > 256: the fp64 re-rank of the near-tie sets runs one warp per 256-row strip,
+    k_refine_cta; the full window at L = 600 also goes through the row-strip kernel.)"""
     rng = np.random.default_rng(L * 31 + w)
     Tr = datagen.random_series(rng, 257, L, kind)
     Tr[200:210] = Tr[17]          # duplicates after the original
