@@ -351,7 +351,11 @@ __global__ void __launch_bounds__(256, band_min_blocks<R, KM>()) k_dtw_band(Band
         float lmin = D[0];
 #pragma unroll
         for (int r = 1; r < R; ++r) lmin = fminf(lmin, D[r]);
-        float thr = p.mode == 0 ? key_dist(kprev) * (1.0f + p.eps_t) : thr_batch;
+        // (the freshest observed best-so-far: the key loaded at this period's start, when this
+        // group's item was already running then -- keys only decrease)
+        const unsigned long long kuse = (p.mode == 0 && active && knext != 0ull && knext < kprev)
+                                            ? knext : kprev;
+        float thr = p.mode == 0 ? key_dist(kuse) * (1.0f + p.eps_t) : thr_batch;
         kprev = knext;
         bool vote = !(lmin <= thr);
         unsigned ballot = __ballot_sync(0xffffffffu, vote);
