@@ -115,9 +115,9 @@ def main():
                  "MIN all-reduces between phases synchronise the ranks; their tens of "
                  "microseconds on NVLink are not included).  Exchange 'own': every shard prunes "
                  "against its own seed; 'seed': against the MIN over shards of the seed keys "
-                 "(NNDTW_CLASSIFY_PHASE_SEED / _SEARCH); 'split': in addition the survivor round "
-                 "runs in two halves with another MIN between them (PHASE_SEARCH_A / _B, the "
-                 "default of dist.py).\n",
+                 "(NNDTW_CLASSIFY_PHASE_SEED / _SEARCH; dist.py's default, split=False); 'split': "
+                 "in addition the survivor round runs in two halves with another MIN between "
+                 "them (PHASE_SEARCH_A / _B; dist.py with split=True).\n",
                  "| GPUs | exchange | step ms (phases) | projected queries/s | "
                  "projected efficiency | DTW cells (all shards) | DTW calls |",
                  "|---|---|---|---|---|---|---|"]
