@@ -134,3 +134,20 @@ def test_classify_query_blocking(dev, oracle_lib):
     assert pred.stats["lb_pairs"] == 100 * 100
     _check_nn(oracle_lib, ds.train, ds.train_labels, ds.test, w, pred.idx.cpu().numpy(),
               pred.label.cpu().numpy(), pred.dist.cpu().numpy())
+
+
+def test_loocv_degenerate_sizes(dev, oracle_lib):
+    """LOOCV with n = 1 (the held-out series is never its own neighbour: index -1, an error,
+    reading C17) and n = 2, through the ABI against the oracle, including a constant pair
+    (DTW = 0 between the two)."""
+    import torch
+    from paper_1808_09617_b200 import nndtw
+    rng = np.random.default_rng(22)
+    wins = [0, 4, 15]
+    for X in (datagen.random_series(rng, 2, 16, "walk"), np.ones((2, 16), np.float32)):
+        for n, lab in ((1, [3]), (2, [3, 4]), (2, [3, 3])):
+            lab = np.array(lab, np.int32)
+            err, nn, _ = nndtw.loocv_window(T(X[:n], dev), T(lab, dev), wins, v=5, with_nn=True)
+            rerr, rnn = oracle_lib.loocv(X[:n], lab, wins, V=5, mode="pruned")
+            assert (err.cpu().numpy() == rerr).all()
+            assert (nn.cpu().numpy() == rnn).all()

@@ -486,3 +486,17 @@ def test_enhanced_improved_admissible_and_dominant(oracle_lib):
             d = o.dtw(X[i], X[i + 20], w)
             for V in (1, 3, 5, 16):
                 assert o.lb_enhanced_improved(X[i], X[i + 20], w, V) <= d * (1 + 1e-12)
+
+
+def test_loocv_degenerate_sizes(oracle_lib):
+    # reading C17: with one series there is no other candidate (index -1, counted as an error);
+    # with two, each is the other's neighbour whatever the window
+    rng = np.random.default_rng(21)
+    X = datagen.random_series(rng, 2, 16, "walk")
+    for mode in ("exhaustive", "pruned"):
+        err, nn = oracle_lib.loocv(X[:1], np.array([3], np.int32), [0, 4, 15], mode=mode)
+        assert (nn == -1).all() and (err == 1).all()
+        err, nn = oracle_lib.loocv(X, np.array([3, 4], np.int32), [0, 4, 15], mode=mode)
+        assert (nn == [[1, 0]] * 3).all() and (err == 2).all()
+        err, nn = oracle_lib.loocv(X, np.array([3, 3], np.int32), [0, 4, 15], mode=mode)
+        assert (nn == [[1, 0]] * 3).all() and (err == 0).all()
